@@ -1,0 +1,175 @@
+/*
+ * kcache_c.h -- C ABI of the B200-native KCache decode-attention library
+ * (libkcache_b200.so). Plain pointers and sizes only; no torch or C++ types.
+ *
+ * This is the drop-in boundary for the reference's decode-step TopN attention
+ * operator (arXiv 2404.18057 reference, /root/reference/proj). The reference
+ * has no FFI of its own: its operator API is the C++ header surface of
+ * kcache_core (proj/core/include/kcache/{attention,kv_cache}.hpp). The C++
+ * headers under include/kcache/ re-declare that surface source-compatibly and
+ * are implemented on top of the functions below (see INTEGRATION.md for the
+ * ctypes / C++ bindings a maintainer adds on the reference side).
+ *
+ * Storage:
+ *   K   HBM            [layer][batch][kv_head][max_seq][head_dim]   fp16/bf16/fp32
+ *   V   layers <  L    HBM, same layout
+ *   V   layers >= L    pinned, device-mapped host memory, same layout
+ * Every function returns KC_OK or an error code; kc_last_error() returns a
+ * thread-local message. A cache handle is single-owner and not thread-safe,
+ * like TieredKVCache.
+ */
+#ifndef KCACHE_C_H
+#define KCACHE_C_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes. The C++ shim rethrows them as the reference's exceptions
+ * (proj/core/include/kcache/errors.hpp:10-38): */
+#define KC_OK 0
+#define KC_ESHAPE 1     /* kcache::ShapeError            */
+#define KC_ESTATE 2     /* kcache::StateError            */
+#define KC_ECAPACITY 3  /* kcache::CapacityError         */
+#define KC_EARG 4       /* std::invalid_argument         */
+#define KC_ERANGE 5     /* std::out_of_range             */
+#define KC_ECUDA 6      /* std::runtime_error (CUDA)     */
+#define KC_EOVERFLOW 7  /* std::overflow_error (checked_mul, checked.hpp:10-20) */
+
+/* Element types for storage and for q inputs. */
+#define KC_F32 0
+#define KC_F16 1
+#define KC_BF16 2
+
+/* kc_decode_* flags. */
+#define KC_RENORMALIZE 1u    /* renormalize=true (attention.cpp:167-174)            */
+#define KC_REVERSE_ACCUM 2u  /* ordered_accumulation=false fault hook (:180-186)    */
+#define KC_IO_DEVICE 4u      /* q and every output pointer are device pointers;
+                                the call is asynchronous on `stream`. Otherwise
+                                host pointers and the call returns finished.     */
+
+/* Ledger directions / phases (kv_cache.hpp:14-29). */
+#define KC_D2H 0
+#define KC_H2D 1
+#define KC_PREFILL 0
+#define KC_DECODE 1
+
+/* ModelConfig's attention shape (proj/core/include/kcache/model.hpp:18-40).
+ * n_kv_heads == n_heads is the reference's MHA; n_heads = G*n_kv_heads is
+ * GQA (a B200-side extension). */
+typedef struct kc_config {
+  uint64_t n_layers;
+  uint64_t d_model; /* n_heads * head_dim */
+  uint64_t n_heads;
+  uint64_t n_kv_heads;
+  uint64_t head_dim;
+  uint64_t max_seq;
+} kc_config;
+
+typedef struct kc_cache kc_cache;
+
+/* Result of one decode_attention_topn call (attention.hpp:20-30,48-52).
+ * slot = b*n_heads + head; nc = min(top_n, len). Optional outputs may be NULL. */
+typedef struct kc_topn_out {
+  float* out;            /* [batch][n_heads*head_dim]                  */
+  uint32_t* indices;     /* [batch*n_heads][nc], ascending per slot    */
+  float* weights;        /* [batch*n_heads][nc], raw softmax values     */
+  double* dropped_mass;  /* [batch*n_heads], 1 - sum(double(weights))  */
+  uint64_t nc;           /* written: entries per slot                  */
+  uint64_t h2d_bytes;    /* written: ledger H2D bytes of this call     */
+} kc_topn_out;
+
+const char* kc_last_error(void);
+const char* kc_version(void);
+
+/* TieredKVCache(config, batch, TierPlacement{resident_layers, n_layers,
+ * bytes_per_element}, fast_capacity) -- kv_cache.hpp:100-102,
+ * kv_cache.cpp:68-81. bytes_per_element is ledger accounting (as in the
+ * reference); storage_dtype is the physical element type. device = CUDA
+ * ordinal; numa_node < 0 = no binding of the pinned V arena. */
+int kc_cache_create(const kc_config* config, uint64_t batch, uint64_t resident_layers,
+                    uint64_t bytes_per_element, int storage_dtype, int has_fast_capacity,
+                    uint64_t fast_capacity_bytes, int device, int numa_node, kc_cache** out);
+int kc_cache_destroy(kc_cache* cache);
+
+/* append_kv (kv_cache.hpp:106, kv_cache.cpp:96-121). k, v: host fp32
+ * [rows][n_kv_heads*head_dim], position-major (all batch rows of a position
+ * together); rows a positive multiple of batch. Converted on device. */
+int kc_append_kv(kc_cache* cache, uint64_t layer, const float* k, const float* v, uint64_t rows);
+/* Same, from device buffers of `dtype`, asynchronous on `stream`. */
+int kc_append_kv_device(kc_cache* cache, uint64_t layer, const void* k, const void* v, int dtype,
+                        uint64_t rows, void* stream);
+
+/* offload_prefill_v / begin_decode (kv_cache.cpp:123-148). */
+int kc_offload_prefill_v(kc_cache* cache, uint64_t layer);
+int kc_begin_decode(kc_cache* cache);
+
+/* decode_attention_topn (attention.hpp:64-67, attention.cpp:116-190).
+ * q: [batch][n_heads*head_dim] of q_dtype. */
+int kc_decode_topn(kc_cache* cache, uint64_t layer, const void* q, int q_dtype, uint64_t top_n,
+                   uint32_t flags, kc_topn_out* out, void* stream);
+
+/* n independent decode_attention_topn calls (one q per layer), pipelined:
+ * the V recall + P.V of layers[i] overlaps the scoring of layers[i+1]. This is
+ * the attention-only step the bench times; results equal n single calls. */
+int kc_decode_topn_layers(kc_cache* cache, uint64_t n, const uint64_t* layers,
+                          const void* const* q, int q_dtype, uint64_t top_n, uint32_t flags,
+                          kc_topn_out* outs, void* stream);
+
+/* decode_attention_full (attention.hpp:45-46, attention.cpp:91-114):
+ * softmax over every position, V read from whichever tier holds it, nothing
+ * ledgered. */
+int kc_decode_full(kc_cache* cache, uint64_t layer, const void* q, int q_dtype, uint32_t flags,
+                   float* out, void* stream);
+
+/* Full softmax rows of every (batch, q head) -- the ScoreObserver debug path
+ * (attention.hpp:34-35, attention.cpp:137-139): probs [batch*n_heads][len]
+ * fp32, host. Not on the hot path. */
+int kc_score_probs(kc_cache* cache, uint64_t layer, const void* q, int q_dtype, float* probs);
+
+/* gather_v (kv_cache.hpp:121, kv_cache.cpp:150-187): counts[batch*n_heads],
+ * indices concatenated per slot; out [sum(counts)][head_dim] fp32 (host). */
+int kc_gather_v(kc_cache* cache, uint64_t layer, const uint32_t* indices, const uint64_t* counts,
+                float* out, uint64_t* h2d_bytes);
+
+/* k_row / v_row (kv_cache.hpp:123-124): one position of one batch row,
+ * [n_kv_heads*head_dim] fp32 into host `out`. which: 0 = K, 1 = V. */
+int kc_read_row(kc_cache* cache, uint64_t layer, uint64_t pos, uint64_t batch_idx, int which,
+                float* out);
+
+/* Accessors (kv_cache.hpp:126-136). */
+int kc_current_len(const kc_cache* cache, uint64_t* len);
+int kc_phase(const kc_cache* cache, int* phase);
+int kc_fast_bytes_used(const kc_cache* cache, uint64_t* bytes);
+int kc_slow_bytes_used(const kc_cache* cache, uint64_t* bytes);
+int kc_d2h_bytes_total(const kc_cache* cache, uint64_t* bytes);
+int kc_h2d_bytes_total(const kc_cache* cache, uint64_t* bytes);
+int kc_ledger_size(const kc_cache* cache, uint64_t* n);
+int kc_ledger_event(const kc_cache* cache, uint64_t i, int* phase, uint64_t* layer, int* dir,
+                    uint64_t* bytes, uint64_t* elements);
+/* Device pointers of one layer's K and V storage (V may be a mapped host
+ * pointer) and the element strides; for tests and tooling. */
+int kc_layer_storage(const kc_cache* cache, uint64_t layer, void** k, void** v, int* v_on_host);
+/* Wait for all work the cache enqueued. */
+int kc_sync(kc_cache* cache);
+/* Tuning knobs ("score_chunk", "recall_ctas", ...); DESIGN.md lists them. */
+int kc_set_tuning(kc_cache* cache, const char* key, int64_t value);
+
+/* arg_topk (matrix.hpp:49-52, matrix.cpp:109-122) on the GPU: indices of the
+ * k largest of n host floats, ties to the lowest index, ascending. */
+int kc_arg_topk(const float* values, uint64_t n, uint64_t k, uint32_t* out, uint64_t* count);
+
+/* Synthetic input generator: elements [offset, offset+n) of SeededRng(seed)
+ * .next_uniform(lo, hi) (rng.hpp:13-26), rounded to dtype, written to the
+ * device buffer dst. Counter-based, so any slice is reproducible. */
+int kc_fill_uniform(void* dst, int dtype, uint64_t n, uint64_t seed, uint64_t offset, float lo,
+                    float hi, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* KCACHE_C_H */

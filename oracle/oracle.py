@@ -208,6 +208,7 @@ class Reference:
         lib.kcref_arg_topk.restype = _c.c_long
         lib.kcref_arg_topk.argtypes = [_fp, _sz, _sz, _u32p]
         lib.kcref_softmax.argtypes = [_fp, _sz]
+        lib.kcref_rng_uniform.argtypes = [_c.c_uint64, _sz, _c.c_float, _c.c_float, _fp]
         lib.kcref_bench_create.restype = _c.c_void_p
         lib.kcref_bench_create.argtypes = [_sz] * 6 + [_c.c_int, _c.c_uint, _c.c_uint64, _c.c_uint64, _c.c_uint64]
         lib.kcref_bench_run.restype = _c.c_double
@@ -258,6 +259,11 @@ class Reference:
         r = np.array(row, dtype=np.float32)
         self.lib.kcref_softmax(_f(r), len(r))
         return r
+
+    def rng_uniform(self, seed, n, lo=-1.0, hi=1.0):
+        out = np.zeros(n, np.float32)
+        self.lib.kcref_rng_uniform(seed, n, lo, hi, _f(out))
+        return out
 
 
 class ReferenceBench:

@@ -27,6 +27,7 @@
 #include "kcache/kv_cache.hpp"
 #include "kcache/matrix.hpp"
 #include "kcache/model.hpp"
+#include "kcache/rng.hpp"
 
 using namespace kcache;
 
@@ -162,6 +163,13 @@ long kcref_arg_topk(const float* values, std::size_t n, std::size_t k, uint32_t*
 }
 
 void kcref_softmax(float* row, std::size_t n) { softmax_inplace({row, n}); }
+
+// The first n draws of SeededRng(seed).next_uniform(lo, hi) (rng.hpp:22-26):
+// pins the counter-indexed generators of the oracle and the GPU.
+void kcref_rng_uniform(uint64_t seed, std::size_t n, float lo, float hi, float* out) {
+  SeededRng rng(seed);
+  for (std::size_t i = 0; i < n; ++i) out[i] = rng.next_uniform(lo, hi);
+}
 
 // ---------------------------------------------------------------------------
 // Timed CPU baseline: the reference decode_attention_topn over a sample of the

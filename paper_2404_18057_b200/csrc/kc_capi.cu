@@ -1,0 +1,875 @@
+// kc_capi.cu -- the C ABI (include/kcache_c.h): the tiered store, its ledger
+// and phase machine, and the decode-step orchestration over the sm_100a
+// kernels.
+//
+// Store semantics follow TieredKVCache (proj/core/src/kv_cache.cpp:68-235):
+// byte counters, ledger events and errors are the reference's, but storage is
+// physical: K in HBM, V of layers >= L in pinned device-mapped host memory
+// (from the first append -- the "fast tier" of a not-yet-offloaded layer is a
+// ledger state, the bytes already live in the host arena), V of layers < L in
+// HBM. Layout [layer][b][kv_head][max_seq][h] so one (b, kv head) row of K is
+// a contiguous run the scoring kernel can stream with TMA bulk copies.
+#include <sys/mman.h>
+#include <sys/syscall.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <cmath>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "kc_kernels.cuh"
+#include "kcache_c.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+struct KcError {
+  int code;
+  std::string msg;
+};
+
+[[noreturn]] void fail(int code, const std::string& msg) { throw KcError{code, msg}; }
+
+#define CK(x)                                                                              \
+  do {                                                                                     \
+    cudaError_t e_ = (x);                                                                  \
+    if (e_ != cudaSuccess)                                                                 \
+      fail(KC_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_));                     \
+  } while (0)
+
+uint64_t checked_mul(std::initializer_list<uint64_t> f) {
+  unsigned __int128 acc = 1;
+  for (uint64_t x : f) {
+    acc *= x;
+    if (acc > (unsigned __int128)UINT64_MAX) fail(KC_EOVERFLOW, "checked_mul: product exceeds 64 bits");
+  }
+  return (uint64_t)acc;
+}
+
+size_t dtype_size(int dt) {
+  switch (dt) {
+    case KC_F32: return 4;
+    case KC_F16:
+    case KC_BF16: return 2;
+    default: fail(KC_EARG, "unknown dtype " + std::to_string(dt));
+  }
+}
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  void ensure(size_t n) {
+    if (n <= bytes) return;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    CK(cudaMalloc(&p, std::max<size_t>(n, 256)));
+    bytes = std::max<size_t>(n, 256);
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  template <typename T>
+  T* as() const { return static_cast<T*>(p); }
+};
+
+struct PinnedBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  void ensure(size_t n) {
+    if (n <= bytes) return;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    bytes = 0;
+    CK(cudaHostAlloc(&p, std::max<size_t>(n, 256), cudaHostAllocPortable));
+    bytes = std::max<size_t>(n, 256);
+  }
+  void release() {
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    bytes = 0;
+  }
+};
+
+struct LedgerEvent {
+  int phase;
+  uint64_t layer;
+  int dir;
+  uint64_t bytes;
+  uint64_t elements;
+};
+
+struct LayerState {
+  uint64_t len = 0;
+  bool offloaded = false;
+  uint64_t k_elems = 0, vfast_elems = 0, vslow_elems = 0;
+};
+
+constexpr int kRing = 2;
+
+bool host_pinned(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+}  // namespace
+
+struct kc_cache {
+  kc_config cfg{};
+  uint64_t batch = 0, L = 0, bpe = 2;
+  int dtype = KC_F16;
+  size_t esz = 2;
+  bool has_cap = false;
+  uint64_t cap = 0;
+  int device = 0;
+  int phase = KC_PREFILL;
+  uint64_t G = 1, n_kv = 1, h = 1, dkv = 1, n_q = 1, rows = 1;
+  std::vector<LayerState> layers;
+  std::vector<LedgerEvent> ledger;
+  uint64_t d2h_total = 0, h2d_total = 0;
+
+  // storage
+  void* k_arena = nullptr;
+  size_t k_layer_bytes = 0;
+  void* v_dev = nullptr;
+  void* v_host = nullptr;       // mmap'd, registered
+  void* v_host_dev = nullptr;   // device alias of v_host
+  size_t v_host_bytes = 0;
+  size_t v_layer_bytes = 0;
+
+  // scratch
+  int64_t lstride = 0, kstride = 0;
+  int max_splits = 0;
+  DevBuf logits, partials, keys, part_out, stage_src, stage_k, stage_v, sel_rows, sel_pos, gather_out;
+  DevBuf q32[kRing], idx[kRing], w[kRing], dropped[kRing], norm[kRing], out_tmp[kRing], idx_exp[kRing];
+  PinnedBuf host_in, host_out;
+  cudaStream_t main_st = nullptr, side_st = nullptr;
+  cudaEvent_t ev_start = nullptr, ev_end = nullptr, ev_sel[kRing] = {}, ev_rec[kRing] = {};
+
+  // tuning
+  int score_chunk = 0;
+  int pipeline = 1;
+
+  void* k_layer(uint64_t layer) const { return (char*)k_arena + layer * k_layer_bytes; }
+  void* v_layer(uint64_t layer) const {
+    return layer < L ? (void*)((char*)v_dev + layer * v_layer_bytes)
+                     : (void*)((char*)v_host_dev + (layer - L) * v_layer_bytes);
+  }
+  bool v_in_slow(uint64_t layer) const { return layer >= L && layers[layer].offloaded; }
+  void check_layer(uint64_t layer) const {
+    if (layer >= layers.size())
+      fail(KC_ERANGE, "TieredKVCache: layer " + std::to_string(layer) + " out of range");
+  }
+  uint64_t current_len() const { return layers.empty() ? 0 : layers[0].len; }
+  uint64_t fast_bytes() const {
+    uint64_t e = 0;
+    for (const auto& l : layers) e += l.k_elems + l.vfast_elems;
+    return checked_mul({bpe, e});
+  }
+  uint64_t slow_bytes() const {
+    uint64_t e = 0;
+    for (const auto& l : layers) e += l.vslow_elems;
+    return checked_mul({bpe, e});
+  }
+  void record(int ph, uint64_t layer, int dir, uint64_t bytes, uint64_t elements) {
+    ledger.push_back({ph, layer, dir, bytes, elements});
+    (dir == KC_D2H ? d2h_total : h2d_total) += bytes;
+  }
+};
+
+namespace {
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return KC_OK;
+  } catch (const KcError& e) {
+    g_err = e.msg;
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_err = "out of host memory";
+    return KC_ECUDA;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return KC_ECUDA;
+  }
+}
+
+void set_dev(const kc_cache* c) { CK(cudaSetDevice(c->device)); }
+
+void* alloc_pinned_arena(size_t bytes, int numa_node, void** dev_alias) {
+  void* p = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS | MAP_NORESERVE,
+                 -1, 0);
+  if (p == MAP_FAILED) fail(KC_ECUDA, "mmap of the pinned V arena failed");
+  madvise(p, bytes, MADV_HUGEPAGE);
+  if (numa_node >= 0 && numa_node < 64) {
+    // MPOL_BIND to the GPU's NUMA node (no libnuma in the image: raw syscall);
+    // best effort -- single-node hosts simply keep the default policy.
+    unsigned long mask = 1ul << numa_node;
+    syscall(SYS_mbind, p, bytes, 2 /*MPOL_BIND*/, &mask, 64, 0);
+  }
+  cudaError_t e = cudaHostRegister(p, bytes, cudaHostRegisterMapped | cudaHostRegisterPortable);
+  if (e != cudaSuccess) {
+    munmap(p, bytes);
+    fail(KC_ECUDA, std::string("cudaHostRegister(V arena): ") + cudaGetErrorString(e));
+  }
+  CK(cudaHostGetDevicePointer(dev_alias, p, 0));
+  return p;
+}
+
+void destroy(kc_cache* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->main_st) cudaStreamSynchronize(c->main_st);
+  if (c->side_st) cudaStreamSynchronize(c->side_st);
+  cudaDeviceSynchronize();
+  if (c->k_arena) cudaFree(c->k_arena);
+  if (c->v_dev) cudaFree(c->v_dev);
+  if (c->v_host) {
+    cudaHostUnregister(c->v_host);
+    munmap(c->v_host, c->v_host_bytes);
+  }
+  for (DevBuf* b : {&c->logits, &c->partials, &c->keys, &c->part_out, &c->stage_src, &c->stage_k,
+                    &c->stage_v, &c->sel_rows, &c->sel_pos, &c->gather_out})
+    b->release();
+  for (int i = 0; i < kRing; ++i) {
+    c->q32[i].release(); c->idx[i].release(); c->w[i].release(); c->dropped[i].release();
+    c->norm[i].release(); c->out_tmp[i].release(); c->idx_exp[i].release();
+    if (c->ev_sel[i]) cudaEventDestroy(c->ev_sel[i]);
+    if (c->ev_rec[i]) cudaEventDestroy(c->ev_rec[i]);
+  }
+  c->host_in.release();
+  c->host_out.release();
+  if (c->ev_start) cudaEventDestroy(c->ev_start);
+  if (c->ev_end) cudaEventDestroy(c->ev_end);
+  if (c->main_st) cudaStreamDestroy(c->main_st);
+  if (c->side_st) cudaStreamDestroy(c->side_st);
+  delete c;
+}
+
+// ---- append ----------------------------------------------------------------
+void append_checks(kc_cache* c, uint64_t layer, uint64_t rows) {
+  c->check_layer(layer);
+  if (rows == 0 || rows % c->batch != 0)
+    fail(KC_ESHAPE, "append_kv: need a positive multiple of batch rows for K and V");
+  const uint64_t m = rows / c->batch;
+  if (c->layers[layer].len + m > c->cfg.max_seq) fail(KC_ESTATE, "append_kv: cache grew past max_seq");
+}
+
+// kv_cache.cpp:96-121 accounting after the rows are stored
+void append_account(kc_cache* c, uint64_t layer, uint64_t rows) {
+  LayerState& st = c->layers[layer];
+  const uint64_t elements = rows * c->dkv;
+  st.k_elems += elements;
+  const bool to_slow = c->phase == KC_DECODE && layer >= c->L;
+  if (to_slow) {
+    st.vslow_elems += elements;
+    c->record(c->phase, layer, KC_D2H, checked_mul({c->bpe, elements}), elements);
+  } else {
+    st.vfast_elems += elements;
+  }
+  st.len += rows / c->batch;
+  if (c->has_cap && c->fast_bytes() > c->cap)
+    fail(KC_ECAPACITY, "fast tier over budget: " + std::to_string(c->fast_bytes()) + " > " +
+                           std::to_string(c->cap) + " bytes");
+}
+
+void enqueue_append(kc_cache* c, uint64_t layer, const void* k, const void* v, int dt, uint64_t rows,
+                    cudaStream_t st) {
+  kc::AppendParams ap{};
+  ap.n_rows = (int64_t)rows;
+  ap.max_seq = (int64_t)c->cfg.max_seq;
+  ap.pos0 = (int64_t)c->layers[layer].len;
+  ap.batch = (int)c->batch;
+  ap.n_kv = (int)c->n_kv;
+  ap.h = (int)c->h;
+  ap.src = k;
+  ap.dst = c->k_layer(layer);
+  kc::append_launch(ap, dt, c->dtype, st);
+  ap.src = v;
+  ap.dst = c->v_layer(layer);
+  kc::append_launch(ap, dt, c->dtype, st);
+  CK(cudaGetLastError());
+}
+
+// ---- decode ----------------------------------------------------------------
+void decode_checks(kc_cache* c, uint64_t layer) {
+  if (c->current_len() == 0) fail(KC_ESTATE, "decode attention: cache is empty");
+  c->check_layer(layer);
+  if (c->layers[layer].len < c->current_len())
+    fail(KC_ERANGE, "k_row: position or batch index out of range");
+}
+
+struct StepGeom {
+  int s, nc, chunk, n_splits;
+};
+
+StepGeom geom(kc_cache* c, uint64_t top_n) {
+  StepGeom g{};
+  g.s = (int)c->current_len();
+  g.nc = (int)std::min<uint64_t>(top_n, (uint64_t)g.s);
+  g.chunk = kc::score_pick_chunk(g.s, (int)c->rows, c->score_chunk);
+  g.n_splits = (g.s + g.chunk - 1) / g.chunk;
+  if (g.n_splits > c->max_splits) {
+    g.chunk = ((g.s + c->max_splits - 1) / c->max_splits + 63) / 64 * 64;
+    g.n_splits = (g.s + g.chunk - 1) / g.chunk;
+  }
+  return g;
+}
+
+void enqueue_score(kc_cache* c, uint64_t layer, const float* q32, const StepGeom& g, cudaStream_t st) {
+  kc::ScoreParams sp{};
+  sp.k = c->k_layer(layer);
+  sp.q = q32;
+  sp.logits = c->logits.as<float>();
+  sp.partials = c->partials.as<float2>();
+  sp.max_seq = (int64_t)c->cfg.max_seq;
+  sp.lstride = c->lstride;
+  sp.s = g.s;
+  sp.h = (int)c->h;
+  sp.n_kv = (int)c->n_kv;
+  sp.G = (int)c->G;
+  sp.rows = (int)c->rows;
+  sp.chunk = g.chunk;
+  sp.n_splits = g.n_splits;
+  sp.max_splits = c->max_splits;
+  sp.scale = 1.0f / std::sqrt(static_cast<float>(c->h));  // attention.hpp:15-17
+  kc::score_launch(sp, c->dtype, st);
+}
+
+// q (any dtype, host or device) -> fp32 device buffer for ring slot
+const float* stage_q(kc_cache* c, int slot, const void* q, int q_dtype, bool io_device,
+                     cudaStream_t st) {
+  const uint64_t nq = c->batch * c->n_q * c->h;
+  if (io_device && q_dtype == KC_F32) return static_cast<const float*>(q);
+  c->q32[slot].ensure(nq * sizeof(float));
+  const void* src = q;
+  if (!io_device) {
+    const size_t bytes = nq * dtype_size(q_dtype);
+    c->stage_src.ensure(bytes * kRing);
+    void* dst = (char*)c->stage_src.p + slot * bytes;
+    CK(cudaMemcpyAsync(dst, q, bytes, cudaMemcpyHostToDevice, st));
+    src = dst;
+  }
+  kc::to_f32_launch(src, q_dtype, c->q32[slot].as<float>(), (int64_t)nq, st);
+  return c->q32[slot].as<float>();
+}
+
+void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const void* const* q,
+                      int q_dtype, uint64_t top_n, uint32_t flags, kc_topn_out* outs,
+                      cudaStream_t user_st) {
+  if (top_n == 0) fail(KC_EARG, "decode_attention_topn: top_n must be >= 1");
+  dtype_size(q_dtype);
+  for (uint64_t i = 0; i < n; ++i) decode_checks(c, layers[i]);
+  if (c->G * c->h > 1024) fail(KC_ESHAPE, "decode attention: group*head_dim > 1024 unsupported");
+  set_dev(c);
+  const bool io_device = flags & KC_IO_DEVICE;
+  cudaStream_t st = io_device ? user_st : c->main_st;
+  const StepGeom g = geom(c, top_n);
+  const uint64_t nc = (uint64_t)g.nc;
+  const uint64_t slots = c->batch * c->n_q;
+  for (int r = 0; r < kRing; ++r) {
+    c->idx[r].ensure(c->rows * nc * 4);
+    c->w[r].ensure(slots * nc * 4);
+    c->dropped[r].ensure(slots * 8);
+    c->norm[r].ensure(slots * 4);
+    if (!io_device) c->out_tmp[r].ensure(slots * c->h * 4);
+    if (c->G > 1) c->idx_exp[r].ensure(slots * nc * 4);
+  }
+  // host outputs land in one pinned staging block per call
+  const size_t o_out = slots * c->h * 4, o_idx = slots * nc * 4, o_w = slots * nc * 4, o_dr = slots * 8;
+  const size_t per_layer = o_out + o_idx + o_w + o_dr;
+  if (!io_device) c->host_out.ensure(per_layer * n);
+
+  cudaStream_t side = c->pipeline ? c->side_st : st;
+  CK(cudaEventRecord(c->ev_start, st));
+  if (side != st) CK(cudaStreamWaitEvent(side, c->ev_start, 0));
+
+  for (uint64_t i = 0; i < n; ++i) {
+    const int slot = (int)(i % kRing);
+    const uint64_t layer = layers[i];
+    const float* q32 = stage_q(c, slot, q[i], q_dtype, io_device, st);
+    enqueue_score(c, layer, q32, g, st);
+    if (i >= (uint64_t)kRing && side != st) CK(cudaStreamWaitEvent(st, c->ev_rec[slot], 0));
+
+    kc::SelectParams sp{};
+    sp.logits = c->logits.as<float>();
+    sp.partials = c->partials.as<float2>();
+    sp.keys = c->keys.as<uint32_t>();
+    sp.idx = c->idx[slot].as<uint32_t>();
+    sp.w = c->w[slot].as<float>();
+    sp.dropped = c->dropped[slot].as<double>();
+    sp.norm = c->norm[slot].as<float>();
+    sp.lstride = c->lstride;
+    sp.kstride = c->kstride;
+    sp.s = g.s;
+    sp.nc = g.nc;
+    sp.n_kv = (int)c->n_kv;
+    sp.G = (int)c->G;
+    sp.n_splits = g.n_splits;
+    sp.max_splits = c->max_splits;
+    sp.rows = (int)c->rows;
+    kc::select_launch(sp, st);
+    CK(cudaEventRecord(c->ev_sel[slot], st));
+    if (side != st) CK(cudaStreamWaitEvent(side, c->ev_sel[slot], 0));
+
+    kc_topn_out& o = outs[i];
+    kc::RecallParams rp{};
+    rp.v = c->v_layer(layer);
+    rp.idx = c->idx[slot].as<uint32_t>();
+    rp.w = c->w[slot].as<float>();
+    rp.norm = c->norm[slot].as<float>();
+    rp.out = io_device ? o.out : c->out_tmp[slot].as<float>();
+    rp.max_seq = (int64_t)c->cfg.max_seq;
+    rp.nc = g.nc;
+    rp.h = (int)c->h;
+    rp.n_kv = (int)c->n_kv;
+    rp.G = (int)c->G;
+    rp.rows = (int)c->rows;
+    rp.renormalize = (flags & KC_RENORMALIZE) ? 1 : 0;
+    rp.reverse = (flags & KC_REVERSE_ACCUM) ? 1 : 0;
+    rp.row_offset = 0;
+    kc::recall_launch(rp, c->dtype, side);
+
+    const uint32_t* idx_slots = c->idx[slot].as<uint32_t>();
+    if (c->G > 1 && (o.indices || !io_device)) {
+      kc::expand_idx_launch(idx_slots, c->idx_exp[slot].as<uint32_t>(), (int)c->rows, (int)c->G,
+                            g.nc, side);
+      idx_slots = c->idx_exp[slot].as<uint32_t>();
+    }
+    if (io_device) {
+      if (o.indices) CK(cudaMemcpyAsync(o.indices, idx_slots, o_idx, cudaMemcpyDeviceToDevice, side));
+      if (o.weights) CK(cudaMemcpyAsync(o.weights, c->w[slot].p, o_w, cudaMemcpyDeviceToDevice, side));
+      if (o.dropped_mass)
+        CK(cudaMemcpyAsync(o.dropped_mass, c->dropped[slot].p, o_dr, cudaMemcpyDeviceToDevice, side));
+    } else {
+      char* hb = (char*)c->host_out.p + i * per_layer;
+      CK(cudaMemcpyAsync(hb, c->out_tmp[slot].p, o_out, cudaMemcpyDeviceToHost, side));
+      if (o.indices) CK(cudaMemcpyAsync(hb + o_out, idx_slots, o_idx, cudaMemcpyDeviceToHost, side));
+      if (o.weights) CK(cudaMemcpyAsync(hb + o_out + o_idx, c->w[slot].p, o_w, cudaMemcpyDeviceToHost, side));
+      if (o.dropped_mass)
+        CK(cudaMemcpyAsync(hb + o_out + o_idx + o_w, c->dropped[slot].p, o_dr, cudaMemcpyDeviceToHost, side));
+    }
+    CK(cudaEventRecord(c->ev_rec[slot], side));
+    CK(cudaGetLastError());
+
+    // ledger: gather_v charges bytes * sum(counts) * h for offloaded layers
+    // (kv_cache.cpp:181-185); GQA recalls one row set per kv head.
+    o.nc = nc;
+    o.h2d_bytes = 0;
+    if (c->v_in_slow(layer)) {
+      const uint64_t elements = checked_mul({c->rows, nc, c->h});
+      o.h2d_bytes = checked_mul({c->bpe, elements});
+      c->record(c->phase, layer, KC_H2D, o.h2d_bytes, elements);
+    }
+  }
+  if (side != st) {
+    CK(cudaEventRecord(c->ev_end, side));
+    CK(cudaStreamWaitEvent(st, c->ev_end, 0));
+  }
+  if (!io_device) {
+    CK(cudaStreamSynchronize(st));
+    for (uint64_t i = 0; i < n; ++i) {
+      const char* hb = (const char*)c->host_out.p + i * per_layer;
+      kc_topn_out& o = outs[i];
+      std::memcpy(o.out, hb, o_out);
+      if (o.indices) std::memcpy(o.indices, hb + o_out, o_idx);
+      if (o.weights) std::memcpy(o.weights, hb + o_out + o_idx, o_w);
+      if (o.dropped_mass) std::memcpy(o.dropped_mass, hb + o_out + o_idx + o_w, o_dr);
+    }
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* kc_last_error(void) { return g_err.c_str(); }
+const char* kc_version(void) { return "kcache-b200 0.1 (sm_100a)"; }
+
+int kc_cache_create(const kc_config* cfg, uint64_t batch, uint64_t resident_layers,
+                    uint64_t bytes_per_element, int storage_dtype, int has_fast_capacity,
+                    uint64_t fast_capacity_bytes, int device, int numa_node, kc_cache** out) {
+  return guarded([&] {
+    if (!cfg || !out) fail(KC_EARG, "kc_cache_create: null argument");
+    *out = nullptr;
+    // ModelConfig::validate (model.cpp:13-27) for the attention fields
+    if (!cfg->n_layers || !cfg->d_model || !cfg->n_heads || !cfg->head_dim || !cfg->max_seq)
+      fail(KC_ESHAPE, "ModelConfig: all counts must be >= 1");
+    if (cfg->d_model != cfg->n_heads * cfg->head_dim)
+      fail(KC_ESHAPE, "ModelConfig: d_model must equal n_heads * head_dim");
+    const uint64_t n_kv = cfg->n_kv_heads ? cfg->n_kv_heads : cfg->n_heads;
+    if (cfg->n_heads % n_kv != 0) fail(KC_ESHAPE, "ModelConfig: n_kv_heads must divide n_heads");
+    // TierPlacement::validate (kv_cache.cpp:39-46)
+    if (resident_layers > cfg->n_layers)
+      fail(KC_ESHAPE, "TierPlacement: resident_layers must be <= n_layers");
+    if (bytes_per_element == 0) fail(KC_ESHAPE, "TierPlacement: bytes_per_element must be >= 1");
+    if (batch == 0) fail(KC_ESHAPE, "TieredKVCache: batch must be >= 1");
+    if (cfg->n_heads / n_kv > 32) fail(KC_ESHAPE, "GQA group size > 32 unsupported");
+    const size_t esz = dtype_size(storage_dtype);
+    if (cfg->max_seq > (1ull << 30)) fail(KC_ESHAPE, "max_seq too large");
+
+    auto* c = new kc_cache;
+    try {
+      c->cfg = *cfg;
+      c->cfg.n_kv_heads = n_kv;
+      c->batch = batch;
+      c->L = resident_layers;
+      c->bpe = bytes_per_element;
+      c->dtype = storage_dtype;
+      c->esz = esz;
+      c->has_cap = has_fast_capacity != 0;
+      c->cap = fast_capacity_bytes;
+      c->device = device;
+      c->n_kv = n_kv;
+      c->h = cfg->head_dim;
+      c->n_q = cfg->n_heads;
+      c->G = cfg->n_heads / n_kv;
+      c->dkv = n_kv * cfg->head_dim;
+      c->rows = batch * n_kv;
+      c->layers.resize(cfg->n_layers);
+      set_dev(c);
+      c->k_layer_bytes = checked_mul({c->rows, cfg->max_seq, c->h, esz});
+      c->v_layer_bytes = c->k_layer_bytes;
+      CK(cudaMalloc(&c->k_arena, checked_mul({c->k_layer_bytes, cfg->n_layers})));
+      if (c->L > 0) CK(cudaMalloc(&c->v_dev, checked_mul({c->v_layer_bytes, c->L})));
+      if (cfg->n_layers > c->L) {
+        c->v_host_bytes = checked_mul({c->v_layer_bytes, cfg->n_layers - c->L});
+        c->v_host = alloc_pinned_arena(c->v_host_bytes, numa_node, &c->v_host_dev);
+      }
+      c->lstride = (int64_t)((cfg->max_seq + 3) & ~3ull);
+      c->kstride = (int64_t)cfg->max_seq;
+      c->max_splits = (int)((cfg->max_seq + 63) / 64);
+      c->logits.ensure(checked_mul({batch, c->n_q, (uint64_t)c->lstride, 4}));
+      c->partials.ensure(checked_mul({batch, c->n_q, (uint64_t)c->max_splits, 8}));
+      c->keys.ensure(checked_mul({c->rows, (uint64_t)c->kstride, 4}));
+      int lo = 0, hi = 0;
+      CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      CK(cudaStreamCreateWithFlags(&c->main_st, cudaStreamNonBlocking));
+      CK(cudaStreamCreateWithPriority(&c->side_st, cudaStreamNonBlocking, hi));
+      CK(cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&c->ev_end, cudaEventDisableTiming));
+      for (int i = 0; i < kRing; ++i) {
+        CK(cudaEventCreateWithFlags(&c->ev_sel[i], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&c->ev_rec[i], cudaEventDisableTiming));
+      }
+    } catch (...) {
+      destroy(c);
+      throw;
+    }
+    *out = c;
+  });
+}
+
+int kc_cache_destroy(kc_cache* c) {
+  return guarded([&] { destroy(c); });
+}
+
+int kc_append_kv(kc_cache* c, uint64_t layer, const float* k, const float* v, uint64_t rows) {
+  return guarded([&] {
+    append_checks(c, layer, rows);
+    set_dev(c);
+    const size_t bytes = rows * c->dkv * sizeof(float);
+    c->stage_k.ensure(bytes);
+    c->stage_v.ensure(bytes);
+    CK(cudaMemcpyAsync(c->stage_k.p, k, bytes, cudaMemcpyHostToDevice, c->main_st));
+    CK(cudaMemcpyAsync(c->stage_v.p, v, bytes, cudaMemcpyHostToDevice, c->main_st));
+    enqueue_append(c, layer, c->stage_k.p, c->stage_v.p, KC_F32, rows, c->main_st);
+    CK(cudaStreamSynchronize(c->main_st));
+    append_account(c, layer, rows);
+  });
+}
+
+int kc_append_kv_device(kc_cache* c, uint64_t layer, const void* k, const void* v, int dtype,
+                        uint64_t rows, void* stream) {
+  return guarded([&] {
+    dtype_size(dtype);
+    append_checks(c, layer, rows);
+    set_dev(c);
+    enqueue_append(c, layer, k, v, dtype, rows, (cudaStream_t)stream);
+    append_account(c, layer, rows);
+  });
+}
+
+int kc_offload_prefill_v(kc_cache* c, uint64_t layer) {
+  return guarded([&] {
+    c->check_layer(layer);
+    if (layer < c->L) return;
+    LayerState& st = c->layers[layer];
+    if (st.offloaded)
+      fail(KC_ESTATE, "offload_prefill_v: layer " + std::to_string(layer) + " already offloaded");
+    const uint64_t elements = st.vfast_elems;
+    st.vslow_elems += elements;
+    st.vfast_elems = 0;
+    st.offloaded = true;
+    c->record(KC_PREFILL, layer, KC_D2H, checked_mul({c->bpe, elements}), elements);
+  });
+}
+
+int kc_begin_decode(kc_cache* c) {
+  return guarded([&] {
+    for (uint64_t l = c->L; l < c->layers.size(); ++l)
+      if (!c->layers[l].offloaded)
+        fail(KC_ESTATE, "begin_decode: layer " + std::to_string(l) + " was never offloaded");
+    c->phase = KC_DECODE;
+  });
+}
+
+int kc_decode_topn(kc_cache* c, uint64_t layer, const void* q, int q_dtype, uint64_t top_n,
+                   uint32_t flags, kc_topn_out* out, void* stream) {
+  return guarded([&] {
+    if (!out || !q) fail(KC_EARG, "kc_decode_topn: null argument");
+    const void* qs[1] = {q};
+    decode_topn_impl(c, 1, &layer, qs, q_dtype, top_n, flags, out, (cudaStream_t)stream);
+  });
+}
+
+int kc_decode_topn_layers(kc_cache* c, uint64_t n, const uint64_t* layers, const void* const* q,
+                          int q_dtype, uint64_t top_n, uint32_t flags, kc_topn_out* outs,
+                          void* stream) {
+  return guarded([&] {
+    if (n == 0) return;
+    if (!layers || !q || !outs) fail(KC_EARG, "kc_decode_topn_layers: null argument");
+    decode_topn_impl(c, n, layers, q, q_dtype, top_n, flags, outs, (cudaStream_t)stream);
+  });
+}
+
+int kc_decode_full(kc_cache* c, uint64_t layer, const void* q, int q_dtype, uint32_t flags,
+                   float* out, void* stream) {
+  return guarded([&] {
+    if (!q || !out) fail(KC_EARG, "kc_decode_full: null argument");
+    dtype_size(q_dtype);
+    decode_checks(c, layer);
+    if (c->G * c->h > 1024) fail(KC_ESHAPE, "decode attention: group*head_dim > 1024 unsupported");
+    set_dev(c);
+    const bool io_device = flags & KC_IO_DEVICE;
+    cudaStream_t st = io_device ? (cudaStream_t)stream : c->main_st;
+    const StepGeom g = geom(c, 1);
+    const float* q32 = stage_q(c, 0, q, q_dtype, io_device, st);
+    enqueue_score(c, layer, q32, g, st);
+    const uint64_t slots = c->batch * c->n_q;
+    c->part_out.ensure(checked_mul({slots, (uint64_t)g.n_splits, c->h, 4}));
+    if (!io_device) c->out_tmp[0].ensure(slots * c->h * 4);
+    kc::PvFullParams pp{};
+    pp.v = c->v_layer(layer);
+    pp.logits = c->logits.as<float>();
+    pp.partials = c->partials.as<float2>();
+    pp.part_out = c->part_out.as<float>();
+    pp.out = io_device ? out : c->out_tmp[0].as<float>();
+    pp.max_seq = (int64_t)c->cfg.max_seq;
+    pp.lstride = c->lstride;
+    pp.s = g.s;
+    pp.h = (int)c->h;
+    pp.n_kv = (int)c->n_kv;
+    pp.G = (int)c->G;
+    pp.rows = (int)c->rows;
+    pp.chunk = g.chunk;
+    pp.n_splits = g.n_splits;
+    pp.max_splits = c->max_splits;
+    kc::pv_full_launch(pp, c->dtype, st);
+    CK(cudaGetLastError());
+    if (!io_device) {
+      CK(cudaMemcpyAsync(out, c->out_tmp[0].p, slots * c->h * 4, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+    }
+  });
+}
+
+int kc_score_probs(kc_cache* c, uint64_t layer, const void* q, int q_dtype, float* probs) {
+  return guarded([&] {
+    if (!q || !probs) fail(KC_EARG, "kc_score_probs: null argument");
+    dtype_size(q_dtype);
+    decode_checks(c, layer);
+    set_dev(c);
+    cudaStream_t st = c->main_st;
+    const StepGeom g = geom(c, 1);
+    const float* q32 = stage_q(c, 0, q, q_dtype, false, st);
+    enqueue_score(c, layer, q32, g, st);
+    const uint64_t slots = c->batch * c->n_q;
+    c->gather_out.ensure(checked_mul({slots, (uint64_t)g.s, 4}));
+    kc::SelectParams sp{};
+    sp.logits = c->logits.as<float>();
+    sp.partials = c->partials.as<float2>();
+    sp.lstride = c->lstride;
+    sp.s = g.s;
+    sp.n_kv = (int)c->n_kv;
+    sp.G = (int)c->G;
+    sp.n_splits = g.n_splits;
+    sp.max_splits = c->max_splits;
+    sp.rows = (int)c->rows;
+    kc::probs_launch(sp, c->gather_out.as<float>(), st);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(probs, c->gather_out.p, slots * g.s * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  });
+}
+
+int kc_gather_v(kc_cache* c, uint64_t layer, const uint32_t* indices, const uint64_t* counts,
+                float* out, uint64_t* h2d_bytes) {
+  return guarded([&] {
+    c->check_layer(layer);
+    const uint64_t slots = c->batch * c->n_q;
+    uint64_t total = 0;
+    for (uint64_t s = 0; s < slots; ++s) total += counts[s];
+    std::vector<uint32_t> rows(total), pos(total);
+    const uint64_t len = c->layers[layer].len;
+    uint64_t e = 0;
+    for (uint64_t s = 0; s < slots; ++s) {
+      const uint64_t b = s / c->n_q, head = s % c->n_q;
+      for (uint64_t r = 0; r < counts[s]; ++r, ++e) {
+        if (indices[e] >= len)
+          fail(KC_ERANGE, "gather_v: index " + std::to_string(indices[e]) + " past current length " +
+                              std::to_string(len));
+        rows[e] = (uint32_t)(b * c->n_kv + head / c->G);
+        pos[e] = indices[e];
+      }
+    }
+    set_dev(c);
+    if (total > 0) {
+      c->sel_rows.ensure(total * 4);
+      c->sel_pos.ensure(total * 4);
+      c->gather_out.ensure(total * c->h * 4);
+      CK(cudaMemcpyAsync(c->sel_rows.p, rows.data(), total * 4, cudaMemcpyHostToDevice, c->main_st));
+      CK(cudaMemcpyAsync(c->sel_pos.p, pos.data(), total * 4, cudaMemcpyHostToDevice, c->main_st));
+      kc::gather_rows_launch(c->v_layer(layer), c->dtype, c->sel_rows.as<uint32_t>(),
+                             c->sel_pos.as<uint32_t>(), (int64_t)total, (int)c->h,
+                             (int64_t)c->cfg.max_seq, c->gather_out.as<float>(), c->main_st);
+      CK(cudaGetLastError());
+      CK(cudaMemcpyAsync(out, c->gather_out.p, total * c->h * 4, cudaMemcpyDeviceToHost, c->main_st));
+      CK(cudaStreamSynchronize(c->main_st));
+    }
+    uint64_t bytes = 0;
+    if (c->v_in_slow(layer)) {
+      const uint64_t elements = checked_mul({total, c->h});
+      bytes = checked_mul({c->bpe, elements});
+      c->record(c->phase, layer, KC_H2D, bytes, elements);
+    }
+    if (h2d_bytes) *h2d_bytes = bytes;
+  });
+}
+
+int kc_read_row(kc_cache* c, uint64_t layer, uint64_t pos, uint64_t bi, int which, float* out) {
+  return guarded([&] {
+    c->check_layer(layer);
+    if (pos >= c->layers[layer].len || bi >= c->batch)
+      fail(KC_ERANGE, std::string(which ? "v_row" : "k_row") + ": position or batch index out of range");
+    set_dev(c);
+    std::vector<uint32_t> rows(c->n_kv), ps(c->n_kv, (uint32_t)pos);
+    for (uint64_t k = 0; k < c->n_kv; ++k) rows[k] = (uint32_t)(bi * c->n_kv + k);
+    c->sel_rows.ensure(c->n_kv * 4);
+    c->sel_pos.ensure(c->n_kv * 4);
+    c->gather_out.ensure(c->dkv * 4);
+    CK(cudaMemcpyAsync(c->sel_rows.p, rows.data(), c->n_kv * 4, cudaMemcpyHostToDevice, c->main_st));
+    CK(cudaMemcpyAsync(c->sel_pos.p, ps.data(), c->n_kv * 4, cudaMemcpyHostToDevice, c->main_st));
+    kc::gather_rows_launch(which ? c->v_layer(layer) : c->k_layer(layer), c->dtype,
+                           c->sel_rows.as<uint32_t>(), c->sel_pos.as<uint32_t>(), (int64_t)c->n_kv,
+                           (int)c->h, (int64_t)c->cfg.max_seq, c->gather_out.as<float>(), c->main_st);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(out, c->gather_out.p, c->dkv * 4, cudaMemcpyDeviceToHost, c->main_st));
+    CK(cudaStreamSynchronize(c->main_st));
+  });
+}
+
+int kc_current_len(const kc_cache* c, uint64_t* len) {
+  return guarded([&] { *len = c->current_len(); });
+}
+int kc_phase(const kc_cache* c, int* phase) {
+  return guarded([&] { *phase = c->phase; });
+}
+int kc_fast_bytes_used(const kc_cache* c, uint64_t* bytes) {
+  return guarded([&] { *bytes = c->fast_bytes(); });
+}
+int kc_slow_bytes_used(const kc_cache* c, uint64_t* bytes) {
+  return guarded([&] { *bytes = c->slow_bytes(); });
+}
+int kc_d2h_bytes_total(const kc_cache* c, uint64_t* bytes) {
+  return guarded([&] { *bytes = c->d2h_total; });
+}
+int kc_h2d_bytes_total(const kc_cache* c, uint64_t* bytes) {
+  return guarded([&] { *bytes = c->h2d_total; });
+}
+int kc_ledger_size(const kc_cache* c, uint64_t* n) {
+  return guarded([&] { *n = c->ledger.size(); });
+}
+int kc_ledger_event(const kc_cache* c, uint64_t i, int* phase, uint64_t* layer, int* dir,
+                    uint64_t* bytes, uint64_t* elements) {
+  return guarded([&] {
+    if (i >= c->ledger.size()) fail(KC_ERANGE, "ledger event index out of range");
+    const LedgerEvent& e = c->ledger[i];
+    *phase = e.phase;
+    *layer = e.layer;
+    *dir = e.dir;
+    *bytes = e.bytes;
+    *elements = e.elements;
+  });
+}
+int kc_layer_storage(const kc_cache* c, uint64_t layer, void** k, void** v, int* v_on_host) {
+  return guarded([&] {
+    c->check_layer(layer);
+    *k = c->k_layer(layer);
+    *v = c->v_layer(layer);
+    *v_on_host = layer >= c->L ? 1 : 0;
+  });
+}
+int kc_sync(kc_cache* c) {
+  return guarded([&] {
+    set_dev(c);
+    CK(cudaStreamSynchronize(c->main_st));
+    CK(cudaStreamSynchronize(c->side_st));
+  });
+}
+int kc_set_tuning(kc_cache* c, const char* key, int64_t value) {
+  return guarded([&] {
+    const std::string k = key ? key : "";
+    if (k == "score_chunk") c->score_chunk = (int)value;
+    else if (k == "pipeline") c->pipeline = value ? 1 : 0;
+    else fail(KC_EARG, "unknown tuning key '" + k + "'");
+  });
+}
+
+int kc_arg_topk(const float* values, uint64_t n, uint64_t k, uint32_t* out, uint64_t* count) {
+  return guarded([&] {
+    if (k == 0) fail(KC_EARG, "arg_topk: k must be >= 1");
+    const uint64_t m = std::min(k, n);
+    if (count) *count = m;
+    if (n == 0) return;
+    if (n > (1ull << 31)) fail(KC_EARG, "arg_topk: too many values");
+    float* dv = nullptr;
+    uint32_t *dk = nullptr, *dout = nullptr;
+    CK(cudaMalloc(&dv, n * 4));
+    CK(cudaMalloc(&dk, n * 4));
+    CK(cudaMalloc(&dout, m * 4));
+    CK(cudaMemcpy(dv, values, n * 4, cudaMemcpyHostToDevice));
+    kc::arg_topk_launch(dv, (int)n, (int)m, dk, dout, nullptr);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaMemcpy(out, dout, m * 4, cudaMemcpyDeviceToHost);
+    cudaFree(dv);
+    cudaFree(dk);
+    cudaFree(dout);
+    if (e != cudaSuccess) fail(KC_ECUDA, std::string("arg_topk: ") + cudaGetErrorString(e));
+  });
+}
+
+int kc_fill_uniform(void* dst, int dtype, uint64_t n, uint64_t seed, uint64_t offset, float lo,
+                    float hi, void* stream) {
+  return guarded([&] {
+    dtype_size(dtype);
+    if (n == 0) return;
+    kc::fill_uniform_launch(dst, dtype, n, seed, offset, lo, hi, (cudaStream_t)stream);
+    CK(cudaGetLastError());
+  });
+}
+
+}  // extern "C"

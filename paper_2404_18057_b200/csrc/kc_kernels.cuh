@@ -1,0 +1,128 @@
+// kc_kernels.cuh -- launch interfaces of the sm_100a kernels (host side).
+//
+// One decode_attention_topn call (proj/core/src/attention.cpp:116-190) is
+//   score_launch    q.K^T over every cached position + per-split (max, sum exp)
+//   select_launch   global softmax stats, top-N radix select, weights, dropped
+//   recall_launch   V recall of the selected rows (HBM or mapped host) + P.V
+// decode_attention_full (attention.cpp:91-114) is score_launch + pv_full_launch.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace kc {
+
+struct ScoreParams {
+  const void* k;        // layer's K: [rows][max_seq][h], rows = batch*n_kv
+  const float* q;       // [batch][n_q][h] fp32
+  float* logits;        // [batch][n_q][lstride]
+  float2* partials;     // [batch][n_q][max_splits]  (max, sum exp)
+  int64_t max_seq;      // K slot stride in positions
+  int64_t lstride;      // logits row stride
+  int s;                // current length
+  int h;                // head_dim
+  int n_kv;
+  int G;                // q heads per kv head
+  int rows;             // batch*n_kv
+  int chunk;            // positions per CTA (multiple of 64)
+  int n_splits;
+  int max_splits;
+  float scale;          // 1/sqrt(h) as the reference computes it
+};
+// dtype: KC_F32 / KC_F16 / KC_BF16 (storage)
+void score_launch(const ScoreParams& p, int dtype, cudaStream_t st);
+// positions per CTA for a given shape (tuning override when > 0)
+int score_pick_chunk(int s, int rows, int override_chunk);
+
+struct SelectParams {
+  const float* logits;    // [batch][n_q][lstride]
+  const float2* partials; // [batch][n_q][max_splits]
+  uint32_t* keys;         // scratch [rows][kstride]
+  uint32_t* idx;          // [rows][nc]
+  float* w;               // [batch*n_q][nc]
+  double* dropped;        // [batch*n_q]
+  float* norm;            // [batch*n_q]  1/sum(w) for renormalize (1 if sum == 0)
+  int64_t lstride;
+  int64_t kstride;
+  int s;
+  int nc;                 // min(top_n, s)
+  int n_kv;
+  int G;
+  int n_splits;
+  int max_splits;
+  int rows;
+};
+void select_launch(const SelectParams& p, cudaStream_t st);
+
+// p = exp(s - M)/Z for every position of every (batch, q head) -> probs
+// [batch*n_q][s] (ScoreObserver debug path).
+void probs_launch(const SelectParams& p, float* probs, cudaStream_t st);
+
+// Standalone arg_topk over raw floats (ordered-float keys).
+void arg_topk_launch(const float* values, int n, int k, uint32_t* keys_scratch, uint32_t* out,
+                     cudaStream_t st);
+
+struct RecallParams {
+  const void* v;          // layer's V: [rows][max_seq][h] (device or mapped host)
+  const uint32_t* idx;    // [rows][nc]
+  const float* w;         // [batch*n_q][nc]
+  const float* norm;      // [batch*n_q]
+  float* out;             // [batch][n_q*h]
+  int64_t max_seq;
+  int nc;
+  int h;
+  int n_kv;
+  int G;
+  int rows;
+  int renormalize;
+  int reverse;            // fault hook: descending accumulation
+  int row_offset;         // first row of this launch (pipelined chunks)
+};
+void recall_launch(const RecallParams& p, int dtype, cudaStream_t st);
+
+struct PvFullParams {
+  const void* v;          // [rows][max_seq][h]
+  const float* logits;
+  const float2* partials;
+  float* part_out;        // scratch [batch*n_q][n_splits][h]
+  float* out;             // [batch][n_q*h]
+  int64_t max_seq;
+  int64_t lstride;
+  int s;
+  int h;
+  int n_kv;
+  int G;
+  int rows;
+  int chunk;
+  int n_splits;
+  int max_splits;
+};
+void pv_full_launch(const PvFullParams& p, int dtype, cudaStream_t st);
+
+// Position-major [rows][n_kv*h] input rows -> [b][n_kv][max_seq][h] storage
+// at positions [pos0, pos0 + rows/batch).
+struct AppendParams {
+  const void* src;
+  void* dst;
+  int64_t n_rows;         // m*batch
+  int64_t max_seq;
+  int64_t pos0;
+  int batch;
+  int n_kv;
+  int h;
+};
+void append_launch(const AppendParams& p, int src_dtype, int dst_dtype, cudaStream_t st);
+
+void fill_uniform_launch(void* dst, int dtype, uint64_t n, uint64_t seed, uint64_t offset, float lo,
+                         float hi, cudaStream_t st);
+// q of any dtype -> fp32
+void to_f32_launch(const void* src, int dtype, float* dst, int64_t n, cudaStream_t st);
+// [rows][nc] kv-head indices -> [rows*G][nc] q-head slots
+void expand_idx_launch(const uint32_t* src, uint32_t* dst, int rows, int G, int nc,
+                       cudaStream_t st);
+
+// (slot row, position) pairs of a [rows][max_seq][h] store -> fp32 [n][h]
+void gather_rows_launch(const void* base, int dtype, const uint32_t* slot_row, const uint32_t* pos,
+                        int64_t n, int h, int64_t max_seq, float* out, cudaStream_t st);
+
+}  // namespace kc

@@ -1,0 +1,381 @@
+// kc_recall.cu -- V recall + P.V, the full-attention comparator's P.V, and
+// the store's append/convert kernels (sm_100a).
+//
+// recall_pv_kernel replaces gather_v (proj/core/src/kv_cache.cpp:150-187) and
+// the P.V loop + add_scaled (proj/core/src/attention.cpp:159-188, :23-27).
+// One CTA per (batch, kv head): the N selected V rows (256 B each at h=128,
+// fp16) are pulled from the layer's V storage -- pinned, device-mapped host
+// memory for offloaded layers (zero-copy PCIe reads, 16 B per lane, a whole
+// chunk of rows in flight per CTA) or HBM for resident layers -- into shared
+// memory, then every (q head, column) thread accumulates sum_r w_r * v_r[c]
+// in ascending position order with separately rounded multiply and add
+// (__fmul_rn/__fadd_rn), i.e. the same operation sequence as the reference's
+// `acc[c] += w * v[c]` compiled with -ffp-contract=off. `reverse` is the
+// reference's ordered_accumulation=false fault hook.
+#include <algorithm>
+
+#include "kc_device.cuh"
+#include "kc_kernels.cuh"
+#include "kcache_c.h"
+
+namespace kc {
+
+namespace {
+
+constexpr int kRecallThreads = 256;
+constexpr int kRecallSmem = 40 * 1024;
+
+template <typename T>
+__global__ void __launch_bounds__(kRecallThreads) recall_pv_kernel(const RecallParams p, int rc_max) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int row = p.row_offset + blockIdx.x;
+  const int b = row / p.n_kv;
+  const int kvh = row - b * p.n_kv;
+  const int G = p.G, h = p.h, n_q = p.n_kv * G, nc = p.nc;
+  const int tid = threadIdx.x;
+  const size_t rowb = (size_t)h * sizeof(T);
+  T* vbuf = reinterpret_cast<T*>(smem);
+  float* wbuf = reinterpret_cast<float*>(smem + (((size_t)rc_max * rowb + 15) & ~size_t(15)));
+  const T* vslot = static_cast<const T*>(p.v) + (size_t)row * p.max_seq * h;
+  const uint32_t* idx = p.idx + (size_t)row * nc;
+  const int n_out = G * h;
+  constexpr int kMaxOut = 4;  // G*h <= 1024
+  float acc[kMaxOut];
+#pragma unroll
+  for (int i = 0; i < kMaxOut; ++i) acc[i] = 0.0f;
+
+  const int n_chunks = (nc + rc_max - 1) / rc_max;
+  for (int ci = 0; ci < n_chunks; ++ci) {
+    const int chunk = p.reverse ? (n_chunks - 1 - ci) : ci;
+    const int c0 = chunk * rc_max;
+    const int rc = min(rc_max, nc - c0);
+    // ---- recall: selected rows -> shared memory ----
+    if ((rowb & 15) == 0) {
+      const int vpr = (int)(rowb >> 4);
+      const int total = rc * vpr;
+      uint4* dst = reinterpret_cast<uint4*>(vbuf);
+      constexpr int kBatch = 8;
+      for (int v0 = tid; v0 < total; v0 += kRecallThreads * kBatch) {
+        uint4 tmp[kBatch];
+#pragma unroll
+        for (int u = 0; u < kBatch; ++u) {
+          const int v = v0 + u * kRecallThreads;
+          if (v < total) {
+            const int r = v / vpr, part = v - r * vpr;
+            tmp[u] = *(reinterpret_cast<const uint4*>(vslot + (size_t)idx[c0 + r] * h) + part);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kBatch; ++u) {
+          const int v = v0 + u * kRecallThreads;
+          if (v < total) dst[v] = tmp[u];
+        }
+      }
+    } else {
+      for (int e = tid; e < rc * h; e += kRecallThreads) {
+        const int r = e / h, c = e - r * h;
+        vbuf[e] = vslot[(size_t)idx[c0 + r] * h + c];
+      }
+    }
+    // ---- weights (raw p, or p * (1/sum p) when renormalising) ----
+    for (int e = tid; e < G * rc; e += kRecallThreads) {
+      const int g = e / rc, r = e - g * rc;
+      const size_t slot = (size_t)b * n_q + kvh * G + g;
+      float w = p.w[slot * nc + c0 + r];
+      if (p.renormalize) w = __fmul_rn(w, p.norm[slot]);
+      wbuf[g * rc_max + r] = w;
+    }
+    __syncthreads();
+    // ---- P.V, fixed position order per output element ----
+#pragma unroll
+    for (int i = 0; i < kMaxOut; ++i) {
+      const int o = tid + i * kRecallThreads;
+      if (o < n_out) {
+        const int g = o / h, c = o - g * h;
+        const float* wg = wbuf + g * rc_max;
+        float a = acc[i];
+        if (!p.reverse) {
+          for (int r = 0; r < rc; ++r) a = __fadd_rn(a, __fmul_rn(wg[r], to_f32<T>(vbuf[r * h + c])));
+        } else {
+          for (int r = rc - 1; r >= 0; --r)
+            a = __fadd_rn(a, __fmul_rn(wg[r], to_f32<T>(vbuf[r * h + c])));
+        }
+        acc[i] = a;
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < kMaxOut; ++i) {
+    const int o = tid + i * kRecallThreads;
+    if (o < n_out) {
+      const int g = o / h, c = o - g * h;
+      p.out[((size_t)b * n_q + kvh * G + g) * h + c] = acc[i];
+    }
+  }
+}
+
+// decode_attention_full P.V: CTA (split, row) accumulates its positions in
+// order with the global softmax weights; pv_reduce sums splits in order.
+template <typename T>
+__global__ void __launch_bounds__(256) pv_full_kernel(const PvFullParams p) {
+  extern __shared__ float sh[];  // M[G], Z[G], w[G][chunk]
+  const int split = blockIdx.x, row = blockIdx.y;
+  const int b = row / p.n_kv, kvh = row - b * p.n_kv;
+  const int G = p.G, h = p.h, n_q = p.n_kv * G;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  float* sM = sh;
+  float* sZ = sh + G;
+  float* wb = sh + 2 * G;
+  for (int g = warp; g < G; g += 8) {
+    const float2* part = p.partials + ((size_t)b * n_q + kvh * G + g) * p.max_splits;
+    float m = -INFINITY;
+    for (int i = lane; i < p.n_splits; i += 32) m = fmaxf(m, part[i].x);
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) {
+      float z = 0.0f;
+      for (int i = 0; i < p.n_splits; ++i) {
+        const float2 ml = part[i];
+        if (ml.y > 0.0f) z += ml.y * expf(ml.x - m);
+      }
+      sM[g] = m;
+      sZ[g] = z;
+    }
+  }
+  __syncthreads();
+  const int pos0 = split * p.chunk;
+  const int npos = min(p.chunk, p.s - pos0);
+  constexpr int kTile = 256;
+  const T* vslot = static_cast<const T*>(p.v) + ((size_t)row * p.max_seq + pos0) * h;
+  constexpr int kMaxOut = 4;  // G*h <= 1024
+  float acc[kMaxOut];
+#pragma unroll
+  for (int i = 0; i < kMaxOut; ++i) acc[i] = 0.0f;
+  for (int t0 = 0; t0 < npos; t0 += kTile) {
+    const int nt = min(kTile, npos - t0);
+    for (int e = tid; e < G * nt; e += 256) {
+      const int g = e / nt, j = e - g * nt;
+      const float* lrow = p.logits + ((size_t)b * n_q + kvh * G + g) * p.lstride;
+      wb[g * kTile + j] = expf(lrow[pos0 + t0 + j] - sM[g]) / sZ[g];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < kMaxOut; ++i) {
+      const int o = tid + i * 256;
+      if (o < G * h) {
+        const int g = o / h, c = o - g * h;
+        float a = acc[i];
+        for (int j = 0; j < nt; ++j)
+          a = __fadd_rn(a, __fmul_rn(wb[g * kTile + j], to_f32<T>(vslot[(size_t)(t0 + j) * h + c])));
+        acc[i] = a;
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < kMaxOut; ++i) {
+    const int o = tid + i * 256;
+    if (o < G * h) {
+      const int g = o / h, c = o - g * h;
+      p.part_out[(((size_t)b * n_q + kvh * G + g) * p.n_splits + split) * h + c] = acc[i];
+    }
+  }
+}
+
+__global__ void pv_reduce_kernel(const float* part, float* out, int slots, int n_splits, int h) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)slots * h) return;
+  const int64_t slot = e / h, c = e - slot * h;
+  float a = 0.0f;
+  for (int i = 0; i < n_splits; ++i) a += part[(slot * n_splits + i) * h + c];
+  out[slot * h + c] = a;
+}
+
+// ---- append: position-major rows -> [b][kv][pos][h] storage ----
+template <typename Ti, typename To>
+__global__ void append_kernel(const AppendParams p) {
+  const int64_t width = (int64_t)p.n_kv * p.h;
+  const int64_t n = p.n_rows * width;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / width, col = e - r * width;
+    const int64_t pos = p.pos0 + r / p.batch, bi = r % p.batch;
+    const int64_t kvh = col / p.h, c = col - kvh * p.h;
+    const float x = to_f32<Ti>(static_cast<const Ti*>(p.src)[e]);
+    static_cast<To*>(p.dst)[((bi * p.n_kv + kvh) * p.max_seq + pos) * p.h + c] = from_f32<To>(x);
+  }
+}
+
+// 8 consecutive elements of one head per thread (h % 8 == 0): 16-B stores.
+template <typename Ti, typename To>
+__global__ void append_vec8_kernel(const AppendParams p) {
+  const int64_t width = (int64_t)p.n_kv * p.h;
+  const int64_t n8 = p.n_rows * width / 8;
+  for (int64_t e8 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e8 < n8;
+       e8 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = e8 * 8;
+    const int64_t r = e / width, col = e - r * width;
+    const int64_t pos = p.pos0 + r / p.batch, bi = r % p.batch;
+    const int64_t kvh = col / p.h, c = col - kvh * p.h;
+    const Ti* s = static_cast<const Ti*>(p.src) + e;
+    To o[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) o[i] = from_f32<To>(to_f32<Ti>(s[i]));
+    To* d = static_cast<To*>(p.dst) + ((bi * p.n_kv + kvh) * p.max_seq + pos) * p.h + c;
+    if constexpr (sizeof(To) == 2) {
+      *reinterpret_cast<uint4*>(d) = *reinterpret_cast<const uint4*>(o);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) d[i] = o[i];
+    }
+  }
+}
+
+template <typename Ti, typename To>
+void append_typed(const AppendParams& p, cudaStream_t st) {
+  const int64_t n = p.n_rows * (int64_t)p.n_kv * p.h;
+  if (p.h % 8 == 0) {
+    const int64_t n8 = n / 8;
+    const int blocks = (int)std::min<int64_t>((n8 + 255) / 256, 148 * 16);
+    append_vec8_kernel<Ti, To><<<std::max(blocks, 1), 256, 0, st>>>(p);
+  } else {
+    const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
+    append_kernel<Ti, To><<<std::max(blocks, 1), 256, 0, st>>>(p);
+  }
+}
+
+template <typename Ti>
+void append_dst(const AppendParams& p, int dst_dtype, cudaStream_t st) {
+  switch (dst_dtype) {
+    case KC_F16: append_typed<Ti, __half>(p, st); break;
+    case KC_BF16: append_typed<Ti, __nv_bfloat16>(p, st); break;
+    default: append_typed<Ti, float>(p, st); break;
+  }
+}
+
+// SplitMix64 (rng.hpp:13-19) counter-indexed; next_uniform (rng.hpp:22-26)
+// with separately rounded multiply/add like the -ffp-contract=off host code.
+template <typename T>
+__global__ void fill_uniform_kernel(T* dst, uint64_t n, uint64_t seed, uint64_t offset, float lo,
+                                    float hi) {
+  const float span = __fsub_rn(hi, lo);
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t z = seed + (offset + i + 1) * 0x9e3779b97f4a7c15ull;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    z ^= z >> 31;
+    const double u = __dmul_rn((double)(z >> 11), 0x1.0p-53);
+    const float f = __double2float_rn(u);
+    dst[i] = from_f32<T>(__fadd_rn(lo, __fmul_rn(f, span)));
+  }
+}
+
+
+// gather_v slow path / k_row / v_row: listed (slot row, position) pairs -> fp32.
+template <typename T>
+__global__ void gather_rows_kernel(const T* base, const uint32_t* slot_row, const uint32_t* pos,
+                                   int64_t n, int h, int64_t max_seq, float* out) {
+  const int64_t total = n * h;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / h, c = e - i * h;
+    out[e] = to_f32<T>(base[((int64_t)slot_row[i] * max_seq + pos[i]) * h + c]);
+  }
+}
+
+int grid_for(int64_t n);
+
+template <typename T>
+__global__ void to_f32_kernel(const T* src, float* dst, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = to_f32<T>(src[i]);
+}
+
+__global__ void expand_idx_kernel(const uint32_t* src, uint32_t* dst, int rows, int G, int nc) {
+  const int64_t n = (int64_t)rows * G * nc;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t slot = e / nc, r = e - slot * nc;
+    dst[e] = src[(slot / G) * nc + r];
+  }
+}
+
+int grid_for(int64_t n) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 8));
+}
+
+}  // namespace
+
+void recall_launch(const RecallParams& p, int dtype, cudaStream_t st) {
+  const size_t esz = dtype == KC_F32 ? 4 : 2;
+  const size_t rowb = (size_t)p.h * esz;
+  int rc_max = (int)(kRecallSmem / (rowb + 4 * (size_t)p.G));
+  rc_max = std::max(1, std::min(rc_max, p.nc));
+  const size_t smem = ((rc_max * rowb + 15) & ~size_t(15)) + 4 * (size_t)p.G * rc_max;
+  switch (dtype) {
+    case KC_F16: recall_pv_kernel<__half><<<p.rows, kRecallThreads, smem, st>>>(p, rc_max); break;
+    case KC_BF16: recall_pv_kernel<__nv_bfloat16><<<p.rows, kRecallThreads, smem, st>>>(p, rc_max); break;
+    default: recall_pv_kernel<float><<<p.rows, kRecallThreads, smem, st>>>(p, rc_max); break;
+  }
+}
+
+void pv_full_launch(const PvFullParams& p, int dtype, cudaStream_t st) {
+  dim3 grid(p.n_splits, p.rows);
+  const size_t smem = (2 * (size_t)p.G + (size_t)p.G * 256) * sizeof(float);
+  switch (dtype) {
+    case KC_F16: pv_full_kernel<__half><<<grid, 256, smem, st>>>(p); break;
+    case KC_BF16: pv_full_kernel<__nv_bfloat16><<<grid, 256, smem, st>>>(p); break;
+    default: pv_full_kernel<float><<<grid, 256, smem, st>>>(p); break;
+  }
+  const int slots = (p.rows / p.n_kv) * p.n_kv * p.G;
+  pv_reduce_kernel<<<grid_for((int64_t)slots * p.h), 256, 0, st>>>(p.part_out, p.out, slots,
+                                                                    p.n_splits, p.h);
+}
+
+void append_launch(const AppendParams& p, int src_dtype, int dst_dtype, cudaStream_t st) {
+  switch (src_dtype) {
+    case KC_F16: append_dst<__half>(p, dst_dtype, st); break;
+    case KC_BF16: append_dst<__nv_bfloat16>(p, dst_dtype, st); break;
+    default: append_dst<float>(p, dst_dtype, st); break;
+  }
+}
+
+void fill_uniform_launch(void* dst, int dtype, uint64_t n, uint64_t seed, uint64_t offset, float lo,
+                         float hi, cudaStream_t st) {
+  const int g = grid_for((int64_t)std::min<uint64_t>(n, 1ull << 40));
+  switch (dtype) {
+    case KC_F16: fill_uniform_kernel<__half><<<g, 256, 0, st>>>((__half*)dst, n, seed, offset, lo, hi); break;
+    case KC_BF16: fill_uniform_kernel<__nv_bfloat16><<<g, 256, 0, st>>>((__nv_bfloat16*)dst, n, seed, offset, lo, hi); break;
+    default: fill_uniform_kernel<float><<<g, 256, 0, st>>>((float*)dst, n, seed, offset, lo, hi); break;
+  }
+}
+
+void to_f32_launch(const void* src, int dtype, float* dst, int64_t n, cudaStream_t st) {
+  switch (dtype) {
+    case KC_F16: to_f32_kernel<__half><<<grid_for(n), 256, 0, st>>>((const __half*)src, dst, n); break;
+    case KC_BF16: to_f32_kernel<__nv_bfloat16><<<grid_for(n), 256, 0, st>>>((const __nv_bfloat16*)src, dst, n); break;
+    default: cudaMemcpyAsync(dst, src, n * sizeof(float), cudaMemcpyDeviceToDevice, st); break;
+  }
+}
+
+void expand_idx_launch(const uint32_t* src, uint32_t* dst, int rows, int G, int nc, cudaStream_t st) {
+  expand_idx_kernel<<<grid_for((int64_t)rows * G * nc), 256, 0, st>>>(src, dst, rows, G, nc);
+}
+
+}  // namespace kc
+
+namespace kc {
+void gather_rows_launch(const void* base, int dtype, const uint32_t* slot_row, const uint32_t* pos,
+                        int64_t n, int h, int64_t max_seq, float* out, cudaStream_t st) {
+  if (n <= 0) return;
+  const int g = grid_for(n * h);
+  switch (dtype) {
+    case KC_F16: gather_rows_kernel<__half><<<g, 256, 0, st>>>((const __half*)base, slot_row, pos, n, h, max_seq, out); break;
+    case KC_BF16: gather_rows_kernel<__nv_bfloat16><<<g, 256, 0, st>>>((const __nv_bfloat16*)base, slot_row, pos, n, h, max_seq, out); break;
+    default: gather_rows_kernel<float><<<g, 256, 0, st>>>((const float*)base, slot_row, pos, n, h, max_seq, out); break;
+  }
+}
+}  // namespace kc

@@ -1,0 +1,273 @@
+// kc_score.cu -- split-sequence q.K^T scoring kernel (sm_100a).
+//
+// Replaces head_weights + dot_scaled (proj/core/src/attention.cpp:15-21,66-78)
+// and the max/sum half of softmax_inplace (proj/core/src/matrix.cpp:45-61).
+//
+// Grid (split, row): row = b*n_kv + kv_head, split = a chunk of positions.
+// The row's K for the chunk is one contiguous run of chunk*h elements in the
+// [b][kv][pos][h] arena, so a single elected thread streams it into a
+// 4-stage shared-memory ring with 1-D TMA bulk copies (cp.async.bulk, L2
+// evict-first) on mbarriers; eight consumer warps score 64-position stages
+// against every q head of the GQA group held in registers (the K tile is
+// read from HBM once per kv head, not once per q head). Each lane owns 128/LPR
+// elements of a row (LPR lanes per row, 16-B chunks rotated per row so a
+// quarter-warp's 16-B shared loads hit eight distinct bank groups), FMA in
+// fp32, log2(LPR) xor-shuffles per row. Writes fp32 logits (score * scale, the
+// multiply after the sum like dot_scaled) and a per-split online (max, sum
+// exp) per q head; select_kernel combines the splits into the global softmax.
+#include <algorithm>
+
+#include "kc_device.cuh"
+#include "kc_kernels.cuh"
+#include "kcache_c.h"
+
+namespace kc {
+
+namespace {
+
+constexpr int kRows = 64;     // positions per pipeline stage
+constexpr int kStages = 4;    // ring depth
+constexpr int kCWarps = 8;    // consumer warps
+constexpr int kH = 128;       // head_dim of the fast path
+
+__device__ __forceinline__ void named_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+template <int LPR>
+__device__ __forceinline__ int chunk_of(int ci, int rl, int sub) {
+  if constexpr (LPR == 4) {
+    return ((ci ^ (rl & 1)) << 2) | sub;
+  } else {
+    return ci * LPR + sub;
+  }
+}
+
+template <typename T, int G, int LPR>
+__global__ void __launch_bounds__((kCWarps + 1) * 32)
+    score_fast_kernel(const ScoreParams p) {
+  constexpr int CPL = 16 / LPR;            // 16-B chunks per lane per row
+  constexpr int RPP = 32 / LPR;            // rows per warp pass
+  constexpr int PASSES = (kRows / kCWarps) / RPP;
+  constexpr int ROWB = kH * (int)sizeof(T);  // 256 B
+  static_assert(G <= LPR, "one writer lane per q head");
+
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint8_t* ring = smem;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kRows * ROWB);
+  uint64_t* empty = full + kStages;
+  float2* red = reinterpret_cast<float2*>(empty + kStages);  // [kCWarps][G]
+
+  const int split = blockIdx.x;
+  const int row = blockIdx.y;
+  const int b = row / p.n_kv;
+  const int kvh = row - b * p.n_kv;
+  const int pos0 = split * p.chunk;
+  const int npos = min(p.chunk, p.s - pos0);
+  const int n_it = (npos + kRows - 1) / kRows;
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int st = 0; st < kStages; ++st) {
+      mbar_init(&full[st], 1);
+      mbar_init(&empty[st], kCWarps);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp == kCWarps) {
+    // ---------------- producer: one elected lane streams K ----------------
+    if (lane == 0) {
+      const T* kslot = static_cast<const T*>(p.k) + (size_t)row * p.max_seq * kH;
+      const uint64_t pol = l2_evict_first_policy();
+      for (int it = 0; it < n_it; ++it) {
+        const int st = it % kStages;
+        if (it >= kStages) mbar_wait(&empty[st], ((it / kStages) - 1) & 1);
+        const int rows = min(kRows, npos - it * kRows);
+        const uint32_t bytes = (uint32_t)(rows * ROWB);
+        mbar_arrive_expect_tx(&full[st], bytes);
+        tma_bulk_g2s(ring + st * kRows * ROWB, kslot + (size_t)(pos0 + it * kRows) * kH, bytes,
+                     &full[st], pol);
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumers ----------------
+  const int sub = lane % LPR;
+  const int rl = lane / LPR;
+  const int n_q = p.n_kv * G;
+  float qf[G][CPL][8];
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    const float* qh = p.q + ((size_t)b * n_q + kvh * G + g) * kH;
+#pragma unroll
+    for (int ci = 0; ci < CPL; ++ci) {
+      const int c = chunk_of<LPR>(ci, rl, sub);
+      const float4 a = *reinterpret_cast<const float4*>(qh + c * 8);
+      const float4 bq = *reinterpret_cast<const float4*>(qh + c * 8 + 4);
+      qf[g][ci][0] = a.x; qf[g][ci][1] = a.y; qf[g][ci][2] = a.z; qf[g][ci][3] = a.w;
+      qf[g][ci][4] = bq.x; qf[g][ci][5] = bq.y; qf[g][ci][6] = bq.z; qf[g][ci][7] = bq.w;
+    }
+  }
+  float m_run = -INFINITY, l_run = 0.0f;
+  float* lrow = p.logits + ((size_t)b * n_q + kvh * G + (sub < G ? sub : 0)) * p.lstride + pos0;
+
+  for (int it = 0; it < n_it; ++it) {
+    const int st = it % kStages;
+    mbar_wait(&full[st], (it / kStages) & 1);
+    const uint8_t* sb = ring + st * kRows * ROWB;
+#pragma unroll
+    for (int pass = 0; pass < PASSES; ++pass) {
+      const int r = warp * (kRows / kCWarps) + pass * RPP + rl;
+      const int pl = it * kRows + r;
+      const uint4* srow = reinterpret_cast<const uint4*>(sb + r * ROWB);
+      float acc[G];
+#pragma unroll
+      for (int g = 0; g < G; ++g) acc[g] = 0.0f;
+#pragma unroll
+      for (int ci = 0; ci < CPL; ++ci) {
+        const uint4 raw = srow[chunk_of<LPR>(ci, rl, sub)];
+        float kf[8];
+        unpack8<T>(raw, kf);
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) acc[g] = fmaf(qf[g][ci][e], kf[e], acc[g]);
+        }
+      }
+#pragma unroll
+      for (int o = LPR / 2; o >= 1; o >>= 1) {
+#pragma unroll
+        for (int g = 0; g < G; ++g) acc[g] += __shfl_xor_sync(0xffffffffu, acc[g], o);
+      }
+      float mine = acc[0];
+#pragma unroll
+      for (int g = 1; g < G; ++g) mine = (sub == g) ? acc[g] : mine;
+      const float sc = mine * p.scale;
+      if (pl < npos && sub < G) {
+        lrow[pl] = sc;
+        if (sc > m_run) {
+          l_run = l_run * expf(m_run - sc) + 1.0f;
+          m_run = sc;
+        } else {
+          l_run += expf(sc - m_run);
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
+  }
+
+  // per-split (max, sum exp) per q head: lanes with equal `sub`, then warps
+#pragma unroll
+  for (int o = LPR; o < 32; o <<= 1) {
+    const float m2 = __shfl_xor_sync(0xffffffffu, m_run, o);
+    const float l2 = __shfl_xor_sync(0xffffffffu, l_run, o);
+    ml_combine(m_run, l_run, m2, l2);
+  }
+  if (lane < G) red[warp * G + lane] = make_float2(m_run, l_run);
+  named_sync(1, kCWarps * 32);
+  if (threadIdx.x < G) {
+    const int g = threadIdx.x;
+    float m = -INFINITY, l = 0.0f;
+    for (int w = 0; w < kCWarps; ++w) ml_combine(m, l, red[w * G + g].x, red[w * G + g].y);
+    p.partials[((size_t)b * n_q + kvh * G + g) * p.max_splits + split] = make_float2(m, l);
+  }
+}
+
+// Any dtype / head_dim / group size: one warp per position, lane-strided dot.
+template <typename T>
+__global__ void __launch_bounds__(256) score_generic_kernel(const ScoreParams p) {
+  extern __shared__ float2 wstat[];  // [8][G]
+  const int split = blockIdx.x;
+  const int row = blockIdx.y;
+  const int b = row / p.n_kv;
+  const int kvh = row - b * p.n_kv;
+  const int G = p.G, h = p.h, n_q = p.n_kv * G;
+  const int pos0 = split * p.chunk;
+  const int npos = min(p.chunk, p.s - pos0);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const T* kslot = static_cast<const T*>(p.k) + (size_t)row * p.max_seq * h;
+  for (int g = lane; g < G; g += 32) wstat[warp * G + g] = make_float2(-INFINITY, 0.0f);
+  __syncwarp();
+  for (int pl = warp; pl < npos; pl += 8) {
+    const T* krow = kslot + (size_t)(pos0 + pl) * h;
+    for (int g = 0; g < G; ++g) {
+      const float* qh = p.q + ((size_t)b * n_q + kvh * G + g) * h;
+      float acc = 0.0f;
+      for (int c = lane; c < h; c += 32) acc = fmaf(qh[c], to_f32<T>(krow[c]), acc);
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (lane == 0) {
+        const float sc = acc * p.scale;
+        p.logits[((size_t)b * n_q + kvh * G + g) * p.lstride + pos0 + pl] = sc;
+        float2 ml = wstat[warp * G + g];
+        ml_combine(ml.x, ml.y, sc, 1.0f);
+        wstat[warp * G + g] = ml;
+      }
+    }
+  }
+  __syncthreads();
+  for (int g = threadIdx.x; g < G; g += blockDim.x) {
+    float m = -INFINITY, l = 0.0f;
+    for (int w = 0; w < 8; ++w) ml_combine(m, l, wstat[w * G + g].x, wstat[w * G + g].y);
+    p.partials[((size_t)b * n_q + kvh * G + g) * p.max_splits + split] = make_float2(m, l);
+  }
+}
+
+template <typename T, int G, int LPR>
+void launch_fast(const ScoreParams& p, cudaStream_t st) {
+  constexpr int ROWB = kH * (int)sizeof(T);
+  const size_t smem = kStages * kRows * ROWB + 2 * kStages * sizeof(uint64_t) +
+                      kCWarps * G * sizeof(float2);
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(score_fast_kernel<T, G, LPR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    configured = true;
+  }
+  dim3 grid(p.n_splits, p.rows);
+  score_fast_kernel<T, G, LPR><<<grid, (kCWarps + 1) * 32, smem, st>>>(p);
+}
+
+template <typename T>
+bool try_fast(const ScoreParams& p, cudaStream_t st) {
+  if (p.h != kH || (p.chunk % kRows) != 0) return false;
+  switch (p.G) {
+    case 1: launch_fast<T, 1, 4>(p, st); return true;
+    case 2: launch_fast<T, 2, 4>(p, st); return true;
+    case 4: launch_fast<T, 4, 8>(p, st); return true;
+    case 8: launch_fast<T, 8, 16>(p, st); return true;
+    default: return false;
+  }
+}
+
+}  // namespace
+
+int score_pick_chunk(int s, int rows, int override_chunk) {
+  if (override_chunk > 0) return ((override_chunk + kRows - 1) / kRows) * kRows;
+  // ~6 resident CTAs per SM x 148 SMs per wave; chunks of 256..2048 positions.
+  const long long work = (long long)s * rows;
+  long long c = (work + 148LL * 6 - 1) / (148LL * 6);
+  c = std::max<long long>(256, std::min<long long>(2048, c));
+  c = ((c + kRows - 1) / kRows) * kRows;
+  return (int)c;
+}
+
+void score_launch(const ScoreParams& p, int dtype, cudaStream_t st) {
+  if (dtype == KC_F16 && try_fast<__half>(p, st)) return;
+  if (dtype == KC_BF16 && try_fast<__nv_bfloat16>(p, st)) return;
+  dim3 grid(p.n_splits, p.rows);
+  const size_t smem = 8 * (size_t)p.G * sizeof(float2);
+  switch (dtype) {
+    case KC_F16: score_generic_kernel<__half><<<grid, 256, smem, st>>>(p); break;
+    case KC_BF16: score_generic_kernel<__nv_bfloat16><<<grid, 256, smem, st>>>(p); break;
+    default: score_generic_kernel<float><<<grid, 256, smem, st>>>(p); break;
+  }
+}
+
+}  // namespace kc
