@@ -1,0 +1,373 @@
+#!/usr/bin/env python
+"""KCache decode-attention benchmark (BASELINE.json metric).
+
+Metric: "KCache decode-attn tokens/s/GPU, LLaMA2-7B shape 32k ctx; % of
+HBM+H2D roofline". One step = decode_attention_topn for every layer of one
+decode token of the whole batch: q.K^T scoring over the HBM-resident K cache,
+top-N selection, recall of the selected V rows from pinned host memory, P.V
+(SURVEY.md section 8(d)). tokens/s = batch / step time.
+
+Default workload (N=1): configs[1] -- LLaMA2-7B shape, 32 layers, batch 8,
+32k context, N=128, fp16 K in HBM (64 GiB) and fp16 V in pinned host memory
+(64 GiB), synthetic SeededRng inputs. Inputs (64 GiB of K) dwarf the 126 MB
+L2, so no flush is needed between steps.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c3|c1]
+    python bench.py --impl reference ...   # the reference CPU path, all host cores
+
+Multi-GPU (torchrun): one process per GPU, each with its own batch of
+sequences and its own K/V shards (partition by request batch, no collective on
+the data path): weak scaling, value = all ranks' tokens / max-over-ranks time.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    "c2": dict(workload="LLaMA2-7B-shape KCache decode attention: 32 layers, batch 8, 32k context, N=128, "
+                        "fp16 K in HBM / fp16 V in pinned host memory",
+               n_layers=32, batch=8, n_heads=32, n_kv=32, h=128, s=32768, top_n=128),
+    "c3": dict(workload="LLaMA3-8B-shape GQA (32 q / 8 kv heads) KCache decode attention: 32 layers, batch 32, "
+                        "16k context, N=128",
+               n_layers=32, batch=32, n_heads=32, n_kv=8, h=128, s=16384, top_n=128),
+    "c1": dict(workload="LLaMA2-7B-shape single attention layer, batch 1, 4k context, N=128",
+               n_layers=1, batch=1, n_heads=32, n_kv=32, h=128, s=4096, top_n=128),
+}
+METRIC = "KCache decode-attn tokens/s/GPU, LLaMA2-7B shape 32k ctx; % of HBM+H2D roofline"
+UNIT = "tokens/s"
+SEED_Q, SEED_K, SEED_V = 1, 2, 3
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)),
+            int(os.environ.get("WORLD_SIZE", 1)))
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu):
+        self.gpu = gpu
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-lms", "200", "-i", str(self.gpu)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out, _ = self.proc.communicate()
+        rows = [r.split(",") for r in out.strip().splitlines() if r.count(",") >= 8]
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows if r[1].strip().replace(".", "").isdigit()]
+        smax = max(float(r[2]) for r in rows)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].strip() == "Active"})
+        load = [x for x in sm if x > 0.5 * smax] or sm
+        return {"sm_mhz": statistics.median(load), "sm_max_mhz": smax, "reasons": reasons, "samples": len(rows)}
+
+
+def h2d_bandwidth(torch):
+    """Pinned cudaMemcpyAsync of 256 MiB, best of 10 (SURVEY 8(d) BW_H2D)."""
+    n = 256 << 20
+    src = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    dst = torch.empty(n, dtype=torch.uint8, device="cuda")
+    for _ in range(3):
+        dst.copy_(src, non_blocking=True)
+    torch.cuda.synchronize()
+    best = 1e9
+    for _ in range(10):
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        dst.copy_(src, non_blocking=True)
+        b.record()
+        b.synchronize()
+        best = min(best, a.elapsed_time(b))
+    del src, dst
+    return n / (best * 1e-3) / 1e9
+
+
+def cpu_reference_sample(cfg, threads, passes, warm=1):
+    """The reference decode_attention_topn (oracle/_ref) on host threads over
+    one layer of the workload (all batch rows, all heads); returns
+    (seconds per layer-pass list, kind, sample text)."""
+    from oracle.oracle import Reference, ReferenceBench
+    if cfg["n_kv"] != cfg["n_heads"] or not Reference.available():
+        return None
+    hps = 16 if cfg["n_heads"] % 16 == 0 else cfg["n_heads"]
+    rb = ReferenceBench(cfg["s"], cfg["batch"], cfg["n_heads"], cfg["h"], hps, cfg["top_n"], threads,
+                        seeds=(SEED_Q, SEED_K, SEED_V))
+    try:
+        for _ in range(warm):
+            rb.run()
+        times = [rb.run()[0] for _ in range(passes)]
+    finally:
+        rb.close()
+    sample = (f"reference decode_attention_topn (oracle/_ref, -O3 -ffp-contract=off) on 1 of {cfg['n_layers']} "
+              f"layers x {cfg['batch']} rows x {cfg['n_heads']} heads at s={cfg['s']}, N={cfg['top_n']}, "
+              f"{threads} threads over {cfg['batch'] * cfg['n_heads'] // hps} (row, 16-head) shards; "
+              f"step time = layer time x {cfg['n_layers']}")
+    return times, "reference", sample
+
+
+def run_reference_arm(args, cfg):
+    rank, _, world = dist_env()
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    res = cpu_reference_sample(cfg, threads, passes=args.steps, warm=args.warmup)
+    if res is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built or config is GQA (reference is MHA-only)"}))
+        return
+    times, kind, sample = res
+    t_layer = statistics.mean(times)
+    value = cfg["batch"] / (t_layer * cfg["n_layers"])
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_layer * cfg["n_layers"] * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (SeededRng, fp16-rounded, fed as fp32)",
+        "config": {"workload": cfg["workload"], "layers": cfg["n_layers"], "batch": cfg["batch"], "s": cfg["s"],
+                   "top_n": cfg["top_n"]},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, cfg):
+    import numpy as np
+    import torch
+
+    from paper_2404_18057_b200 import kcache as kc
+
+    rank, local_rank, world = dist_env()
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+
+    L, b, n, n_kv, h, s, N = (cfg[k] for k in ("n_layers", "batch", "n_heads", "n_kv", "h", "s", "top_n"))
+    G = n // n_kv
+    d = n * h
+    nc = min(N, s)
+    slots = b * n
+    mcfg = kc.ModelConfig(L, d, n, h, kc.ModelConfig.default_ffn_hidden(d), 32000, s, n_kv)
+    t0 = time.time()
+    cache = kc.TieredKVCache(mcfg, b, kc.TierPlacement.kcache(0, L, 2, "f16"), device=local_rank)
+    for kv in args.tune:
+        key, val = kv.split("=")
+        cache.set_tuning(key, int(val))
+    rows = s * b
+    kbuf = torch.empty(rows, n_kv * h, dtype=torch.float16, device=dev)
+    vbuf = torch.empty_like(kbuf)
+    seed_off = 1_000_003 * rank
+    for layer in range(L):
+        kc.fill_uniform(kbuf, SEED_K + 100 * layer + seed_off)
+        kc.fill_uniform(vbuf, SEED_V + 100 * layer + seed_off)
+        cache.append_kv_device(layer, kbuf, vbuf)
+    torch.cuda.synchronize()
+    del kbuf, vbuf
+    torch.cuda.empty_cache()
+    for layer in range(L):
+        cache.offload_prefill_v(layer)
+    cache.begin_decode()
+    setup_s = time.time() - t0
+
+    qs = []
+    for layer in range(L):
+        q16 = torch.empty(b, d, dtype=torch.float16, device=dev)
+        kc.fill_uniform(q16, SEED_Q + 100 * layer + seed_off)
+        qs.append(q16.float())
+    outs = [{"out": torch.empty(b, d, dtype=torch.float32, device=dev),
+             "indices": torch.empty(slots, nc, dtype=torch.int32, device=dev),
+             "weights": torch.empty(slots, nc, dtype=torch.float32, device=dev),
+             "dropped": torch.empty(slots, dtype=torch.float64, device=dev)} for _ in range(L)]
+    layers = list(range(L))
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    def step():
+        return cache.decode_topn_layers_device(layers, qs, N, outs, stream=stream)
+
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    cache.profile(True)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        info = step()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    ms_local = ev0.elapsed_time(ev1) / args.steps
+    score_ms, score_n = cache.profile_read("score")
+    select_ms, select_n = cache.profile_read("select")
+    recall_ms, recall_n = cache.profile_read("recall")
+    cache.profile(False)
+    h2d_per_layer = info[0][1]
+
+    # ---- end to end: host (pinned) q in, every output back to the host ----
+    qh = [torch.empty(b, d, dtype=torch.float32, pin_memory=True) for _ in range(L)]
+    for i in range(L):
+        qh[i].copy_(qs[i])
+    qh_np = [t.numpy() for t in qh]
+    outs_h = [{"out": torch.empty(b, d, dtype=torch.float32, pin_memory=True).numpy(),
+               "indices": torch.empty(slots, nc, dtype=torch.int32, pin_memory=True).numpy(),
+               "weights": torch.empty(slots, nc, dtype=torch.float32, pin_memory=True).numpy(),
+               "dropped": torch.empty(slots, dtype=torch.float64, pin_memory=True).numpy()} for _ in range(L)]
+    e2e_steps = 0 if args.no_e2e else args.steps
+    for _ in range(args.warmup if e2e_steps else 0):
+        cache.decode_topn_layers_host(layers, qh_np, N, outs_h)
+    barrier()
+    te0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        cache.decode_topn_layers_host(layers, qh_np, N, outs_h)
+    te1 = time.perf_counter()
+    barrier()
+    e2e_ms_local = (te1 - te0) * 1e3 / max(e2e_steps, 1)
+    clocks = sampler.stop()
+    h2d_bw = h2d_bandwidth(torch) if rank == 0 else None
+    e2e_check = float(np.abs(outs_h[0]["out"]).sum())
+    del outs_h, qh, qh_np
+
+    ms = ms_local
+    e2e_ms = e2e_ms_local
+    if world > 1:
+        t = torch.tensor([ms_local, e2e_ms_local], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms, e2e_ms = float(t[0]), float(t[1])
+    cache.close()
+    del qs, outs
+    torch.cuda.empty_cache()
+
+    if rank != 0:
+        if world > 1:
+            torch.distributed.destroy_process_group()
+        return
+
+    hbm_peak, peak_kind = measured_peaks()
+    k_bytes_layer = 2 * b * n_kv * s * h
+    v_bytes_layer = 2 * b * n_kv * nc * h
+    score_avg_ms = score_ms / max(score_n, 1)
+    achieved = k_bytes_layer / (score_avg_ms * 1e-3) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_score_summary.json")) as f:
+            prof = json.load(f)
+        if prof.get("config") == args.config:
+            traffic = prof.get("dram_bytes_per_launch")
+    except Exception:
+        pass
+    t_k = L * k_bytes_layer / (hbm_peak * 1e9)
+    t_v = L * v_bytes_layer / (h2d_bw * 1e9)
+    value = world * b / (ms * 1e-3)
+    e2e_value = world * b / (e2e_ms * 1e-3)
+    launches_per_layer = 3 + (1 if G > 1 else 0)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f16 storage / f32 accumulate",
+        "data": "synthetic (SeededRng SplitMix64 U[-1,1], fp16-rounded)",
+        "config": {"workload": cfg["workload"], "config": args.config, "layers": L, "batch_per_gpu": b,
+                   "global_batch": b * world, "n_heads": n, "n_kv_heads": n_kv, "head_dim": h, "s": s, "top_n": N,
+                   "parallelism": f"partition by request batch x{world}, no data-path collective",
+                   "l2": "inputs larger than L2 (64 GiB K per GPU)", "pipeline": "recall(l) overlaps scoring(l+1)"},
+        "per_gpu_tokens_per_s": value / world,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": achieved / hbm_peak, "traffic": traffic, "peak_kind": peak_kind,
+                     "kernel": "score_fast_kernel (q.K^T, TMA bulk-staged K)",
+                     "algorithmic_bytes_per_launch": k_bytes_layer, "avg_launch_ms": score_avg_ms},
+        "step_roofline": {"k_bytes_per_step": L * k_bytes_layer, "vsel_bytes_per_step": L * v_bytes_layer,
+                          "hbm_gbs": hbm_peak, "h2d_gbs_measured": h2d_bw,
+                          "t_roof_sum_ms": (t_k + t_v) * 1e3, "t_roof_max_ms": max(t_k, t_v) * 1e3,
+                          "frac_of_sum_roofline": (t_k + t_v) * 1e3 / ms,
+                          "frac_of_max_roofline": max(t_k, t_v) * 1e3 / ms},
+        "kernel_ms_per_step": {"score": score_ms / args.steps, "select": select_ms / args.steps,
+                               "recall_pv": recall_ms / args.steps},
+        "h2d_ledger_bytes_per_layer": h2d_per_layer,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": L * b * d * 4,
+                "d2h_bytes_per_step": L * (b * d * 4 + slots * nc * 8 + slots * 8), "ms_per_step": e2e_ms,
+                "path": "kc_decode_topn_layers with pinned host q / outputs (TieredKVCache.decode_topn_layers_host)"},
+        "gpu_launches": launches_per_layer * L * args.steps,
+        "clocks": clocks,
+        "setup_s": setup_s,
+        "e2e_checksum": e2e_check,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        res = cpu_reference_sample(cfg, os.cpu_count() or 1, passes=1)
+        if res is not None:
+            times, kind, sample = res
+            cpu_val = b / (statistics.mean(times) * L)
+            line["cpu_baseline"] = {"value": cpu_val, "unit": UNIT, "cores": os.cpu_count() or 1, "kind": kind,
+                                    "sample": sample}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--topn", type=int, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--tune", action="append", default=[], help="kc_set_tuning key=value")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    cfg = dict(CONFIGS[args.config])
+    if args.topn:
+        cfg["top_n"] = args.topn
+    if args.impl == "reference":
+        run_reference_arm(args, cfg)
+    else:
+        run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

@@ -158,6 +158,15 @@ int kc_sync(kc_cache* cache);
 /* Tuning knobs ("score_chunk", "recall_ctas", ...); DESIGN.md lists them. */
 int kc_set_tuning(kc_cache* cache, const char* key, int64_t value);
 
+/* Per-kernel CUDA-event timing of subsequent decode calls (bench / roofline):
+ * kc_profile(c, 1) clears and starts recording one event pair around every
+ * scoring, selection and recall launch on the stream it runs on;
+ * kc_profile_read(c, "score"|"select"|"recall", ...) returns the summed
+ * device time and the launch count. */
+int kc_profile(kc_cache* cache, int enable);
+int kc_profile_read(kc_cache* cache, const char* kernel, double* total_ms, uint64_t* launches);
+int kc_profile_launch(kc_cache* cache, const char* kernel, uint64_t i, double* ms);
+
 /* arg_topk (matrix.hpp:49-52, matrix.cpp:109-122) on the GPU: indices of the
  * k largest of n host floats, ties to the lowest index, ascending. */
 int kc_arg_topk(const float* values, uint64_t n, uint64_t k, uint32_t* out, uint64_t* count);

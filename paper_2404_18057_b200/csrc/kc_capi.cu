@@ -21,6 +21,9 @@
 #include <string>
 #include <vector>
 
+#include <memory>
+
+#include "kc_gather.hpp"
 #include "kc_kernels.cuh"
 #include "kcache_c.h"
 
@@ -108,11 +111,16 @@ struct LedgerEvent {
 
 struct LayerState {
   uint64_t len = 0;
+  uint64_t clean_len = 0;  // K positions written back to DRAM (safe to drop from L2)
   bool offloaded = false;
   uint64_t k_elems = 0, vfast_elems = 0, vslow_elems = 0;
 };
 
-constexpr int kRing = 2;
+constexpr int kRing = 3;
+
+// V recall strategies for offloaded layers (kc_set_tuning "recall_mode"):
+// the host-compaction + DMA path is the default (see kc_gather.hpp).
+constexpr int kRecallAuto = 0, kRecallZeroCopy = 1, kRecallDma = 2;
 
 bool host_pinned(const void* p) {
   cudaPointerAttributes a{};
@@ -154,12 +162,48 @@ struct kc_cache {
   DevBuf logits, partials, keys, part_out, stage_src, stage_k, stage_v, sel_rows, sel_pos, gather_out;
   DevBuf q32[kRing], idx[kRing], w[kRing], dropped[kRing], norm[kRing], out_tmp[kRing], idx_exp[kRing];
   PinnedBuf host_in, host_out;
-  cudaStream_t main_st = nullptr, side_st = nullptr;
-  cudaEvent_t ev_start = nullptr, ev_end = nullptr, ev_sel[kRing] = {}, ev_rec[kRing] = {};
+  // DMA recall: pinned copy of the selection, pinned compacted rows, HBM copy
+  PinnedBuf idx_host[kRing], stage_host[kRing];
+  DevBuf stage_dev[kRing];
+  std::unique_ptr<kc::GatherPool> pool;
+  cudaStream_t main_st = nullptr, side_st = nullptr, gather_st = nullptr;
+  cudaEvent_t ev_start = nullptr, ev_end = nullptr, ev_sel[kRing] = {}, ev_rec[kRing] = {},
+              ev_gath[kRing] = {};
 
   // tuning
   int score_chunk = 0;
   int pipeline = 1;
+  int recall_mode = kRecallAuto;
+  int discard = 1;
+  int select_global = 0;
+  int gather_threads = 0;  // 0: min(8, cores/2)
+
+  // per-kernel CUDA-event timing (kc_profile): [kind] -> (start, stop) pairs
+  bool prof_on = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof[3];
+  std::vector<cudaEvent_t> prof_pool;
+  size_t prof_used = 0;
+  cudaEvent_t prof_event() {
+    if (prof_used == prof_pool.size()) {
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      prof_pool.push_back(e);
+    }
+    return prof_pool[prof_used++];
+  }
+  // record around one launch when profiling is on
+  template <typename F>
+  void timed(int kind, cudaStream_t st, F&& launch) {
+    if (!prof_on) {
+      launch();
+      return;
+    }
+    cudaEvent_t a = prof_event(), b = prof_event();
+    CK(cudaEventRecord(a, st));
+    launch();
+    CK(cudaEventRecord(b, st));
+    prof[kind].push_back({a, b});
+  }
 
   void* k_layer(uint64_t layer) const { return (char*)k_arena + layer * k_layer_bytes; }
   void* v_layer(uint64_t layer) const {
@@ -234,7 +278,16 @@ void destroy(kc_cache* c) {
   cudaSetDevice(c->device);
   if (c->main_st) cudaStreamSynchronize(c->main_st);
   if (c->side_st) cudaStreamSynchronize(c->side_st);
+  if (c->gather_st) cudaStreamSynchronize(c->gather_st);
   cudaDeviceSynchronize();
+  c->pool.reset();
+  for (int i = 0; i < kRing; ++i) {
+    c->idx_host[i].release();
+    c->stage_host[i].release();
+    c->stage_dev[i].release();
+    if (c->ev_gath[i]) cudaEventDestroy(c->ev_gath[i]);
+  }
+  if (c->gather_st) cudaStreamDestroy(c->gather_st);
   if (c->k_arena) cudaFree(c->k_arena);
   if (c->v_dev) cudaFree(c->v_dev);
   if (c->v_host) {
@@ -252,6 +305,7 @@ void destroy(kc_cache* c) {
   }
   c->host_in.release();
   c->host_out.release();
+  for (cudaEvent_t e : c->prof_pool) cudaEventDestroy(e);
   if (c->ev_start) cudaEventDestroy(c->ev_start);
   if (c->ev_end) cudaEventDestroy(c->ev_end);
   if (c->main_st) cudaStreamDestroy(c->main_st);
@@ -329,6 +383,34 @@ StepGeom geom(kc_cache* c, uint64_t top_n) {
   return g;
 }
 
+// Write back every dirty L2 line (a read sweep of 2.5x L2) so that all stored
+// K becomes clean and the scoring kernel may drop its lines after use. Done
+// at the first decode after appends, then whenever the not-yet-clean tail of
+// a layer exceeds ~8 MB; positions appended since stay un-dropped.
+void maybe_flush_l2(kc_cache* c, const uint64_t* layers, uint64_t n, cudaStream_t st) {
+  const uint64_t pos_bytes = c->rows * c->h * c->esz;
+  const uint64_t slack = (8ull << 20) / std::max<uint64_t>(pos_bytes, 1);
+  bool need = false;
+  for (uint64_t i = 0; i < n; ++i) {
+    const LayerState& ls = c->layers[layers[i]];
+    if (ls.len > ls.clean_len && (ls.clean_len == 0 || ls.len - ls.clean_len > slack)) need = true;
+  }
+  if (!need) return;
+  static std::mutex mu;
+  static std::vector<std::pair<void*, size_t>> bufs(64, {nullptr, 0});
+  std::lock_guard<std::mutex> lk(mu);
+  auto& buf = bufs[c->device & 63];
+  if (!buf.first) {
+    int l2 = 0;
+    CK(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, c->device));
+    buf.second = ((size_t)l2 * 5 / 2 + 4095) & ~size_t(4095);
+    CK(cudaMalloc(&buf.first, buf.second));
+    CK(cudaMemsetAsync(buf.first, 0, buf.second, st));
+  }
+  kc::l2_flush_launch(buf.first, buf.second, st);
+  for (auto& ls : c->layers) ls.clean_len = ls.len;
+}
+
 void enqueue_score(kc_cache* c, uint64_t layer, const float* q32, const StepGeom& g, cudaStream_t st) {
   kc::ScoreParams sp{};
   sp.k = c->k_layer(layer);
@@ -346,12 +428,17 @@ void enqueue_score(kc_cache* c, uint64_t layer, const float* q32, const StepGeom
   sp.n_splits = g.n_splits;
   sp.max_splits = c->max_splits;
   sp.scale = 1.0f / std::sqrt(static_cast<float>(c->h));  // attention.hpp:15-17
-  kc::score_launch(sp, c->dtype, st);
+  sp.discard_len = (int)std::min<uint64_t>(c->layers[layer].clean_len, (uint64_t)g.s);
+  if (!c->discard) sp.discard_len = 0;
+  c->timed(0, st, [&] { kc::score_launch(sp, c->dtype, st); });
 }
 
 // q (any dtype, host or device) -> fp32 device buffer for ring slot
+// host_slot/host_slots: position of this q in the call's pageable staging
+// (each q of a multi-layer call gets its own slot: the async H2D of q_i may
+// still be pending when q_{i+1} is staged).
 const float* stage_q(kc_cache* c, int slot, const void* q, int q_dtype, bool io_device,
-                     cudaStream_t st) {
+                     cudaStream_t st, uint64_t host_slot = 0, uint64_t host_slots = 1) {
   const uint64_t nq = c->batch * c->n_q * c->h;
   if (io_device && q_dtype == KC_F32) return static_cast<const float*>(q);
   c->q32[slot].ensure(nq * sizeof(float));
@@ -360,7 +447,15 @@ const float* stage_q(kc_cache* c, int slot, const void* q, int q_dtype, bool io_
     const size_t bytes = nq * dtype_size(q_dtype);
     c->stage_src.ensure(bytes * kRing);
     void* dst = (char*)c->stage_src.p + slot * bytes;
-    CK(cudaMemcpyAsync(dst, q, bytes, cudaMemcpyHostToDevice, st));
+    const void* hsrc = q;
+    if (!host_pinned(q)) {
+      // pageable input: stage through pinned memory so the copy stays async
+      c->host_in.ensure(bytes * host_slots);
+      void* hp = (char*)c->host_in.p + host_slot * bytes;
+      std::memcpy(hp, q, bytes);
+      hsrc = hp;
+    }
+    CK(cudaMemcpyAsync(dst, hsrc, bytes, cudaMemcpyHostToDevice, st));
     src = dst;
   }
   kc::to_f32_launch(src, q_dtype, c->q32[slot].as<float>(), (int64_t)nq, st);
@@ -394,13 +489,14 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
   if (!io_device) c->host_out.ensure(per_layer * n);
 
   cudaStream_t side = c->pipeline ? c->side_st : st;
+  maybe_flush_l2(c, layers, n, st);
   CK(cudaEventRecord(c->ev_start, st));
   if (side != st) CK(cudaStreamWaitEvent(side, c->ev_start, 0));
 
   for (uint64_t i = 0; i < n; ++i) {
     const int slot = (int)(i % kRing);
     const uint64_t layer = layers[i];
-    const float* q32 = stage_q(c, slot, q[i], q_dtype, io_device, st);
+    const float* q32 = stage_q(c, slot, q[i], q_dtype, io_device, st, i, n);
     enqueue_score(c, layer, q32, g, st);
     if (i >= (uint64_t)kRing && side != st) CK(cudaStreamWaitEvent(st, c->ev_rec[slot], 0));
 
@@ -421,13 +517,48 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
     sp.n_splits = g.n_splits;
     sp.max_splits = c->max_splits;
     sp.rows = (int)c->rows;
-    kc::select_launch(sp, st);
+    sp.force_global = c->select_global;
+    c->timed(1, st, [&] { kc::select_launch(sp, st); });
     CK(cudaEventRecord(c->ev_sel[slot], st));
     if (side != st) CK(cudaStreamWaitEvent(side, c->ev_sel[slot], 0));
 
     kc_topn_out& o = outs[i];
     kc::RecallParams rp{};
     rp.v = c->v_layer(layer);
+    // Offloaded layer: compact the selected rows on the host (pool threads,
+    // stream-ordered via cudaLaunchHostFunc on gather_st), then one DMA.
+    const bool dma = layer >= c->L && c->recall_mode != kRecallZeroCopy;
+    const size_t stage_bytes = c->rows * nc * c->h * c->esz;
+    if (dma) {
+      c->idx_host[slot].ensure(c->rows * nc * 4);
+      c->stage_host[slot].ensure(stage_bytes);
+      c->stage_dev[slot].ensure(stage_bytes);
+      if (!c->pool) {
+        int t = c->gather_threads;
+        if (t <= 0) t = std::max(1, std::min(8, (int)std::thread::hardware_concurrency() / 2));
+        c->pool = std::make_unique<kc::GatherPool>(t - 1);
+      }
+      CK(cudaStreamWaitEvent(c->gather_st, c->ev_sel[slot], 0));
+      CK(cudaMemcpyAsync(c->idx_host[slot].p, c->idx[slot].p, c->rows * nc * 4, cudaMemcpyDeviceToHost,
+                         c->gather_st));
+      auto* job = new kc::GatherJob{c->pool.get(),
+                                    (const char*)c->v_host + (layer - c->L) * c->v_layer_bytes,
+                                    c->cfg.max_seq * c->h * c->esz,
+                                    c->h * c->esz,
+                                    static_cast<const uint32_t*>(c->idx_host[slot].p),
+                                    c->rows,
+                                    nc,
+                                    static_cast<char*>(c->stage_host[slot].p)};
+      cudaError_t he = cudaLaunchHostFunc(c->gather_st, kc::gather_host_fn, job);
+      if (he != cudaSuccess) {
+        delete job;
+        CK(he);
+      }
+      CK(cudaEventRecord(c->ev_gath[slot], c->gather_st));
+      CK(cudaStreamWaitEvent(side, c->ev_gath[slot], 0));
+      rp.v = c->stage_dev[slot].p;
+    }
+    rp.staged = dma ? 1 : 0;
     rp.idx = c->idx[slot].as<uint32_t>();
     rp.w = c->w[slot].as<float>();
     rp.norm = c->norm[slot].as<float>();
@@ -441,7 +572,12 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
     rp.renormalize = (flags & KC_RENORMALIZE) ? 1 : 0;
     rp.reverse = (flags & KC_REVERSE_ACCUM) ? 1 : 0;
     rp.row_offset = 0;
-    kc::recall_launch(rp, c->dtype, side);
+    c->timed(2, side, [&] {
+      if (dma)
+        CK(cudaMemcpyAsync(c->stage_dev[slot].p, c->stage_host[slot].p, stage_bytes,
+                           cudaMemcpyHostToDevice, side));
+      kc::recall_launch(rp, c->dtype, side);
+    });
 
     const uint32_t* idx_slots = c->idx[slot].as<uint32_t>();
     if (c->G > 1 && (o.indices || !io_device)) {
@@ -455,12 +591,17 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
       if (o.dropped_mass)
         CK(cudaMemcpyAsync(o.dropped_mass, c->dropped[slot].p, o_dr, cudaMemcpyDeviceToDevice, side));
     } else {
+      // D2H straight into pinned user buffers, else into pinned staging
       char* hb = (char*)c->host_out.p + i * per_layer;
-      CK(cudaMemcpyAsync(hb, c->out_tmp[slot].p, o_out, cudaMemcpyDeviceToHost, side));
-      if (o.indices) CK(cudaMemcpyAsync(hb + o_out, idx_slots, o_idx, cudaMemcpyDeviceToHost, side));
-      if (o.weights) CK(cudaMemcpyAsync(hb + o_out + o_idx, c->w[slot].p, o_w, cudaMemcpyDeviceToHost, side));
-      if (o.dropped_mass)
-        CK(cudaMemcpyAsync(hb + o_out + o_idx + o_w, c->dropped[slot].p, o_dr, cudaMemcpyDeviceToHost, side));
+      auto d2h = [&](void* user, size_t off, const void* src, size_t bytes) {
+        if (!user) return;
+        void* dst = host_pinned(user) ? user : (void*)(hb + off);
+        CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, side));
+      };
+      d2h(o.out, 0, c->out_tmp[slot].p, o_out);
+      d2h(o.indices, o_out, idx_slots, o_idx);
+      d2h(o.weights, o_out + o_idx, c->w[slot].p, o_w);
+      d2h(o.dropped_mass, o_out + o_idx + o_w, c->dropped[slot].p, o_dr);
     }
     CK(cudaEventRecord(c->ev_rec[slot], side));
     CK(cudaGetLastError());
@@ -484,10 +625,13 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
     for (uint64_t i = 0; i < n; ++i) {
       const char* hb = (const char*)c->host_out.p + i * per_layer;
       kc_topn_out& o = outs[i];
-      std::memcpy(o.out, hb, o_out);
-      if (o.indices) std::memcpy(o.indices, hb + o_out, o_idx);
-      if (o.weights) std::memcpy(o.weights, hb + o_out + o_idx, o_w);
-      if (o.dropped_mass) std::memcpy(o.dropped_mass, hb + o_out + o_idx + o_w, o_dr);
+      auto copy = [&](void* user, size_t off, size_t bytes) {
+        if (user && !host_pinned(user)) std::memcpy(user, hb + off, bytes);
+      };
+      copy(o.out, 0, o_out);
+      copy(o.indices, o_out, o_idx);
+      copy(o.weights, o_out + o_idx, o_w);
+      copy(o.dropped_mass, o_out + o_idx + o_w, o_dr);
     }
   }
 }
@@ -549,8 +693,9 @@ int kc_cache_create(const kc_config* cfg, uint64_t batch, uint64_t resident_laye
         c->v_host_bytes = checked_mul({c->v_layer_bytes, cfg->n_layers - c->L});
         c->v_host = alloc_pinned_arena(c->v_host_bytes, numa_node, &c->v_host_dev);
       }
-      c->lstride = (int64_t)((cfg->max_seq + 3) & ~3ull);
-      c->kstride = (int64_t)cfg->max_seq;
+      // rows padded to 128 B: the selection kernel drops them from L2 by line
+      c->lstride = (int64_t)((cfg->max_seq + 31) & ~31ull);
+      c->kstride = c->lstride;
       c->max_splits = (int)((cfg->max_seq + 63) / 64);
       c->logits.ensure(checked_mul({batch, c->n_q, (uint64_t)c->lstride, 4}));
       c->partials.ensure(checked_mul({batch, c->n_q, (uint64_t)c->max_splits, 8}));
@@ -559,11 +704,13 @@ int kc_cache_create(const kc_config* cfg, uint64_t batch, uint64_t resident_laye
       CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
       CK(cudaStreamCreateWithFlags(&c->main_st, cudaStreamNonBlocking));
       CK(cudaStreamCreateWithPriority(&c->side_st, cudaStreamNonBlocking, hi));
+      CK(cudaStreamCreateWithPriority(&c->gather_st, cudaStreamNonBlocking, hi));
       CK(cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming));
       CK(cudaEventCreateWithFlags(&c->ev_end, cudaEventDisableTiming));
       for (int i = 0; i < kRing; ++i) {
         CK(cudaEventCreateWithFlags(&c->ev_sel[i], cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&c->ev_rec[i], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&c->ev_gath[i], cudaEventDisableTiming));
       }
     } catch (...) {
       destroy(c);
@@ -657,6 +804,7 @@ int kc_decode_full(kc_cache* c, uint64_t layer, const void* q, int q_dtype, uint
     const bool io_device = flags & KC_IO_DEVICE;
     cudaStream_t st = io_device ? (cudaStream_t)stream : c->main_st;
     const StepGeom g = geom(c, 1);
+    maybe_flush_l2(c, &layer, 1, st);
     const float* q32 = stage_q(c, 0, q, q_dtype, io_device, st);
     enqueue_score(c, layer, q32, g, st);
     const uint64_t slots = c->batch * c->n_q;
@@ -695,6 +843,7 @@ int kc_score_probs(kc_cache* c, uint64_t layer, const void* q, int q_dtype, floa
     set_dev(c);
     cudaStream_t st = c->main_st;
     const StepGeom g = geom(c, 1);
+    maybe_flush_l2(c, &layer, 1, st);
     const float* q32 = stage_q(c, 0, q, q_dtype, false, st);
     enqueue_score(c, layer, q32, g, st);
     const uint64_t slots = c->batch * c->n_q;
@@ -835,7 +984,61 @@ int kc_set_tuning(kc_cache* c, const char* key, int64_t value) {
     const std::string k = key ? key : "";
     if (k == "score_chunk") c->score_chunk = (int)value;
     else if (k == "pipeline") c->pipeline = value ? 1 : 0;
+    else if (k == "discard") c->discard = value ? 1 : 0;
+    else if (k == "select_global") c->select_global = value ? 1 : 0;
+    else if (k == "recall_mode") {
+      if (value < 0 || value > 2) fail(KC_EARG, "recall_mode: 0 auto, 1 zero-copy, 2 dma");
+      c->recall_mode = (int)value;
+    } else if (k == "gather_threads") {
+      if (c->main_st) cudaStreamSynchronize(c->main_st);
+      if (c->side_st) cudaStreamSynchronize(c->side_st);
+      if (c->gather_st) cudaStreamSynchronize(c->gather_st);
+      c->gather_threads = (int)value;
+      c->pool.reset();
+    }
     else fail(KC_EARG, "unknown tuning key '" + k + "'");
+  });
+}
+
+int kc_profile(kc_cache* c, int enable) {
+  return guarded([&] {
+    set_dev(c);
+    CK(cudaStreamSynchronize(c->main_st));
+    CK(cudaStreamSynchronize(c->side_st));
+    c->prof_on = enable != 0;
+    for (auto& v : c->prof) v.clear();
+    c->prof_used = 0;
+  });
+}
+
+int kc_profile_read(kc_cache* c, const char* kernel, double* total_ms, uint64_t* launches) {
+  return guarded([&] {
+    const std::string k = kernel ? kernel : "";
+    const int kind = k == "score" ? 0 : k == "select" ? 1 : k == "recall" ? 2 : -1;
+    if (kind < 0) fail(KC_EARG, "kc_profile_read: kernel must be score, select or recall");
+    set_dev(c);
+    double total = 0.0;
+    for (auto& pr : c->prof[kind]) {
+      CK(cudaEventSynchronize(pr.second));
+      float ms = 0.0f;
+      CK(cudaEventElapsedTime(&ms, pr.first, pr.second));
+      total += ms;
+    }
+    *total_ms = total;
+    *launches = c->prof[kind].size();
+  });
+}
+
+int kc_profile_launch(kc_cache* c, const char* kernel, uint64_t i, double* ms) {
+  return guarded([&] {
+    const std::string k = kernel ? kernel : "";
+    const int kind = k == "score" ? 0 : k == "select" ? 1 : k == "recall" ? 2 : -1;
+    if (kind < 0 || i >= c->prof[kind].size()) fail(KC_EARG, "kc_profile_launch: bad kernel or index");
+    set_dev(c);
+    CK(cudaEventSynchronize(c->prof[kind][i].second));
+    float t = 0.0f;
+    CK(cudaEventElapsedTime(&t, c->prof[kind][i].first, c->prof[kind][i].second));
+    *ms = t;
   });
 }
 

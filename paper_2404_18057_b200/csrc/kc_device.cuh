@@ -71,6 +71,27 @@ __device__ __forceinline__ void ml_combine(float& m, float& l, float m2, float l
   l = a + b;
 }
 
+// Global softmax stats of one (batch, q head) from the scoring kernel's
+// per-split (max, sum exp): M = max m_i, Z = sum_i l_i exp(m_i - M). Called
+// by a full warp; every kernel that needs p = exp(s - M) / Z uses this one
+// function, so selection, weights and the observer path agree bit for bit.
+__device__ __forceinline__ void softmax_stats(const float2* part, int n_splits, int lane, float& M,
+                                              float& Z) {
+  float m = -INFINITY;
+  for (int i = lane; i < n_splits; i += 32) m = fmaxf(m, part[i].x);
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  float z = 0.0f;
+  for (int i = lane; i < n_splits; i += 32) {
+    const float2 ml = part[i];
+    if (ml.y > 0.0f) z += ml.y * expf(ml.x - m);
+  }
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
+  M = m;
+  Z = z;
+}
+
 // ---- shared-memory address / mbarrier / TMA bulk copy (PTX) ----------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -127,6 +148,13 @@ __device__ __forceinline__ void tma_bulk_g2s(void* dst_smem, const void* src_gme
       "[%1], %2, [%3], %4;" ::"r"(smem_u32(dst_smem)),
       "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
       : "memory");
+}
+
+// Invalidate one 128-B L2 line without write-back. Only for lines known to be
+// clean (their DRAM copy current): the store never issues it for K positions
+// appended since its last L2 flush.
+__device__ __forceinline__ void discard_l2_line(const void* p) {
+  asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
 }
 
 __device__ __forceinline__ uint32_t lanemask_lt() {

@@ -28,7 +28,11 @@ struct ScoreParams {
   int n_splits;
   int max_splits;
   float scale;          // 1/sqrt(h) as the reference computes it
+  int discard_len;      // K positions < discard_len are clean: drop their L2 lines after use
 };
+// Read `bytes` of a scratch buffer larger than L2: evicts (and so writes back)
+// every dirty L2 line, after which all stored K is clean in DRAM.
+void l2_flush_launch(const void* scratch, size_t bytes, cudaStream_t st);
 // dtype: KC_F32 / KC_F16 / KC_BF16 (storage)
 void score_launch(const ScoreParams& p, int dtype, cudaStream_t st);
 // positions per CTA for a given shape (tuning override when > 0)
@@ -51,6 +55,7 @@ struct SelectParams {
   int n_splits;
   int max_splits;
   int rows;
+  int force_global;       // 1: the global-memory-keys kernel even when s fits registers
 };
 void select_launch(const SelectParams& p, cudaStream_t st);
 
@@ -77,6 +82,7 @@ struct RecallParams {
   int renormalize;
   int reverse;            // fault hook: descending accumulation
   int row_offset;         // first row of this launch (pipelined chunks)
+  int staged;             // v is the compacted [rows][nc][h] block (DMA recall)
 };
 void recall_launch(const RecallParams& p, int dtype, cudaStream_t st);
 

@@ -36,7 +36,8 @@ __global__ void __launch_bounds__(kRecallThreads) recall_pv_kernel(const RecallP
   const size_t rowb = (size_t)h * sizeof(T);
   T* vbuf = reinterpret_cast<T*>(smem);
   float* wbuf = reinterpret_cast<float*>(smem + (((size_t)rc_max * rowb + 15) & ~size_t(15)));
-  const T* vslot = static_cast<const T*>(p.v) + (size_t)row * p.max_seq * h;
+  // staged: rows already compacted to [rows][nc][h] (host gather + DMA)
+  const T* vslot = static_cast<const T*>(p.v) + (size_t)row * (p.staged ? (size_t)nc : (size_t)p.max_seq) * h;
   const uint32_t* idx = p.idx + (size_t)row * nc;
   const int n_out = G * h;
   constexpr int kMaxOut = 4;  // G*h <= 1024
@@ -62,7 +63,8 @@ __global__ void __launch_bounds__(kRecallThreads) recall_pv_kernel(const RecallP
           const int v = v0 + u * kRecallThreads;
           if (v < total) {
             const int r = v / vpr, part = v - r * vpr;
-            tmp[u] = *(reinterpret_cast<const uint4*>(vslot + (size_t)idx[c0 + r] * h) + part);
+            const size_t pos = p.staged ? (size_t)(c0 + r) : (size_t)idx[c0 + r];
+            tmp[u] = *(reinterpret_cast<const uint4*>(vslot + pos * h) + part);
           }
         }
 #pragma unroll
@@ -74,7 +76,8 @@ __global__ void __launch_bounds__(kRecallThreads) recall_pv_kernel(const RecallP
     } else {
       for (int e = tid; e < rc * h; e += kRecallThreads) {
         const int r = e / h, c = e - r * h;
-        vbuf[e] = vslot[(size_t)idx[c0 + r] * h + c];
+        const size_t pos = p.staged ? (size_t)(c0 + r) : (size_t)idx[c0 + r];
+        vbuf[e] = vslot[pos * h + c];
       }
     }
     // ---- weights (raw p, or p * (1/sum p) when renormalising) ----
@@ -128,17 +131,9 @@ __global__ void __launch_bounds__(256) pv_full_kernel(const PvFullParams p) {
   float* sZ = sh + G;
   float* wb = sh + 2 * G;
   for (int g = warp; g < G; g += 8) {
-    const float2* part = p.partials + ((size_t)b * n_q + kvh * G + g) * p.max_splits;
-    float m = -INFINITY;
-    for (int i = lane; i < p.n_splits; i += 32) m = fmaxf(m, part[i].x);
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    float m, z;
+    softmax_stats(p.partials + ((size_t)b * n_q + kvh * G + g) * p.max_splits, p.n_splits, lane, m, z);
     if (lane == 0) {
-      float z = 0.0f;
-      for (int i = 0; i < p.n_splits; ++i) {
-        const float2 ml = part[i];
-        if (ml.y > 0.0f) z += ml.y * expf(ml.x - m);
-      }
       sM[g] = m;
       sZ[g] = z;
     }

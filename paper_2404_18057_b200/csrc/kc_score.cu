@@ -79,19 +79,39 @@ __global__ void __launch_bounds__((kCWarps + 1) * 32)
   __syncthreads();
 
   if (warp == kCWarps) {
-    // ---------------- producer: one elected lane streams K ----------------
-    if (lane == 0) {
-      const T* kslot = static_cast<const T*>(p.k) + (size_t)row * p.max_seq * kH;
-      const uint64_t pol = l2_evict_first_policy();
-      for (int it = 0; it < n_it; ++it) {
-        const int st = it % kStages;
-        if (it >= kStages) mbar_wait(&empty[st], ((it / kStages) - 1) & 1);
+    // ---------------- producer warp: lane 0 streams K with TMA ----------------
+    // Once a stage has been consumed, the warp drops that stage's K lines from
+    // L2 (discard.global.L2, positions < discard_len, which the store keeps
+    // clean): a decode step streams the whole K cache once, and an L2 left full
+    // of dead K lines makes the following zero-copy V recall ~1.5x slower
+    // (tools/h2d_probe2.cu). K itself is never written here.
+    const T* kslot = static_cast<const T*>(p.k) + (size_t)row * p.max_seq * kH;
+    const uint64_t pol = l2_evict_first_policy();
+    auto drop = [&](int it) {
+      const int pstart = pos0 + it * kRows;
+      const int pend = min(pos0 + min(npos, (it + 1) * kRows), p.discard_len);
+      const char* base = reinterpret_cast<const char*>(kslot + (size_t)pstart * kH);
+      const int lines = (pend - pstart) * (ROWB / 128);
+      for (int l = lane; l < lines; l += 32) discard_l2_line(base + (size_t)l * 128);
+    };
+    for (int it = 0; it < n_it; ++it) {
+      const int st = it % kStages;
+      if (it >= kStages) {
+        mbar_wait(&empty[st], ((it / kStages) - 1) & 1);
+        drop(it - kStages);
+      }
+      if (lane == 0) {
         const int rows = min(kRows, npos - it * kRows);
         const uint32_t bytes = (uint32_t)(rows * ROWB);
         mbar_arrive_expect_tx(&full[st], bytes);
         tma_bulk_g2s(ring + st * kRows * ROWB, kslot + (size_t)(pos0 + it * kRows) * kH, bytes,
                      &full[st], pol);
       }
+      __syncwarp();
+    }
+    for (int it = max(0, n_it - kStages); it < n_it; ++it) {
+      mbar_wait(&empty[it % kStages], (it / kStages) & 1);
+      drop(it);
     }
     return;
   }
@@ -246,7 +266,19 @@ bool try_fast(const ScoreParams& p, cudaStream_t st) {
   }
 }
 
+__global__ void l2_flush_kernel(const uint4* p, size_t n16, uint32_t* sink) {
+  uint32_t acc = 0;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n16; i += (size_t)gridDim.x * blockDim.x)
+    acc ^= p[i].x;
+  if (acc == 0x9e3779b9u) sink[0] = acc;  // keeps the loads alive
+}
+
 }  // namespace
+
+void l2_flush_launch(const void* scratch, size_t bytes, cudaStream_t st) {
+  l2_flush_kernel<<<148 * 8, 256, 0, st>>>(static_cast<const uint4*>(scratch), bytes / 16,
+                                          (uint32_t*)scratch + (bytes / 4 - 1));
+}
 
 int score_pick_chunk(int s, int rows, int override_chunk) {
   if (override_chunk > 0) return ((override_chunk + kRows - 1) / kRows) * kRows;

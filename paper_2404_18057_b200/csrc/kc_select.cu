@@ -4,23 +4,28 @@
 // arg_topk (proj/core/src/matrix.cpp:109-122) and the TopNSelection fill
 // loop (proj/core/src/attention.cpp:126-154).
 //
-// One 1024-thread CTA per (batch, kv head):
-//   1. global softmax stats per q head from the scoring kernel's per-split
-//      (max, sum exp): M = max m_i, Z = sum_i l_i exp(m_i - M) (ascending i);
-//   2. key_j = fp32 bits of p_j = exp(s_j - M) / Z -- the reference ranks the
-//      fp32 PROBABILITIES (attention.cpp:140), so equal probabilities tie even
-//      when logits differ; for GQA key_j = sum_g p_g[j]. p >= 0,
-//      so the raw bits order like the values;
+// The reference ranks the fp32 PROBABILITIES p_j = exp(s_j - M) / Z
+// (attention.cpp:140) with a stable descending sort, so equal probabilities
+// tie to the lowest position even when their logits differ, and returns the
+// survivors in ascending position order. The GPU reproduces exactly that rule
+// on its own p (for GQA the key is sum_g p_g[j]):
+//   1. global (M, Z) per q head from the scoring kernel's per-split
+//      (max, sum exp) (softmax_stats, kc_device.cuh);
+//   2. keys. MHA: the order-preserving bits of the logit itself -- p is a
+//      monotone non-decreasing function of s, so the p-order and the s-order
+//      can only disagree inside a p-tie, which step 4 resolves exactly.
+//      GQA: the fp32 bits of sum_g p_g (>= 0, so raw bits order like values);
 //   3. MSB-first radix select (11/11/10-bit digits, shared-memory histograms
-//      with warp-aggregated atomics) finds the N-th largest key T and how many
-//      of the keys equal to T to keep;
-//   4. ordered compaction (per-warp contiguous segments, ballot ranks) keeps
-//      every key > T and the LOWEST-index keys == T -- exactly
-//      stable_sort(desc) + resize(N) -- and emits the survivors already in
-//      ascending position order (the reference's final std::sort);
-//   5. weights p_g[idx], dropped = 1 - sum double(p) (ascending order, as
-//      attention.cpp:146-152) and the fp32 renormaliser 1/sum p
-//      (attention.cpp:167-174), each summed sequentially like the reference.
+//      with warp-aggregated atomics) finds the N-th largest key T;
+//   4. classification + ordered compaction: survivors are the keys ranked
+//      above the N-th p plus the lowest-position members of its tie class;
+//      two block scans give every thread its output offset, so indices come
+//      out ascending (the reference's final std::sort) with no sort at all;
+//   5. weights p[idx], dropped = 1 - sum double(p), renormaliser 1/sum p
+//      (attention.cpp:146-152,167-174).
+// s <= 32768: keys stay in registers (select_reg_kernel, thread t owns
+// positions [t*KPT, t*KPT+KPT)); longer rows use a global-memory key scratch
+// (select_kernel).
 #include "kc_device.cuh"
 #include "kc_kernels.cuh"
 
@@ -38,12 +43,14 @@ struct SelShared {
   uint32_t wa[kNW], wb[kNW], wc[kNW], wd[kNW];
   float M[kMaxG], Z[kMaxG];
   uint32_t bin, need;
+  float red_f[kNW];
+  double red_d[kNW];
 };
 
 __device__ __forceinline__ void hist_add(uint32_t* hist, uint32_t bin, bool active, int lane) {
   const uint32_t key = active ? bin : 0xffffffffu;
   const uint32_t peers = __match_any_sync(0xffffffffu, key);
-  const int leader = __ffs(peers) - 1;
+  const int leader = 31 - __clz(peers);  // highest peer lane (FLO, no BREV)
   if (active && lane == leader) atomicAdd(&hist[bin], (uint32_t)__popc(peers));
 }
 
@@ -88,42 +95,403 @@ __device__ __forceinline__ void clear_hist(SelShared& S) {
   __syncthreads();
 }
 
-// keys[0..s) (already written, visible to the block) -> idx[0..nc) ascending.
-__device__ void radix_compact(SelShared& S, const uint32_t* keys, int s, int nc, uint32_t* idx) {
+// Block-wide exclusive prefix sum over the 1024 threads (thread order).
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t x, uint32_t* warp_tot) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t v = x;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t n = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += n;
+  }
+  if (lane == 31) warp_tot[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    const uint32_t t = warp_tot[lane];
+    uint32_t u = t;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t n = __shfl_up_sync(0xffffffffu, u, o);
+      if (lane >= o) u += n;
+    }
+    warp_tot[lane] = u - t;
+  }
+  __syncthreads();
+  const uint32_t r = warp_tot[warp] + v - x;
+  __syncthreads();
+  return r;
+}
+
+// Radix select over (key, valid) pairs given by get(i) for the items a thread
+// owns; returns the N-th largest key T and how many keys equal to T survive.
+template <int KPT, typename Get>
+__device__ __forceinline__ void radix_threshold(SelShared& S, Get&& get, int nc, int n_valid,
+                                                uint32_t& T, uint32_t& k_eq) {
+  const int lane = threadIdx.x & 31;
+  T = 0;
+  k_eq = (uint32_t)nc;
+  if (nc >= n_valid) return;  // everything survives
+  clear_hist(S);
+#pragma unroll
+  for (int i = 0; i < KPT; ++i) {
+    bool v;
+    const uint32_t k = get(i, v);
+    hist_add(S.hist, k >> 21, v, lane);
+  }
+  __syncthreads();
+  find_bin(S, (uint32_t)nc);
+  const uint32_t b0 = S.bin;
+  uint32_t need = S.need;
+  clear_hist(S);
+#pragma unroll
+  for (int i = 0; i < KPT; ++i) {
+    bool v;
+    const uint32_t k = get(i, v);
+    const bool act = v && (k >> 21) == b0;
+    if (__any_sync(0xffffffffu, act)) hist_add(S.hist, (k >> 10) & 0x7ffu, act, lane);
+  }
+  __syncthreads();
+  find_bin(S, need);
+  const uint32_t p01 = (b0 << 11) | S.bin;
+  need = S.need;
+  clear_hist(S);
+#pragma unroll
+  for (int i = 0; i < KPT; ++i) {
+    bool v;
+    const uint32_t k = get(i, v);
+    const bool act = v && (k >> 10) == p01;
+    if (__any_sync(0xffffffffu, act)) hist_add(S.hist, k & 0x3ffu, act, lane);
+  }
+  __syncthreads();
+  find_bin(S, need);
+  T = (p01 << 10) | S.bin;
+  k_eq = S.need;
+}
+
+__device__ __forceinline__ uint32_t ordered_bits(float x) {
+  const uint32_t u = __float_as_uint(x);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+__device__ __forceinline__ void load_stats(SelShared& S, const SelectParams& p, int b, int kvh) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int n_q = p.n_kv * p.G;
+  for (int g = warp; g < p.G; g += kNW) {
+    float m, z;
+    softmax_stats(p.partials + ((size_t)b * n_q + kvh * p.G + g) * p.max_splits, p.n_splits, lane, m, z);
+    if (lane == 0) {
+      S.M[g] = m;
+      S.Z[g] = z;
+    }
+  }
+  __syncthreads();
+}
+
+// dropped mass and renormaliser of every q head of the group from the weights
+// just written (block-wide reductions; the weights are visible after the
+// caller's __syncthreads).
+__device__ void finish_group(SelShared& S, const SelectParams& p, int b, int kvh) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int n_q = p.n_kv * p.G;
+  for (int g = 0; g < p.G; ++g) {
+    const size_t slot = (size_t)b * n_q + kvh * p.G + g;
+    const float* wg = p.w + slot * p.nc;
+    double md = 0.0;
+    float fs = 0.0f;
+    for (int r = tid; r < p.nc; r += kT) {
+      const float x = wg[r];
+      md += (double)x;
+      fs += x;
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+      md += __shfl_xor_sync(0xffffffffu, md, o);
+      fs += __shfl_xor_sync(0xffffffffu, fs, o);
+    }
+    if (lane == 0) {
+      S.red_d[warp] = md;
+      S.red_f[warp] = fs;
+    }
+    __syncthreads();
+    if (warp == 0) {
+      double a = S.red_d[lane];
+      float f = S.red_f[lane];
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) {
+        a += __shfl_xor_sync(0xffffffffu, a, o);
+        f += __shfl_xor_sync(0xffffffffu, f, o);
+      }
+      if (lane == 0) {
+        p.dropped[slot] = 1.0 - a;
+        p.norm[slot] = f > 0.0f ? 1.0f / f : 1.0f;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Drop the row's dead logits (dirty scratch) from L2 without write-back: saves
+// the HBM write and keeps L2 free for the V recall's host reads.
+__device__ __forceinline__ void drop_rows(const float* base, int64_t stride, int nrows, int s) {
+  const int lines = (s * 4 + 127) / 128;
+  for (int e = threadIdx.x; e < nrows * lines; e += kT) {
+    const int g = e / lines, l = e - g * lines;
+    discard_l2_line(reinterpret_cast<const char*>(base + (size_t)g * stride) + (size_t)l * 128);
+  }
+}
+
+template <int KPT>
+__global__ void __launch_bounds__(kT, 1) select_reg_kernel(const SelectParams p) {
+  __shared__ SelShared S;
+  const int row = blockIdx.x;
+  const int b = row / p.n_kv;
+  const int kvh = row - b * p.n_kv;
+  const int G = p.G;
+  const int n_q = p.n_kv * G;
+  const int tid = threadIdx.x;
+  const float* lbase = p.logits + ((size_t)b * n_q + kvh * G) * p.lstride;
+  uint32_t* idx = p.idx + (size_t)row * p.nc;
+  const int s = p.s, nc = p.nc;
+  const int j0 = tid * KPT;
+  load_stats(S, p, b, kvh);
+
+  // keys: MHA -> ordered logit bits; GQA -> bits of sum_g p_g
+  uint32_t key[KPT];
+  if (G == 1) {
+    if (j0 + KPT <= s) {
+#pragma unroll
+      for (int i = 0; i < KPT; i += 4) {
+        const float4 v = *reinterpret_cast<const float4*>(lbase + j0 + i);
+        key[i] = ordered_bits(v.x);
+        key[i + 1] = ordered_bits(v.y);
+        key[i + 2] = ordered_bits(v.z);
+        key[i + 3] = ordered_bits(v.w);
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < KPT; ++i) key[i] = j0 + i < s ? ordered_bits(lbase[j0 + i]) : 0u;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < KPT; ++i) key[i] = 0u;
+    for (int g = 0; g < G; ++g) {
+      const float* lr = lbase + (size_t)g * p.lstride;
+      const float Mg = S.M[g], Zg = S.Z[g];
+#pragma unroll
+      for (int i = 0; i < KPT; ++i) {
+        if (j0 + i < s) {
+          const float pg = expf(lr[j0 + i] - Mg) / Zg;
+          key[i] = (g == 0) ? __float_as_uint(pg) : __float_as_uint(__uint_as_float(key[i]) + pg);
+        }
+      }
+    }
+  }
+
+  // ---- fast path: threshold from thread maxima, exact select on candidates --
+  // tau = the nc-th largest of the 1024 per-thread maxima is a lower bound of
+  // the nc-th largest key (nc threads each hold a key >= tau), and for
+  // unstructured rows only ~nc keys reach it. Those candidates (<= 1024, in
+  // position order) get the exact treatment; anything else (ties flooding
+  // the bound, nc > 1024) falls through to the full radix pass below.
+  if (nc < s && nc <= kT) {
+    uint32_t tmax = 0;
+#pragma unroll
+    for (int i = 0; i < KPT; ++i)
+      if (j0 + i < s) tmax = max(tmax, key[i]);
+    uint32_t tau, dummy;
+    radix_threshold<1>(S, [&](int, bool& v) { v = true; return tmax; }, nc, kT, tau, dummy);
+    uint32_t ccount = 0;
+#pragma unroll
+    for (int i = 0; i < KPT; ++i) ccount += (j0 + i < s && key[i] >= tau) ? 1u : 0u;
+    uint32_t cbase = block_excl_scan(ccount, S.wa);
+    if (tid == kT - 1) S.need = cbase + ccount;
+    __syncthreads();
+    const uint32_t C = S.need;
+    if (C <= (uint32_t)kT) {
+      // candidates -> shared memory (reuse the histogram space), position order
+      uint32_t* ckey = S.hist;
+      uint32_t* cpos = S.hist + kT;
+#pragma unroll
+      for (int i = 0; i < KPT; ++i) {
+        if (j0 + i < s && key[i] >= tau) {
+          ckey[cbase] = key[i];
+          cpos[cbase] = (uint32_t)(j0 + i);
+          ++cbase;
+        }
+      }
+      __syncthreads();
+      const bool have = (uint32_t)tid < C;
+      const uint32_t ck = have ? ckey[tid] : 0u;
+      const uint32_t cp = have ? cpos[tid] : 0u;
+      __syncthreads();  // the histogram space is reused by the radix below
+      uint32_t T, k_eq;
+      radix_threshold<1>(S, [&](int, bool& v) { v = have; return ck; }, nc, (int)C, T, k_eq);
+      uint32_t gt = 0, eq = 0;
+      if ((uint32_t)nc >= C) {
+        gt = have ? 1u : 0u;  // exactly nc candidates: all of them survive
+      } else if (have) {
+        if (G == 1) {
+          const float Ts = __uint_as_float((T & 0x80000000u) ? (T & 0x7fffffffu) : ~T);
+          const float M = S.M[0], Z = S.Z[0];
+          const float pT = expf(Ts - M) / Z;
+          const float win = 4e-5f * (1.0f + fabsf(Ts) + fabsf(M));
+          const float sj = __uint_as_float((ck & 0x80000000u) ? (ck & 0x7fffffffu) : ~ck);
+          if (sj > Ts + win) {
+            gt = 1;
+          } else if (sj >= Ts - win) {
+            const float pj = expf(sj - M) / Z;
+            gt = pj > pT;
+            eq = pj == pT;
+          }
+        } else {
+          gt = ck > T;
+          eq = ck == T;
+        }
+      }
+      const uint32_t gbase = block_excl_scan(gt, S.wc);
+      if (tid == kT - 1) S.need = gbase + gt;
+      __syncthreads();
+      const uint32_t keq = (uint32_t)nc - S.need;
+      const uint32_t ebase = block_excl_scan(eq, S.wa);
+      const bool sel = gt || (eq && ebase < keq);
+      const uint32_t o = block_excl_scan(sel ? 1u : 0u, S.wb);
+      if (sel) {
+        idx[o] = cp;
+        for (int g = 0; g < G; ++g)
+          p.w[((size_t)b * n_q + kvh * G + g) * nc + o] =
+              expf(lbase[(size_t)g * p.lstride + cp] - S.M[g]) / S.Z[g];
+      }
+      __syncthreads();
+      drop_rows(lbase, p.lstride, G, s);
+      finish_group(S, p, b, kvh);
+      return;
+    }
+  }
+
+  uint32_t T, k_eq;
+  radix_threshold<KPT>(S, [&](int i, bool& v) { v = j0 + i < s; return key[i]; }, nc,
+                       min(s, kT * KPT), T, k_eq);
+
+  // classification: 2 = ranked above the N-th p, 1 = in its tie class
+  uint32_t cls_gt = 0, cls_eq = 0;  // bit i set for item i
+  if (G == 1 && nc < s) {
+    // p is monotone in s: only logits close to T_s can share T's probability.
+    // Inside the window compare exact p (the same expression the weights use).
+    const float Ts = __uint_as_float((T & 0x80000000u) ? (T & 0x7fffffffu) : ~T);
+    const float M = S.M[0], Z = S.Z[0];
+    const float pT = expf(Ts - M) / Z;
+    const float win = 4e-5f * (1.0f + fabsf(Ts) + fabsf(M));
+#pragma unroll
+    for (int i = 0; i < KPT; ++i) {
+      if (j0 + i >= s) continue;
+      const float sj = __uint_as_float((key[i] & 0x80000000u) ? (key[i] & 0x7fffffffu) : ~key[i]);
+      if (sj > Ts + win) {
+        cls_gt |= 1u << i;
+      } else if (sj >= Ts - win) {
+        const float pj = expf(sj - M) / Z;
+        if (pj > pT) cls_gt |= 1u << i;
+        else if (pj == pT) cls_eq |= 1u << i;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < KPT; ++i) {
+      if (j0 + i >= s) continue;
+      if (key[i] > T) cls_gt |= 1u << i;
+      else if (key[i] == T) cls_eq |= 1u << i;
+    }
+  }
+  // ties take the remaining places, lowest positions first
+  const uint32_t n_gt_local = __popc(cls_gt);
+  uint32_t n_gt_total;
+  {
+    const uint32_t base = block_excl_scan(n_gt_local, S.wc);
+    if (tid == kT - 1) S.need = base + n_gt_local;
+    __syncthreads();
+    n_gt_total = S.need;
+    __syncthreads();
+  }
+  k_eq = (uint32_t)nc - n_gt_total;
+  const uint32_t ceq = __popc(cls_eq);
+  const uint32_t eq_base = block_excl_scan(ceq, S.wa);
+  const uint32_t take = eq_base >= k_eq ? 0u : min(ceq, k_eq - eq_base);
+  uint32_t o = block_excl_scan(n_gt_local + take, S.wb);
+  uint32_t eqr = eq_base;
+#pragma unroll
+  for (int i = 0; i < KPT; ++i) {
+    bool sel = (cls_gt >> i) & 1u;
+    if ((cls_eq >> i) & 1u) {
+      sel = eqr < k_eq;
+      ++eqr;
+    }
+    if (sel) {
+      const int j = j0 + i;
+      idx[o] = (uint32_t)j;
+      for (int g = 0; g < G; ++g)
+        p.w[((size_t)b * n_q + kvh * G + g) * nc + o] =
+            expf(lbase[(size_t)g * p.lstride + j] - S.M[g]) / S.Z[g];
+      ++o;
+    }
+  }
+  __syncthreads();
+  drop_rows(lbase, p.lstride, G, s);
+  finish_group(S, p, b, kvh);
+}
+
+// Any length: keys in a global scratch row (L2-resident), same rule.
+__global__ void __launch_bounds__(kT) select_kernel(const SelectParams p) {
+  __shared__ SelShared S;
+  const int row = blockIdx.x;
+  const int b = row / p.n_kv;
+  const int kvh = row - b * p.n_kv;
+  const int G = p.G;
+  const int n_q = p.n_kv * G;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const float* lbase = p.logits + ((size_t)b * n_q + kvh * G) * p.lstride;
+  uint32_t* keys = p.keys + (size_t)row * p.kstride;
+  uint32_t* idx = p.idx + (size_t)row * p.nc;
+  const int s = p.s, nc = p.nc;
+  load_stats(S, p, b, kvh);
+
+  for (int j = tid; j < s; j += kT) {
+    float acc = 0.0f;
+    for (int g = 0; g < G; ++g) {
+      const float pg = expf(lbase[(size_t)g * p.lstride + j] - S.M[g]) / S.Z[g];
+      acc = (g == 0) ? pg : acc + pg;
+    }
+    keys[j] = __float_as_uint(acc);
+  }
+  __syncthreads();
+
+  // strided radix passes over the scratch row
   uint32_t T = 0, k_eq = (uint32_t)nc;
   if (nc < s) {
-    // digit 0: bits 31..21
     clear_hist(S);
     for (int base = 0; base < s; base += kT) {
       const int j = base + tid;
-      const bool act = j < s;
-      const uint32_t k = act ? keys[j] : 0u;
-      hist_add(S.hist, k >> 21, act, lane);
+      hist_add(S.hist, (j < s ? keys[j] : 0u) >> 21, j < s, lane);
     }
     __syncthreads();
     find_bin(S, (uint32_t)nc);
     const uint32_t b0 = S.bin;
     uint32_t need = S.need;
-    // digit 1: bits 20..10
     clear_hist(S);
     for (int base = 0; base < s; base += kT) {
       const int j = base + tid;
       const uint32_t k = j < s ? keys[j] : 0u;
       const bool act = j < s && (k >> 21) == b0;
-      hist_add(S.hist, (k >> 10) & 0x7ffu, act, lane);
+      if (__any_sync(0xffffffffu, act)) hist_add(S.hist, (k >> 10) & 0x7ffu, act, lane);
     }
     __syncthreads();
     find_bin(S, need);
     const uint32_t p01 = (b0 << 11) | S.bin;
     need = S.need;
-    // digit 2: bits 9..0
     clear_hist(S);
     for (int base = 0; base < s; base += kT) {
       const int j = base + tid;
       const uint32_t k = j < s ? keys[j] : 0u;
       const bool act = j < s && (k >> 10) == p01;
-      hist_add(S.hist, k & 0x3ffu, act, lane);
+      if (__any_sync(0xffffffffu, act)) hist_add(S.hist, k & 0x3ffu, act, lane);
     }
     __syncthreads();
     find_bin(S, need);
@@ -131,7 +499,7 @@ __device__ void radix_compact(SelShared& S, const uint32_t* keys, int s, int nc,
     k_eq = S.need;
   }
 
-  // ordered compaction: keys > T, plus the first k_eq keys == T by position
+  // ordered compaction over per-warp contiguous segments
   const int seg = (((s + kNW - 1) / kNW) + 31) & ~31;
   const int w0 = warp * seg;
   const int w1 = min(s, w0 + seg);
@@ -180,109 +548,100 @@ __device__ void radix_compact(SelShared& S, const uint32_t* keys, int s, int nc,
     const uint32_t eqr = run_eq + __popc(beq & lt);
     const bool sel = (act && k > T) || (is_eq && eqr < k_eq);
     const uint32_t bsel = __ballot_sync(0xffffffffu, sel);
-    if (sel) idx[run_sel + __popc(bsel & lt)] = (uint32_t)j;
+    if (sel) {
+      const uint32_t o = run_sel + __popc(bsel & lt);
+      idx[o] = (uint32_t)j;
+      for (int g = 0; g < G; ++g)
+        p.w[((size_t)b * n_q + kvh * G + g) * nc + o] =
+            expf(lbase[(size_t)g * p.lstride + j] - S.M[g]) / S.Z[g];
+    }
     run_eq += __popc(beq);
     run_sel += __popc(bsel);
   }
   __syncthreads();
+  drop_rows(lbase, p.lstride, G, s);
+  drop_rows(reinterpret_cast<const float*>(keys), 0, 1, s);
+  finish_group(S, p, b, kvh);
 }
 
-__global__ void __launch_bounds__(kT) select_kernel(const SelectParams p) {
-  __shared__ SelShared S;
-  const int row = blockIdx.x;
-  const int b = row / p.n_kv;
-  const int kvh = row - b * p.n_kv;
-  const int G = p.G;
-  const int n_q = p.n_kv * G;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const float* lbase = p.logits + ((size_t)b * n_q + kvh * G) * p.lstride;
-  uint32_t* keys = p.keys + (size_t)row * p.kstride;
-  uint32_t* idx = p.idx + (size_t)row * p.nc;
-
-  // 1. global softmax stats per q head of the group
-  for (int g = warp; g < G; g += kNW) {
-    const float2* part = p.partials + ((size_t)b * n_q + kvh * G + g) * p.max_splits;
-    float m = -INFINITY;
-    for (int i = lane; i < p.n_splits; i += 32) m = fmaxf(m, part[i].x);
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if (lane == 0) {
-      float z = 0.0f;
-      for (int i = 0; i < p.n_splits; ++i) {
-        const float2 ml = part[i];
-        if (ml.y > 0.0f) z += ml.y * expf(ml.x - m);
-      }
-      S.M[g] = m;
-      S.Z[g] = z;
-    }
-  }
-  __syncthreads();
-
-  // 2. keys
-  for (int j = tid; j < p.s; j += kT) {
-    float acc = 0.0f;
-    for (int g = 0; g < G; ++g) {
-      const float pg = expf(lbase[(size_t)g * p.lstride + j] - S.M[g]) / S.Z[g];
-      acc = (g == 0) ? pg : acc + pg;
-    }
-    keys[j] = __float_as_uint(acc);
-  }
-  __syncthreads();
-
-  // 3-4. select
-  radix_compact(S, keys, p.s, p.nc, idx);
-
-  // 5. weights, dropped mass, renormaliser
-  for (int r = tid; r < p.nc; r += kT) {
-    const uint32_t j = idx[r];
-    for (int g = 0; g < G; ++g) {
-      const float pg = expf(lbase[(size_t)g * p.lstride + j] - S.M[g]) / S.Z[g];
-      p.w[((size_t)b * n_q + kvh * G + g) * p.nc + r] = pg;
-    }
-  }
-  __syncthreads();
-  for (int g = tid; g < G; g += kT) {
-    const size_t slot = (size_t)b * n_q + kvh * G + g;
-    const float* wg = p.w + slot * p.nc;
-    double mass = 0.0;
-    float sum = 0.0f;
-    for (int r = 0; r < p.nc; ++r) {
-      const float x = wg[r];
-      mass += (double)x;
-      sum += x;
-    }
-    p.dropped[slot] = 1.0 - mass;
-    p.norm[slot] = sum > 0.0f ? 1.0f / sum : 1.0f;
-  }
-}
-
+// arg_topk over raw floats: ordered-float keys, lowest index wins ties.
 __global__ void __launch_bounds__(kT)
     arg_topk_kernel(const float* values, int n, int nc, uint32_t* keys, uint32_t* out) {
   __shared__ SelShared S;
-  for (int j = threadIdx.x; j < n; j += kT) {
-    const uint32_t u = __float_as_uint(values[j]);
-    keys[j] = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
-  }
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int j = tid; j < n; j += kT) keys[j] = ordered_bits(values[j]);
   __syncthreads();
-  radix_compact(S, keys, n, nc, out);
+  uint32_t T = 0, k_eq = (uint32_t)nc;
+  if (nc < n) {
+    clear_hist(S);
+    for (int base = 0; base < n; base += kT) {
+      const int j = base + tid;
+      hist_add(S.hist, (j < n ? keys[j] : 0u) >> 21, j < n, lane);
+    }
+    __syncthreads();
+    find_bin(S, (uint32_t)nc);
+    const uint32_t b0 = S.bin;
+    uint32_t need = S.need;
+    clear_hist(S);
+    for (int base = 0; base < n; base += kT) {
+      const int j = base + tid;
+      const uint32_t k = j < n ? keys[j] : 0u;
+      hist_add(S.hist, (k >> 10) & 0x7ffu, j < n && (k >> 21) == b0, lane);
+    }
+    __syncthreads();
+    find_bin(S, need);
+    const uint32_t p01 = (b0 << 11) | S.bin;
+    need = S.need;
+    clear_hist(S);
+    for (int base = 0; base < n; base += kT) {
+      const int j = base + tid;
+      const uint32_t k = j < n ? keys[j] : 0u;
+      hist_add(S.hist, k & 0x3ffu, j < n && (k >> 10) == p01, lane);
+    }
+    __syncthreads();
+    find_bin(S, need);
+    T = (p01 << 10) | S.bin;
+    k_eq = S.need;
+  }
+  const int seg = (((n + kNW - 1) / kNW) + 31) & ~31;
+  const int w0 = warp * seg;
+  const int w1 = min(n, w0 + seg);
+  uint32_t cgt = 0, ceq = 0;
+  for (int j0 = w0; j0 < w1; j0 += 32) {
+    const int j = j0 + lane;
+    const bool act = j < w1;
+    const uint32_t k = act ? keys[j] : 0u;
+    cgt += __popc(__ballot_sync(0xffffffffu, act && k > T));
+    ceq += __popc(__ballot_sync(0xffffffffu, act && k == T));
+  }
+  const uint32_t eq_base = block_excl_scan(lane == 0 ? ceq : 0u, S.wa);
+  const uint32_t take = eq_base >= k_eq ? 0u : min(ceq, k_eq - eq_base);
+  uint32_t run_sel = block_excl_scan(lane == 0 ? cgt + take : 0u, S.wb);
+  run_sel = __shfl_sync(0xffffffffu, run_sel, 0);
+  uint32_t run_eq = __shfl_sync(0xffffffffu, eq_base, 0);
+  const uint32_t lt = lanemask_lt();
+  for (int j0 = w0; j0 < w1; j0 += 32) {
+    const int j = j0 + lane;
+    const bool act = j < w1;
+    const uint32_t k = act ? keys[j] : 0u;
+    const bool is_eq = act && k == T;
+    const uint32_t beq = __ballot_sync(0xffffffffu, is_eq);
+    const uint32_t eqr = run_eq + __popc(beq & lt);
+    const bool sel = (act && k > T) || (is_eq && eqr < k_eq);
+    const uint32_t bsel = __ballot_sync(0xffffffffu, sel);
+    if (sel) out[run_sel + __popc(bsel & lt)] = (uint32_t)j;
+    run_eq += __popc(beq);
+    run_sel += __popc(bsel);
+  }
 }
 
 __global__ void __launch_bounds__(256) probs_kernel(const SelectParams p, float* probs) {
   __shared__ float sMZ[2];
   const int slot = blockIdx.x;  // b*n_q + head
-  const int lane = threadIdx.x & 31;
-  const float2* part = p.partials + (size_t)slot * p.max_splits;
   if (threadIdx.x < 32) {
-    float m = -INFINITY;
-    for (int i = lane; i < p.n_splits; i += 32) m = fmaxf(m, part[i].x);
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if (lane == 0) {
-      float z = 0.0f;
-      for (int i = 0; i < p.n_splits; ++i) {
-        const float2 ml = part[i];
-        if (ml.y > 0.0f) z += ml.y * expf(ml.x - m);
-      }
+    float m, z;
+    softmax_stats(p.partials + (size_t)slot * p.max_splits, p.n_splits, threadIdx.x, m, z);
+    if (threadIdx.x == 0) {
       sMZ[0] = m;
       sMZ[1] = z;
     }
@@ -295,12 +654,20 @@ __global__ void __launch_bounds__(256) probs_kernel(const SelectParams p, float*
 
 }  // namespace
 
-void probs_launch(const SelectParams& p, float* probs, cudaStream_t st) {
-  probs_kernel<<<p.rows * p.G, 256, 0, st>>>(p, probs);
+void select_launch(const SelectParams& p, cudaStream_t st) {
+  // register-resident keys up to 32 per thread (s <= 32768); the lstride
+  // padding (multiple of 32 floats) keeps the float4 loads in bounds.
+  if (!p.force_global && p.G <= kMaxG) {
+    if (p.s <= 4 * kT) { select_reg_kernel<4><<<p.rows, kT, 0, st>>>(p); return; }
+    if (p.s <= 8 * kT) { select_reg_kernel<8><<<p.rows, kT, 0, st>>>(p); return; }
+    if (p.s <= 16 * kT) { select_reg_kernel<16><<<p.rows, kT, 0, st>>>(p); return; }
+    if (p.s <= 32 * kT) { select_reg_kernel<32><<<p.rows, kT, 0, st>>>(p); return; }
+  }
+  select_kernel<<<p.rows, kT, 0, st>>>(p);
 }
 
-void select_launch(const SelectParams& p, cudaStream_t st) {
-  select_kernel<<<p.rows, kT, 0, st>>>(p);
+void probs_launch(const SelectParams& p, float* probs, cudaStream_t st) {
+  probs_kernel<<<p.rows * p.G, 256, 0, st>>>(p, probs);
 }
 
 void arg_topk_launch(const float* values, int n, int k, uint32_t* keys_scratch, uint32_t* out,

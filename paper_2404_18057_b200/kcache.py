@@ -100,6 +100,9 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         "kc_layer_storage": (i32, [vp, u64, C.POINTER(vp), C.POINTER(vp), C.POINTER(i32)]),
         "kc_sync": (i32, [vp]),
         "kc_set_tuning": (i32, [vp, C.c_char_p, C.c_int64]),
+        "kc_profile": (i32, [vp, i32]),
+        "kc_profile_read": (i32, [vp, C.c_char_p, C.POINTER(C.c_double), p64]),
+        "kc_profile_launch": (i32, [vp, C.c_char_p, u64, C.POINTER(C.c_double)]),
         "kc_arg_topk": (i32, [vp, u64, u64, vp, p64]),
         "kc_fill_uniform": (i32, [vp, i32, u64, u64, u64, C.c_float, C.c_float, vp]),
     }
@@ -411,6 +414,25 @@ class TieredKVCache:
 
     def sync(self) -> None:
         _check(self._lib.kc_sync(self._h))
+
+    def profile(self, enable: bool) -> None:
+        _check(self._lib.kc_profile(self._h, int(enable)))
+
+    def profile_read(self, kernel: str):
+        """(summed device ms, launches) of 'score' / 'select' / 'recall'."""
+        ms, n = C.c_double(0), C.c_uint64(0)
+        _check(self._lib.kc_profile_read(self._h, kernel.encode(), C.byref(ms), C.byref(n)))
+        return ms.value, n.value
+
+    def profile_launches(self, kernel: str) -> list:
+        """Per-launch device ms of 'score' / 'select' / 'recall'."""
+        _, n = self.profile_read(kernel)
+        out = []
+        for i in range(n):
+            ms = C.c_double(0)
+            _check(self._lib.kc_profile_launch(self._h, kernel.encode(), i, C.byref(ms)))
+            out.append(ms.value)
+        return out
 
     # ---- device-resident decode (bench / engine path) ----
     def decode_topn_layers_device(self, layers: Sequence[int], qs, top_n: int, outs, renormalize=False,

@@ -68,9 +68,11 @@ CASES = [
 
 @pytest.mark.parametrize("case", CASES, ids=[str(c) for c in CASES])
 @pytest.mark.parametrize("renorm", [False, True])
-def test_random_cases_vs_oracle(kc, oracle, case, renorm):
+@pytest.mark.parametrize("select_global", [0, 1])
+def test_random_cases_vs_oracle(kc, oracle, case, renorm, select_global):
     b, n, n_kv, h, s, N, dtype = case
     cache, ks, vs = build_cache(kc, b, n, n_kv, h, s, dtype)
+    cache.set_tuning("select_global", select_global)
     q = synth_matrix(1, b, n * h, dtype=dtype)
     res = kc.decode_attention_topn(q, cache, 0, N, renorm)
     compare_all(oracle, res, q, ks[0], vs[0], b, n, n_kv, h, s, N, renorm)
@@ -125,6 +127,37 @@ def test_pipelined_layers_equal_single_calls(kc):
         np.testing.assert_array_equal(outs[l]["weights"], singles[l].selection.weights)
         np.testing.assert_array_equal(outs[l]["dropped"], singles[l].selection.dropped_mass)
         assert info[l] == (nc, 2 * b * n_kv * nc * h)
+
+
+@pytest.mark.parametrize("recall_mode", [0, 1])
+def test_repeated_decode_and_decode_appends(kc, oracle, recall_mode):
+    """Decode is idempotent across calls (the scoring kernel drops consumed,
+    clean K lines from L2 -- it must never lose data), and K/V appended in the
+    decode phase (engine.cpp:143: append before attention) are scored and
+    recalled; the appended V goes to the host arena with a D2H ledger event."""
+    b, n, n_kv, h, s, N = 2, 8, 4, 128, 700, 64
+    cache, ks, vs = build_cache(kc, b, n, n_kv, h, s, "f16", max_seq=s + 8)
+    cache.set_tuning("recall_mode", recall_mode)
+    q = synth_matrix(1, b, n * h)
+    first = kc.decode_attention_topn(q, cache, 0, N, False)
+    for _ in range(4):
+        again = kc.decode_attention_topn(q, cache, 0, N, False)
+        np.testing.assert_array_equal(again.out, first.out)
+        np.testing.assert_array_equal(again.selection.indices, first.selection.indices)
+    k, v = ks[0], vs[0]
+    d2h0 = cache.d2h_bytes_total()
+    for step in range(3):
+        knew = synth_matrix(50 + step, b, n_kv * h)
+        vnew = synth_matrix(60 + step, b, n_kv * h)
+        knew[:, :h] = 4.0 * np.float32(np.float16(0.25))  # make the new position attractive for kv head 0
+        cache.append_kv(0, knew, vnew)
+        k = np.concatenate([k, knew])
+        v = np.concatenate([v, vnew])
+        assert cache.d2h_bytes_total() - d2h0 == 2 * b * n_kv * h * (step + 1)
+        res = kc.decode_attention_topn(q, cache, 0, N, False)
+        compare_all(oracle, res, q, k, v, b, n, n_kv, h, s + step + 1, N, False)
+        res2 = kc.decode_attention_topn(q, cache, 0, N, False)
+        np.testing.assert_array_equal(res2.out, res.out)
 
 
 def test_resident_layer_reads_hbm_v(kc, oracle):
