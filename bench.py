@@ -216,7 +216,7 @@ def run_ours(args, cfg):
              "weights": torch.empty(slots, nc, dtype=torch.float32, device=dev),
              "dropped": torch.empty(slots, dtype=torch.float64, device=dev)} for _ in range(L)]
     layers = list(range(L))
-    stream = torch.cuda.current_stream()
+    stream = torch.cuda.Stream(device=dev)  # a dedicated (non-legacy) stream for the device path
 
     def barrier():
         if world > 1:
@@ -225,26 +225,38 @@ def run_ours(args, cfg):
     def step():
         return cache.decode_topn_layers_device(layers, qs, N, outs, stream=stream)
 
+    def timed_steps(n):
+        torch.cuda.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        for _ in range(n):
+            inf = step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        return ev0.elapsed_time(ev1) / n, inf
+
     sampler = ClockSampler(local_rank)
     sampler.start()
     for _ in range(args.warmup):
         step()
-    torch.cuda.synchronize()
-    barrier()
-    torch.cuda.synchronize()
-    cache.profile(True)
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
-    ev0.record(stream)
-    for _ in range(args.steps):
-        info = step()
-    ev1.record(stream)
-    torch.cuda.synchronize()
-    barrier()
-    ms_local = ev0.elapsed_time(ev1) / args.steps
+    # the timed region: no per-kernel events inside
+    ms_local, info = timed_steps(args.steps)
+    # separate profiled passes: events around the scoring launches only (the
+    # roofline kernel; its step time shows the perturbation), then around every
+    # launch for the breakdown
+    prof_steps = min(args.steps, 10)
+    cache.profile(True, kinds=("score",))
+    score_prof_ms, _ = timed_steps(prof_steps)
     score_ms, score_n = cache.profile_read("score")
+    cache.profile(True)
+    prof_ms, _ = timed_steps(prof_steps)
     select_ms, select_n = cache.profile_read("select")
     recall_ms, recall_n = cache.profile_read("recall")
+    all_score_ms, _ = cache.profile_read("score")
     cache.profile(False)
     h2d_per_layer = info[0][1]
 
@@ -324,8 +336,11 @@ def run_ours(args, cfg):
                           "t_roof_sum_ms": (t_k + t_v) * 1e3, "t_roof_max_ms": max(t_k, t_v) * 1e3,
                           "frac_of_sum_roofline": (t_k + t_v) * 1e3 / ms,
                           "frac_of_max_roofline": max(t_k, t_v) * 1e3 / ms},
-        "kernel_ms_per_step": {"score": score_ms / args.steps, "select": select_ms / args.steps,
-                               "recall_pv": recall_ms / args.steps},
+        "kernel_ms_per_step": {"score": all_score_ms / prof_steps, "select": select_ms / prof_steps,
+                               "recall_pv": recall_ms / prof_steps, "profiled_step_ms": prof_ms,
+                               "score_only_profiled_step_ms": score_prof_ms,
+                               "note": "separate profiled passes (CUDA events around launches perturb the "
+                                       "pipelined overlap; ms_per_step is the unprofiled timed region)"},
         "h2d_ledger_bytes_per_layer": h2d_per_layer,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": L * b * d * 4,
                 "d2h_bytes_per_step": L * (b * d * 4 + slots * nc * 8 + slots * 8), "ms_per_step": e2e_ms,

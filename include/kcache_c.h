@@ -160,12 +160,16 @@ int kc_set_tuning(kc_cache* cache, const char* key, int64_t value);
 
 /* Per-kernel CUDA-event timing of subsequent decode calls (bench / roofline):
  * kc_profile(c, 1) clears and starts recording one event pair around every
- * scoring, selection and recall launch on the stream it runs on;
+ * scoring, selection and recall launch on the stream it runs on
+ * (kc_profile(c, mask << 1) for a subset: mask bit 0 score, 1 select,
+ * 2 recall; kc_profile(c, 0) stops);
  * kc_profile_read(c, "score"|"select"|"recall", ...) returns the summed
  * device time and the launch count. */
 int kc_profile(kc_cache* cache, int enable);
 int kc_profile_read(kc_cache* cache, const char* kernel, double* total_ms, uint64_t* launches);
 int kc_profile_launch(kc_cache* cache, const char* kernel, uint64_t i, double* ms);
+/* start / end of launch i in ms since the first profiled event (timelines) */
+int kc_profile_span(kc_cache* cache, const char* kernel, uint64_t i, double* t0, double* t1);
 
 /* arg_topk (matrix.hpp:49-52, matrix.cpp:109-122) on the GPU: indices of the
  * k largest of n host floats, ties to the lowest index, ascending. */

@@ -119,7 +119,10 @@ struct LayerState {
 constexpr int kRing = 3;
 
 // V recall strategies for offloaded layers (kc_set_tuning "recall_mode"):
-// the host-compaction + DMA path is the default (see kc_gather.hpp).
+// zero-copy SM loads of the selected rows from the mapped host arena (the
+// default: with consumed K lines dropped from L2 it reaches ~40 GB/s and hides
+// under the next layer's scoring), or host-side compaction + one DMA per
+// layer (kc_gather.hpp; bounded by host memory latency on this box).
 constexpr int kRecallAuto = 0, kRecallZeroCopy = 1, kRecallDma = 2;
 
 bool host_pinned(const void* p) {
@@ -176,6 +179,8 @@ struct kc_cache {
   int recall_mode = kRecallAuto;
   int discard = 1;
   int select_global = 0;
+  int score_stages = 4;
+  int recall_ctas = 64;  // CTAs of the recall kernel (0: one per (batch, kv head))
   int gather_threads = 0;  // 0: min(8, cores/2)
 
   // per-kernel CUDA-event timing (kc_profile): [kind] -> (start, stop) pairs
@@ -192,9 +197,10 @@ struct kc_cache {
     return prof_pool[prof_used++];
   }
   // record around one launch when profiling is on
+  int prof_mask = 0;  // bit k: time launches of kind k (0 score, 1 select, 2 recall)
   template <typename F>
   void timed(int kind, cudaStream_t st, F&& launch) {
-    if (!prof_on) {
+    if (!prof_on || !((prof_mask >> kind) & 1)) {
       launch();
       return;
     }
@@ -430,6 +436,7 @@ void enqueue_score(kc_cache* c, uint64_t layer, const float* q32, const StepGeom
   sp.scale = 1.0f / std::sqrt(static_cast<float>(c->h));  // attention.hpp:15-17
   sp.discard_len = (int)std::min<uint64_t>(c->layers[layer].clean_len, (uint64_t)g.s);
   if (!c->discard) sp.discard_len = 0;
+  sp.stages = c->score_stages;
   c->timed(0, st, [&] { kc::score_launch(sp, c->dtype, st); });
 }
 
@@ -527,7 +534,7 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
     rp.v = c->v_layer(layer);
     // Offloaded layer: compact the selected rows on the host (pool threads,
     // stream-ordered via cudaLaunchHostFunc on gather_st), then one DMA.
-    const bool dma = layer >= c->L && c->recall_mode != kRecallZeroCopy;
+    const bool dma = layer >= c->L && c->recall_mode == kRecallDma;
     const size_t stage_bytes = c->rows * nc * c->h * c->esz;
     if (dma) {
       c->idx_host[slot].ensure(c->rows * nc * 4);
@@ -559,6 +566,7 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
       rp.v = c->stage_dev[slot].p;
     }
     rp.staged = dma ? 1 : 0;
+    rp.grid = c->recall_ctas;
     rp.idx = c->idx[slot].as<uint32_t>();
     rp.w = c->w[slot].as<float>();
     rp.norm = c->norm[slot].as<float>();
@@ -986,6 +994,8 @@ int kc_set_tuning(kc_cache* c, const char* key, int64_t value) {
     else if (k == "pipeline") c->pipeline = value ? 1 : 0;
     else if (k == "discard") c->discard = value ? 1 : 0;
     else if (k == "select_global") c->select_global = value ? 1 : 0;
+    else if (k == "score_stages") c->score_stages = (int)value;
+    else if (k == "recall_ctas") c->recall_ctas = (int)value;
     else if (k == "recall_mode") {
       if (value < 0 || value > 2) fail(KC_EARG, "recall_mode: 0 auto, 1 zero-copy, 2 dma");
       c->recall_mode = (int)value;
@@ -1006,6 +1016,8 @@ int kc_profile(kc_cache* c, int enable) {
     CK(cudaStreamSynchronize(c->main_st));
     CK(cudaStreamSynchronize(c->side_st));
     c->prof_on = enable != 0;
+    // enable: 1 = every kind; otherwise (enable >> 1) is a kind bit mask
+    c->prof_mask = enable == 1 ? 7 : (enable >> 1) & 7;
     for (auto& v : c->prof) v.clear();
     c->prof_used = 0;
   });
@@ -1026,6 +1038,22 @@ int kc_profile_read(kc_cache* c, const char* kernel, double* total_ms, uint64_t*
     }
     *total_ms = total;
     *launches = c->prof[kind].size();
+  });
+}
+
+int kc_profile_span(kc_cache* c, const char* kernel, uint64_t i, double* t0, double* t1) {
+  return guarded([&] {
+    const std::string k = kernel ? kernel : "";
+    const int kind = k == "score" ? 0 : k == "select" ? 1 : k == "recall" ? 2 : -1;
+    if (kind < 0 || i >= c->prof[kind].size() || c->prof_pool.empty())
+      fail(KC_EARG, "kc_profile_span: bad kernel or index");
+    set_dev(c);
+    CK(cudaEventSynchronize(c->prof[kind][i].second));
+    float a = 0.0f, b = 0.0f;
+    CK(cudaEventElapsedTime(&a, c->prof_pool[0], c->prof[kind][i].first));
+    CK(cudaEventElapsedTime(&b, c->prof_pool[0], c->prof[kind][i].second));
+    *t0 = a;
+    *t1 = b;
   });
 }
 

@@ -29,6 +29,7 @@ struct ScoreParams {
   int max_splits;
   float scale;          // 1/sqrt(h) as the reference computes it
   int discard_len;      // K positions < discard_len are clean: drop their L2 lines after use
+  int stages;           // TMA ring depth (4, 6 or 8 stages of 64 positions)
 };
 // Read `bytes` of a scratch buffer larger than L2: evicts (and so writes back)
 // every dirty L2 line, after which all stored K is clean in DRAM.
@@ -83,6 +84,7 @@ struct RecallParams {
   int reverse;            // fault hook: descending accumulation
   int row_offset;         // first row of this launch (pipelined chunks)
   int staged;             // v is the compacted [rows][nc][h] block (DMA recall)
+  int grid;               // CTAs (0: one per row); CTAs loop over rows
 };
 void recall_launch(const RecallParams& p, int dtype, cudaStream_t st);
 

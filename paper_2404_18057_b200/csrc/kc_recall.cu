@@ -28,7 +28,9 @@ constexpr int kRecallSmem = 40 * 1024;
 template <typename T>
 __global__ void __launch_bounds__(kRecallThreads) recall_pv_kernel(const RecallParams p, int rc_max) {
   extern __shared__ __align__(16) uint8_t smem[];
-  const int row = p.row_offset + blockIdx.x;
+  // grid <= rows: each CTA walks rows blockIdx.x, +gridDim.x, ... so a small
+  // grid leaves SM room for the concurrently running scoring kernel
+  for (int row = p.row_offset + blockIdx.x; row < p.row_offset + p.rows; row += gridDim.x) {
   const int b = row / p.n_kv;
   const int kvh = row - b * p.n_kv;
   const int G = p.G, h = p.h, n_q = p.n_kv * G, nc = p.nc;
@@ -116,6 +118,7 @@ __global__ void __launch_bounds__(kRecallThreads) recall_pv_kernel(const RecallP
       p.out[((size_t)b * n_q + kvh * G + g) * h + c] = acc[i];
     }
   }
+  }  // row loop
 }
 
 // decode_attention_full P.V: CTA (split, row) accumulates its positions in
@@ -310,10 +313,11 @@ void recall_launch(const RecallParams& p, int dtype, cudaStream_t st) {
   int rc_max = (int)(kRecallSmem / (rowb + 4 * (size_t)p.G));
   rc_max = std::max(1, std::min(rc_max, p.nc));
   const size_t smem = ((rc_max * rowb + 15) & ~size_t(15)) + 4 * (size_t)p.G * rc_max;
+  const int grid = (p.grid > 0 && p.grid < p.rows) ? p.grid : p.rows;
   switch (dtype) {
-    case KC_F16: recall_pv_kernel<__half><<<p.rows, kRecallThreads, smem, st>>>(p, rc_max); break;
-    case KC_BF16: recall_pv_kernel<__nv_bfloat16><<<p.rows, kRecallThreads, smem, st>>>(p, rc_max); break;
-    default: recall_pv_kernel<float><<<p.rows, kRecallThreads, smem, st>>>(p, rc_max); break;
+    case KC_F16: recall_pv_kernel<__half><<<grid, kRecallThreads, smem, st>>>(p, rc_max); break;
+    case KC_BF16: recall_pv_kernel<__nv_bfloat16><<<grid, kRecallThreads, smem, st>>>(p, rc_max); break;
+    default: recall_pv_kernel<float><<<grid, kRecallThreads, smem, st>>>(p, rc_max); break;
   }
 }
 

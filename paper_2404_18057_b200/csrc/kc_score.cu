@@ -26,7 +26,6 @@ namespace kc {
 namespace {
 
 constexpr int kRows = 64;     // positions per pipeline stage
-constexpr int kStages = 4;    // ring depth
 constexpr int kCWarps = 8;    // consumer warps
 constexpr int kH = 128;       // head_dim of the fast path
 
@@ -43,7 +42,7 @@ __device__ __forceinline__ int chunk_of(int ci, int rl, int sub) {
   }
 }
 
-template <typename T, int G, int LPR>
+template <typename T, int G, int LPR, int STAGES>
 __global__ void __launch_bounds__((kCWarps + 1) * 32)
     score_fast_kernel(const ScoreParams p) {
   constexpr int CPL = 16 / LPR;            // 16-B chunks per lane per row
@@ -54,9 +53,9 @@ __global__ void __launch_bounds__((kCWarps + 1) * 32)
 
   extern __shared__ __align__(128) uint8_t smem[];
   uint8_t* ring = smem;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kRows * ROWB);
-  uint64_t* empty = full + kStages;
-  float2* red = reinterpret_cast<float2*>(empty + kStages);  // [kCWarps][G]
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * kRows * ROWB);
+  uint64_t* empty = full + STAGES;
+  float2* red = reinterpret_cast<float2*>(empty + STAGES);  // [kCWarps][G]
 
   const int split = blockIdx.x;
   const int row = blockIdx.y;
@@ -70,7 +69,7 @@ __global__ void __launch_bounds__((kCWarps + 1) * 32)
 
   if (threadIdx.x == 0) {
 #pragma unroll
-    for (int st = 0; st < kStages; ++st) {
+    for (int st = 0; st < STAGES; ++st) {
       mbar_init(&full[st], 1);
       mbar_init(&empty[st], kCWarps);
     }
@@ -95,10 +94,10 @@ __global__ void __launch_bounds__((kCWarps + 1) * 32)
       for (int l = lane; l < lines; l += 32) discard_l2_line(base + (size_t)l * 128);
     };
     for (int it = 0; it < n_it; ++it) {
-      const int st = it % kStages;
-      if (it >= kStages) {
-        mbar_wait(&empty[st], ((it / kStages) - 1) & 1);
-        drop(it - kStages);
+      const int st = it % STAGES;
+      if (it >= STAGES) {
+        mbar_wait(&empty[st], ((it / STAGES) - 1) & 1);
+        drop(it - STAGES);
       }
       if (lane == 0) {
         const int rows = min(kRows, npos - it * kRows);
@@ -109,8 +108,8 @@ __global__ void __launch_bounds__((kCWarps + 1) * 32)
       }
       __syncwarp();
     }
-    for (int it = max(0, n_it - kStages); it < n_it; ++it) {
-      mbar_wait(&empty[it % kStages], (it / kStages) & 1);
+    for (int it = max(0, n_it - STAGES); it < n_it; ++it) {
+      mbar_wait(&empty[it % STAGES], (it / STAGES) & 1);
       drop(it);
     }
     return;
@@ -137,8 +136,8 @@ __global__ void __launch_bounds__((kCWarps + 1) * 32)
   float* lrow = p.logits + ((size_t)b * n_q + kvh * G + (sub < G ? sub : 0)) * p.lstride + pos0;
 
   for (int it = 0; it < n_it; ++it) {
-    const int st = it % kStages;
-    mbar_wait(&full[st], (it / kStages) & 1);
+    const int st = it % STAGES;
+    mbar_wait(&full[st], (it / STAGES) & 1);
     const uint8_t* sb = ring + st * kRows * ROWB;
 #pragma unroll
     for (int pass = 0; pass < PASSES; ++pass) {
@@ -239,19 +238,30 @@ __global__ void __launch_bounds__(256) score_generic_kernel(const ScoreParams p)
   }
 }
 
-template <typename T, int G, int LPR>
-void launch_fast(const ScoreParams& p, cudaStream_t st) {
+template <typename T, int G, int LPR, int STAGES>
+void launch_fast_s(const ScoreParams& p, cudaStream_t st) {
   constexpr int ROWB = kH * (int)sizeof(T);
-  const size_t smem = kStages * kRows * ROWB + 2 * kStages * sizeof(uint64_t) +
+  const size_t smem = STAGES * kRows * ROWB + 2 * STAGES * sizeof(uint64_t) +
                       kCWarps * G * sizeof(float2);
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(score_fast_kernel<T, G, LPR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  static unsigned long long configured = 0;  // one bit per device
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!(configured >> (dev & 63) & 1ull)) {
+    cudaFuncSetAttribute(score_fast_kernel<T, G, LPR, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
-    configured = true;
+    configured |= 1ull << (dev & 63);
   }
   dim3 grid(p.n_splits, p.rows);
-  score_fast_kernel<T, G, LPR><<<grid, (kCWarps + 1) * 32, smem, st>>>(p);
+  score_fast_kernel<T, G, LPR, STAGES><<<grid, (kCWarps + 1) * 32, smem, st>>>(p);
+}
+
+template <typename T, int G, int LPR>
+void launch_fast(const ScoreParams& p, cudaStream_t st) {
+  switch (p.stages) {
+    case 6: launch_fast_s<T, G, LPR, 6>(p, st); break;
+    case 8: launch_fast_s<T, G, LPR, 8>(p, st); break;
+    default: launch_fast_s<T, G, LPR, 4>(p, st); break;
+  }
 }
 
 template <typename T>

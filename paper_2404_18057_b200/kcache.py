@@ -103,6 +103,7 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         "kc_profile": (i32, [vp, i32]),
         "kc_profile_read": (i32, [vp, C.c_char_p, C.POINTER(C.c_double), p64]),
         "kc_profile_launch": (i32, [vp, C.c_char_p, u64, C.POINTER(C.c_double)]),
+        "kc_profile_span": (i32, [vp, C.c_char_p, u64, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
         "kc_arg_topk": (i32, [vp, u64, u64, vp, p64]),
         "kc_fill_uniform": (i32, [vp, i32, u64, u64, u64, C.c_float, C.c_float, vp]),
     }
@@ -415,8 +416,10 @@ class TieredKVCache:
     def sync(self) -> None:
         _check(self._lib.kc_sync(self._h))
 
-    def profile(self, enable: bool) -> None:
-        _check(self._lib.kc_profile(self._h, int(enable)))
+    def profile(self, enable: bool, kinds=("score", "select", "recall")) -> None:
+        """Per-launch CUDA-event timing of the given kernel kinds."""
+        mask = sum(1 << i for i, k in enumerate(("score", "select", "recall")) if k in kinds)
+        _check(self._lib.kc_profile(self._h, (mask << 1) if enable else 0))
 
     def profile_read(self, kernel: str):
         """(summed device ms, launches) of 'score' / 'select' / 'recall'."""
@@ -432,6 +435,16 @@ class TieredKVCache:
             ms = C.c_double(0)
             _check(self._lib.kc_profile_launch(self._h, kernel.encode(), i, C.byref(ms)))
             out.append(ms.value)
+        return out
+
+    def profile_spans(self, kernel: str) -> list:
+        """[(start_ms, end_ms)] of every profiled launch since profile(True)."""
+        _, n = self.profile_read(kernel)
+        out = []
+        for i in range(n):
+            a, b = C.c_double(0), C.c_double(0)
+            _check(self._lib.kc_profile_span(self._h, kernel.encode(), i, C.byref(a), C.byref(b)))
+            out.append((a.value, b.value))
         return out
 
     # ---- device-resident decode (bench / engine path) ----
