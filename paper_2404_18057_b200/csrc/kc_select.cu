@@ -169,7 +169,8 @@ __device__ __forceinline__ void radix_threshold(SelShared& S, Get&& get, int nc,
 }
 
 __device__ __forceinline__ uint32_t ordered_bits(float x) {
-  const uint32_t u = __float_as_uint(x);
+  // -0.0 and +0.0 compare equal, so they must tie (one key)
+  const uint32_t u = x == 0.0f ? 0u : __float_as_uint(x);
   return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
 }
 
