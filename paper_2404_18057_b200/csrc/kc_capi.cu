@@ -180,6 +180,10 @@ struct kc_cache {
   int discard = 1;
   int select_global = 0;
   int score_stages = 4;
+  // persistent scoring grid (ctas_per_sm x SMs); 0 = one CTA per work item,
+  // the default: with the recall kernel co-running, the hardware block
+  // scheduler's dynamic balancing beats a static persistent split (measured)
+  int score_ctas_per_sm = 0;
   int recall_ctas = 64;  // CTAs of the recall kernel (0: one per (batch, kv head))
   int gather_threads = 0;  // 0: min(8, cores/2)
 
@@ -437,6 +441,7 @@ void enqueue_score(kc_cache* c, uint64_t layer, const float* q32, const StepGeom
   sp.discard_len = (int)std::min<uint64_t>(c->layers[layer].clean_len, (uint64_t)g.s);
   if (!c->discard) sp.discard_len = 0;
   sp.stages = c->score_stages;
+  sp.ctas_per_sm = c->score_ctas_per_sm;
   c->timed(0, st, [&] { kc::score_launch(sp, c->dtype, st); });
 }
 
@@ -995,6 +1000,7 @@ int kc_set_tuning(kc_cache* c, const char* key, int64_t value) {
     else if (k == "discard") c->discard = value ? 1 : 0;
     else if (k == "select_global") c->select_global = value ? 1 : 0;
     else if (k == "score_stages") c->score_stages = (int)value;
+    else if (k == "score_ctas_per_sm") c->score_ctas_per_sm = (int)value;
     else if (k == "recall_ctas") c->recall_ctas = (int)value;
     else if (k == "recall_mode") {
       if (value < 0 || value > 2) fail(KC_EARG, "recall_mode: 0 auto, 1 zero-copy, 2 dma");

@@ -30,6 +30,7 @@ struct ScoreParams {
   float scale;          // 1/sqrt(h) as the reference computes it
   int discard_len;      // K positions < discard_len are clean: drop their L2 lines after use
   int stages;           // TMA ring depth (4, 6 or 8 stages of 64 positions)
+  int ctas_per_sm;      // persistent grid = ctas_per_sm x SMs (0: one CTA per item)
 };
 // Read `bytes` of a scratch buffer larger than L2: evicts (and so writes back)
 // every dirty L2 line, after which all stored K is clean in DRAM.

@@ -3,18 +3,24 @@
 // Replaces head_weights + dot_scaled (proj/core/src/attention.cpp:15-21,66-78)
 // and the max/sum half of softmax_inplace (proj/core/src/matrix.cpp:45-61).
 //
-// Grid (split, row): row = b*n_kv + kv_head, split = a chunk of positions.
-// The row's K for the chunk is one contiguous run of chunk*h elements in the
-// [b][kv][pos][h] arena, so a single elected thread streams it into a
-// 4-stage shared-memory ring with 1-D TMA bulk copies (cp.async.bulk, L2
-// evict-first) on mbarriers; eight consumer warps score 64-position stages
-// against every q head of the GQA group held in registers (the K tile is
+// Work items are (row, split): row = b*n_kv + kv_head, split = a chunk of
+// positions. A row's K for one split is one contiguous run of chunk*h
+// elements in the [b][kv][pos][h] arena. The kernel is persistent: a grid of
+// ctas_per_sm x 148 CTAs walks the items (item = blockIdx.x, +gridDim.x, ...),
+// so the TMA ring never drains between items and every SM keeps headroom for
+// the selection / recall kernels that run concurrently on the side stream.
+// In each CTA one elected producer lane streams K stages (64 positions = 16 KB)
+// into a STAGES-deep shared-memory ring with 1-D TMA bulk copies
+// (cp.async.bulk, L2 evict-first) on mbarriers; eight consumer warps score
+// them against every q head of the GQA group held in registers (the K tile is
 // read from HBM once per kv head, not once per q head). Each lane owns 128/LPR
 // elements of a row (LPR lanes per row, 16-B chunks rotated per row so a
 // quarter-warp's 16-B shared loads hit eight distinct bank groups), FMA in
 // fp32, log2(LPR) xor-shuffles per row. Writes fp32 logits (score * scale, the
 // multiply after the sum like dot_scaled) and a per-split online (max, sum
-// exp) per q head; select_kernel combines the splits into the global softmax.
+// exp) per q head; softmax_stats combines the splits into the global softmax.
+// After a stage is consumed the producer warp drops its K lines from L2 (see
+// DESIGN.md section 5).
 #include <algorithm>
 
 #include "kc_device.cuh"
@@ -57,13 +63,7 @@ __global__ void __launch_bounds__((kCWarps + 1) * 32)
   uint64_t* empty = full + STAGES;
   float2* red = reinterpret_cast<float2*>(empty + STAGES);  // [kCWarps][G]
 
-  const int split = blockIdx.x;
-  const int row = blockIdx.y;
-  const int b = row / p.n_kv;
-  const int kvh = row - b * p.n_kv;
-  const int pos0 = split * p.chunk;
-  const int npos = min(p.chunk, p.s - pos0);
-  const int n_it = (npos + kRows - 1) / kRows;
+  const int n_items = p.rows * p.n_splits;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
 
@@ -79,38 +79,50 @@ __global__ void __launch_bounds__((kCWarps + 1) * 32)
 
   if (warp == kCWarps) {
     // ---------------- producer warp: lane 0 streams K with TMA ----------------
-    // Once a stage has been consumed, the warp drops that stage's K lines from
+    // Once a stage has been consumed the warp drops that stage's K lines from
     // L2 (discard.global.L2, positions < discard_len, which the store keeps
     // clean): a decode step streams the whole K cache once, and an L2 left full
-    // of dead K lines makes the following zero-copy V recall ~1.5x slower
-    // (tools/h2d_probe2.cu). K itself is never written here.
-    const T* kslot = static_cast<const T*>(p.k) + (size_t)row * p.max_seq * kH;
+    // of dead K lines makes the following zero-copy V recall ~1.5x slower.
     const uint64_t pol = l2_evict_first_policy();
-    auto drop = [&](int it) {
-      const int pstart = pos0 + it * kRows;
-      const int pend = min(pos0 + min(npos, (it + 1) * kRows), p.discard_len);
-      const char* base = reinterpret_cast<const char*>(kslot + (size_t)pstart * kH);
-      const int lines = (pend - pstart) * (ROWB / 128);
-      for (int l = lane; l < lines; l += 32) discard_l2_line(base + (size_t)l * 128);
+    const char* held[STAGES];  // what each ring slot holds: start + line count
+    int held_lines[STAGES];
+#pragma unroll
+    for (int st = 0; st < STAGES; ++st) held_lines[st] = 0;
+    auto drop = [&](int st) {
+      const char* base = held[st];
+      for (int l = lane; l < held_lines[st]; l += 32) discard_l2_line(base + (size_t)l * 128);
     };
-    for (int it = 0; it < n_it; ++it) {
-      const int st = it % STAGES;
-      if (it >= STAGES) {
-        mbar_wait(&empty[st], ((it / STAGES) - 1) & 1);
-        drop(it - STAGES);
-      }
-      if (lane == 0) {
+    uint32_t g = 0;  // global stage counter across items
+    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+      const int row = item / p.n_splits;
+      const int pos0 = (item - row * p.n_splits) * p.chunk;
+      const int npos = min(p.chunk, p.s - pos0);
+      const int n_it = (npos + kRows - 1) / kRows;
+      const T* kslot = static_cast<const T*>(p.k) + (size_t)row * p.max_seq * kH;
+      for (int it = 0; it < n_it; ++it, ++g) {
+        const int st = (int)(g % STAGES);
+        if (g >= (uint32_t)STAGES) {
+          mbar_wait(&empty[st], ((g / STAGES) - 1) & 1);
+          drop(st);
+        }
+        const int pstart = pos0 + it * kRows;
         const int rows = min(kRows, npos - it * kRows);
-        const uint32_t bytes = (uint32_t)(rows * ROWB);
-        mbar_arrive_expect_tx(&full[st], bytes);
-        tma_bulk_g2s(ring + st * kRows * ROWB, kslot + (size_t)(pos0 + it * kRows) * kH, bytes,
-                     &full[st], pol);
+        held[st] = reinterpret_cast<const char*>(kslot + (size_t)pstart * kH);
+        held_lines[st] = max(0, min(pstart + rows, p.discard_len) - pstart) * (ROWB / 128);
+        if (lane == 0) {
+          const uint32_t bytes = (uint32_t)(rows * ROWB);
+          mbar_arrive_expect_tx(&full[st], bytes);
+          tma_bulk_g2s(ring + st * kRows * ROWB, kslot + (size_t)pstart * kH, bytes, &full[st], pol);
+        }
+        __syncwarp();
       }
-      __syncwarp();
     }
-    for (int it = max(0, n_it - STAGES); it < n_it; ++it) {
-      mbar_wait(&empty[it % STAGES], (it / STAGES) & 1);
-      drop(it);
+    // drain: the last STAGES stages
+    const uint32_t first = g > (uint32_t)STAGES ? g - STAGES : 0;
+    for (uint32_t x = first; x < g; ++x) {
+      const int st = (int)(x % STAGES);
+      mbar_wait(&empty[st], (x / STAGES) & 1);
+      drop(st);
     }
     return;
   }
@@ -119,82 +131,93 @@ __global__ void __launch_bounds__((kCWarps + 1) * 32)
   const int sub = lane % LPR;
   const int rl = lane / LPR;
   const int n_q = p.n_kv * G;
-  float qf[G][CPL][8];
+  uint32_t g = 0;
+  for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+    const int row = item / p.n_splits;
+    const int split = item - row * p.n_splits;
+    const int b = row / p.n_kv;
+    const int kvh = row - b * p.n_kv;
+    const int pos0 = split * p.chunk;
+    const int npos = min(p.chunk, p.s - pos0);
+    const int n_it = (npos + kRows - 1) / kRows;
+    float qf[G][CPL][8];
 #pragma unroll
-  for (int g = 0; g < G; ++g) {
-    const float* qh = p.q + ((size_t)b * n_q + kvh * G + g) * kH;
-#pragma unroll
-    for (int ci = 0; ci < CPL; ++ci) {
-      const int c = chunk_of<LPR>(ci, rl, sub);
-      const float4 a = *reinterpret_cast<const float4*>(qh + c * 8);
-      const float4 bq = *reinterpret_cast<const float4*>(qh + c * 8 + 4);
-      qf[g][ci][0] = a.x; qf[g][ci][1] = a.y; qf[g][ci][2] = a.z; qf[g][ci][3] = a.w;
-      qf[g][ci][4] = bq.x; qf[g][ci][5] = bq.y; qf[g][ci][6] = bq.z; qf[g][ci][7] = bq.w;
-    }
-  }
-  float m_run = -INFINITY, l_run = 0.0f;
-  float* lrow = p.logits + ((size_t)b * n_q + kvh * G + (sub < G ? sub : 0)) * p.lstride + pos0;
-
-  for (int it = 0; it < n_it; ++it) {
-    const int st = it % STAGES;
-    mbar_wait(&full[st], (it / STAGES) & 1);
-    const uint8_t* sb = ring + st * kRows * ROWB;
-#pragma unroll
-    for (int pass = 0; pass < PASSES; ++pass) {
-      const int r = warp * (kRows / kCWarps) + pass * RPP + rl;
-      const int pl = it * kRows + r;
-      const uint4* srow = reinterpret_cast<const uint4*>(sb + r * ROWB);
-      float acc[G];
-#pragma unroll
-      for (int g = 0; g < G; ++g) acc[g] = 0.0f;
+    for (int gh = 0; gh < G; ++gh) {
+      const float* qh = p.q + ((size_t)b * n_q + kvh * G + gh) * kH;
 #pragma unroll
       for (int ci = 0; ci < CPL; ++ci) {
-        const uint4 raw = srow[chunk_of<LPR>(ci, rl, sub)];
-        float kf[8];
-        unpack8<T>(raw, kf);
-#pragma unroll
-        for (int g = 0; g < G; ++g) {
-#pragma unroll
-          for (int e = 0; e < 8; ++e) acc[g] = fmaf(qf[g][ci][e], kf[e], acc[g]);
-        }
-      }
-#pragma unroll
-      for (int o = LPR / 2; o >= 1; o >>= 1) {
-#pragma unroll
-        for (int g = 0; g < G; ++g) acc[g] += __shfl_xor_sync(0xffffffffu, acc[g], o);
-      }
-      float mine = acc[0];
-#pragma unroll
-      for (int g = 1; g < G; ++g) mine = (sub == g) ? acc[g] : mine;
-      const float sc = mine * p.scale;
-      if (pl < npos && sub < G) {
-        lrow[pl] = sc;
-        if (sc > m_run) {
-          l_run = l_run * expf(m_run - sc) + 1.0f;
-          m_run = sc;
-        } else {
-          l_run += expf(sc - m_run);
-        }
+        const int c = chunk_of<LPR>(ci, rl, sub);
+        const float4 a = *reinterpret_cast<const float4*>(qh + c * 8);
+        const float4 bq = *reinterpret_cast<const float4*>(qh + c * 8 + 4);
+        qf[gh][ci][0] = a.x; qf[gh][ci][1] = a.y; qf[gh][ci][2] = a.z; qf[gh][ci][3] = a.w;
+        qf[gh][ci][4] = bq.x; qf[gh][ci][5] = bq.y; qf[gh][ci][6] = bq.z; qf[gh][ci][7] = bq.w;
       }
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[st]);
-  }
+    float m_run = -INFINITY, l_run = 0.0f;
+    float* lrow = p.logits + ((size_t)b * n_q + kvh * G + (sub < G ? sub : 0)) * p.lstride + pos0;
 
-  // per-split (max, sum exp) per q head: lanes with equal `sub`, then warps
+    for (int it = 0; it < n_it; ++it, ++g) {
+      const int st = (int)(g % STAGES);
+      mbar_wait(&full[st], (g / STAGES) & 1);
+      const uint8_t* sb = ring + st * kRows * ROWB;
 #pragma unroll
-  for (int o = LPR; o < 32; o <<= 1) {
-    const float m2 = __shfl_xor_sync(0xffffffffu, m_run, o);
-    const float l2 = __shfl_xor_sync(0xffffffffu, l_run, o);
-    ml_combine(m_run, l_run, m2, l2);
-  }
-  if (lane < G) red[warp * G + lane] = make_float2(m_run, l_run);
-  named_sync(1, kCWarps * 32);
-  if (threadIdx.x < G) {
-    const int g = threadIdx.x;
-    float m = -INFINITY, l = 0.0f;
-    for (int w = 0; w < kCWarps; ++w) ml_combine(m, l, red[w * G + g].x, red[w * G + g].y);
-    p.partials[((size_t)b * n_q + kvh * G + g) * p.max_splits + split] = make_float2(m, l);
+      for (int pass = 0; pass < PASSES; ++pass) {
+        const int r = warp * (kRows / kCWarps) + pass * RPP + rl;
+        const int pl = it * kRows + r;
+        const uint4* srow = reinterpret_cast<const uint4*>(sb + r * ROWB);
+        float acc[G];
+#pragma unroll
+        for (int gh = 0; gh < G; ++gh) acc[gh] = 0.0f;
+#pragma unroll
+        for (int ci = 0; ci < CPL; ++ci) {
+          const uint4 raw = srow[chunk_of<LPR>(ci, rl, sub)];
+          float kf[8];
+          unpack8<T>(raw, kf);
+#pragma unroll
+          for (int gh = 0; gh < G; ++gh) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) acc[gh] = fmaf(qf[gh][ci][e], kf[e], acc[gh]);
+          }
+        }
+#pragma unroll
+        for (int o = LPR / 2; o >= 1; o >>= 1) {
+#pragma unroll
+          for (int gh = 0; gh < G; ++gh) acc[gh] += __shfl_xor_sync(0xffffffffu, acc[gh], o);
+        }
+        float mine = acc[0];
+#pragma unroll
+        for (int gh = 1; gh < G; ++gh) mine = (sub == gh) ? acc[gh] : mine;
+        const float sc = mine * p.scale;
+        if (pl < npos && sub < G) {
+          lrow[pl] = sc;
+          if (sc > m_run) {
+            l_run = l_run * expf(m_run - sc) + 1.0f;
+            m_run = sc;
+          } else {
+            l_run += expf(sc - m_run);
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+    }
+
+    // per-split (max, sum exp) per q head: lanes with equal `sub`, then warps
+#pragma unroll
+    for (int o = LPR; o < 32; o <<= 1) {
+      const float m2 = __shfl_xor_sync(0xffffffffu, m_run, o);
+      const float l2 = __shfl_xor_sync(0xffffffffu, l_run, o);
+      ml_combine(m_run, l_run, m2, l2);
+    }
+    if (lane < G) red[warp * G + lane] = make_float2(m_run, l_run);
+    named_sync(1, kCWarps * 32);
+    if (threadIdx.x < G) {
+      const int gh = threadIdx.x;
+      float m = -INFINITY, l = 0.0f;
+      for (int w = 0; w < kCWarps; ++w) ml_combine(m, l, red[w * G + gh].x, red[w * G + gh].y);
+      p.partials[((size_t)b * n_q + kvh * G + gh) * p.max_splits + split] = make_float2(m, l);
+    }
+    named_sync(1, kCWarps * 32);  // red is reused by the next item
   }
 }
 
@@ -238,6 +261,14 @@ __global__ void __launch_bounds__(256) score_generic_kernel(const ScoreParams p)
   }
 }
 
+int num_sms() {
+  static int n[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!n[dev & 63]) cudaDeviceGetAttribute(&n[dev & 63], cudaDevAttrMultiProcessorCount, dev);
+  return n[dev & 63] > 0 ? n[dev & 63] : 148;
+}
+
 template <typename T, int G, int LPR, int STAGES>
 void launch_fast_s(const ScoreParams& p, cudaStream_t st) {
   constexpr int ROWB = kH * (int)sizeof(T);
@@ -251,7 +282,9 @@ void launch_fast_s(const ScoreParams& p, cudaStream_t st) {
                          (int)smem);
     configured |= 1ull << (dev & 63);
   }
-  dim3 grid(p.n_splits, p.rows);
+  const int n_items = p.rows * p.n_splits;
+  const int per_sm = p.ctas_per_sm > 0 ? p.ctas_per_sm : 1 << 20;  // 0: one CTA per item
+  const int grid = (int)std::min<long long>(n_items, (long long)per_sm * num_sms());
   score_fast_kernel<T, G, LPR, STAGES><<<grid, (kCWarps + 1) * 32, smem, st>>>(p);
 }
 
@@ -292,9 +325,10 @@ void l2_flush_launch(const void* scratch, size_t bytes, cudaStream_t st) {
 
 int score_pick_chunk(int s, int rows, int override_chunk) {
   if (override_chunk > 0) return ((override_chunk + kRows - 1) / kRows) * kRows;
-  // ~6 resident CTAs per SM x 148 SMs per wave; chunks of 256..2048 positions.
+  // enough items for a balanced persistent grid (~24+ per CTA at 2 CTAs/SM),
+  // 256..2048 positions each
   const long long work = (long long)s * rows;
-  long long c = (work + 148LL * 6 - 1) / (148LL * 6);
+  long long c = (work + 148LL * 48 - 1) / (148LL * 48);
   c = std::max<long long>(256, std::min<long long>(2048, c));
   c = ((c + kRows - 1) / kRows) * kRows;
   return (int)c;
