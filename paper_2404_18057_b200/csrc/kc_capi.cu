@@ -119,11 +119,13 @@ struct LayerState {
 constexpr int kRing = 3;
 
 // V recall strategies for offloaded layers (kc_set_tuning "recall_mode"):
-// zero-copy SM loads of the selected rows from the mapped host arena (the
-// default: with consumed K lines dropped from L2 it reaches ~40 GB/s and hides
-// under the next layer's scoring), or host-side compaction + one DMA per
-// layer (kc_gather.hpp; bounded by host memory latency on this box).
-constexpr int kRecallAuto = 0, kRecallZeroCopy = 1, kRecallDma = 2;
+// zero-copy SM loads of the selected rows from the mapped host arena (bounded
+// by the GPU's page walks for the scattered 4-KB host pages),
+// host-side compaction + one DMA per layer (kc_gather.hpp; bounded by host
+// memory latency and cores), or both at once on disjoint row ranges: the
+// first host_frac of the (batch, kv head) rows are gathered by host threads
+// and DMA'd, the rest are pulled zero-copy, so the two independent limits add.
+constexpr int kRecallAuto = 0, kRecallZeroCopy = 1, kRecallDma = 2, kRecallHybrid = 3;
 
 bool host_pinned(const void* p) {
   cudaPointerAttributes a{};
@@ -163,6 +165,7 @@ struct kc_cache {
   int64_t lstride = 0, kstride = 0;
   int max_splits = 0;
   DevBuf logits, partials, keys, part_out, stage_src, stage_k, stage_v, sel_rows, sel_pos, gather_out;
+  DevBuf cand, cand_meta, fb_flags;  // candidate-mode selection scratch
   DevBuf q32[kRing], idx[kRing], w[kRing], dropped[kRing], norm[kRing], out_tmp[kRing], idx_exp[kRing];
   PinnedBuf host_in, host_out;
   // DMA recall: pinned copy of the selection, pinned compacted rows, HBM copy
@@ -184,8 +187,16 @@ struct kc_cache {
   // the default: with the recall kernel co-running, the hardware block
   // scheduler's dynamic balancing beats a static persistent split (measured)
   int score_ctas_per_sm = 0;
+  int host_frac_pct = 50;  // hybrid recall: % of rows gathered by host threads
+  int auto_recall_mode = kRecallZeroCopy;  // what recall_mode 0 resolves to
+  int score_groups = 1;
+  int k_policy = 0;        // L2 policy of the K stream (kc_device.cuh l2_policy)
+  int select_cand = 0;     // MHA: per-split candidates instead of dense logits
+  int cand_force_fallback = 0;  // test hook: every candidate-mode row takes the dense redo
+  int debug_skip = 0;      // diagnostic only: bit 0 skips scoring, bit 1 skips selection (stale outputs)   // row groups per layer (score -> select -> recall each)
+  int l2_cleanse_mb = 0;  // diagnostic: read+discard sweep before each recall
   int recall_ctas = 64;  // CTAs of the recall kernel (0: one per (batch, kv head))
-  int gather_threads = 0;  // 0: min(8, cores/2)
+  int gather_threads = 0;  // 0: 3/4 of the host cores
 
   // per-kernel CUDA-event timing (kc_profile): [kind] -> (start, stop) pairs
   bool prof_on = false;
@@ -305,7 +316,8 @@ void destroy(kc_cache* c) {
     munmap(c->v_host, c->v_host_bytes);
   }
   for (DevBuf* b : {&c->logits, &c->partials, &c->keys, &c->part_out, &c->stage_src, &c->stage_k,
-                    &c->stage_v, &c->sel_rows, &c->sel_pos, &c->gather_out})
+                    &c->stage_v, &c->sel_rows, &c->sel_pos, &c->gather_out, &c->cand, &c->cand_meta,
+                    &c->fb_flags})
     b->release();
   for (int i = 0; i < kRing; ++i) {
     c->q32[i].release(); c->idx[i].release(); c->w[i].release(); c->dropped[i].release();
@@ -397,15 +409,8 @@ StepGeom geom(kc_cache* c, uint64_t top_n) {
 // K becomes clean and the scoring kernel may drop its lines after use. Done
 // at the first decode after appends, then whenever the not-yet-clean tail of
 // a layer exceeds ~8 MB; positions appended since stay un-dropped.
-void maybe_flush_l2(kc_cache* c, const uint64_t* layers, uint64_t n, cudaStream_t st) {
-  const uint64_t pos_bytes = c->rows * c->h * c->esz;
-  const uint64_t slack = (8ull << 20) / std::max<uint64_t>(pos_bytes, 1);
-  bool need = false;
-  for (uint64_t i = 0; i < n; ++i) {
-    const LayerState& ls = c->layers[layers[i]];
-    if (ls.len > ls.clean_len && (ls.clean_len == 0 || ls.len - ls.clean_len > slack)) need = true;
-  }
-  if (!need) return;
+// per-device scratch of 2.5x L2 for the flush / cleanse sweeps
+std::pair<void*, size_t> l2_scratch(kc_cache* c, cudaStream_t st) {
   static std::mutex mu;
   static std::vector<std::pair<void*, size_t>> bufs(64, {nullptr, 0});
   std::lock_guard<std::mutex> lk(mu);
@@ -417,12 +422,32 @@ void maybe_flush_l2(kc_cache* c, const uint64_t* layers, uint64_t n, cudaStream_
     CK(cudaMalloc(&buf.first, buf.second));
     CK(cudaMemsetAsync(buf.first, 0, buf.second, st));
   }
+  return buf;
+}
+
+void maybe_flush_l2(kc_cache* c, const uint64_t* layers, uint64_t n, cudaStream_t st) {
+  const uint64_t pos_bytes = c->rows * c->h * c->esz;
+  const uint64_t slack = (8ull << 20) / std::max<uint64_t>(pos_bytes, 1);
+  bool need = false;
+  for (uint64_t i = 0; i < n; ++i) {
+    const LayerState& ls = c->layers[layers[i]];
+    if (ls.len > ls.clean_len && (ls.clean_len == 0 || ls.len - ls.clean_len > slack)) need = true;
+  }
+  if (!need) return;
+  const auto buf = l2_scratch(c, st);
   kc::l2_flush_launch(buf.first, buf.second, st);
   for (auto& ls : c->layers) ls.clean_len = ls.len;
 }
 
-void enqueue_score(kc_cache* c, uint64_t layer, const float* q32, const StepGeom& g, cudaStream_t st) {
+void enqueue_score(kc_cache* c, uint64_t layer, const float* q32, const StepGeom& g, cudaStream_t st,
+                   int row0, int nrows, bool cand = false) {
   kc::ScoreParams sp{};
+  sp.row0 = row0;
+  if (cand) {
+    sp.cand = c->cand.as<uint2>();
+    sp.cand_meta = c->cand_meta.as<uint2>();
+    sp.cand_nc = g.nc;
+  }
   sp.k = c->k_layer(layer);
   sp.q = q32;
   sp.logits = c->logits.as<float>();
@@ -433,7 +458,7 @@ void enqueue_score(kc_cache* c, uint64_t layer, const float* q32, const StepGeom
   sp.h = (int)c->h;
   sp.n_kv = (int)c->n_kv;
   sp.G = (int)c->G;
-  sp.rows = (int)c->rows;
+  sp.rows = nrows;
   sp.chunk = g.chunk;
   sp.n_splits = g.n_splits;
   sp.max_splits = c->max_splits;
@@ -442,6 +467,7 @@ void enqueue_score(kc_cache* c, uint64_t layer, const float* q32, const StepGeom
   if (!c->discard) sp.discard_len = 0;
   sp.stages = c->score_stages;
   sp.ctas_per_sm = c->score_ctas_per_sm;
+  sp.k_policy = c->k_policy;
   c->timed(0, st, [&] { kc::score_launch(sp, c->dtype, st); });
 }
 
@@ -509,88 +535,152 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
     const int slot = (int)(i % kRing);
     const uint64_t layer = layers[i];
     const float* q32 = stage_q(c, slot, q[i], q_dtype, io_device, st, i, n);
-    enqueue_score(c, layer, q32, g, st);
-    if (i >= (uint64_t)kRing && side != st) CK(cudaStreamWaitEvent(st, c->ev_rec[slot], 0));
-
-    kc::SelectParams sp{};
-    sp.logits = c->logits.as<float>();
-    sp.partials = c->partials.as<float2>();
-    sp.keys = c->keys.as<uint32_t>();
-    sp.idx = c->idx[slot].as<uint32_t>();
-    sp.w = c->w[slot].as<float>();
-    sp.dropped = c->dropped[slot].as<double>();
-    sp.norm = c->norm[slot].as<float>();
-    sp.lstride = c->lstride;
-    sp.kstride = c->kstride;
-    sp.s = g.s;
-    sp.nc = g.nc;
-    sp.n_kv = (int)c->n_kv;
-    sp.G = (int)c->G;
-    sp.n_splits = g.n_splits;
-    sp.max_splits = c->max_splits;
-    sp.rows = (int)c->rows;
-    sp.force_global = c->select_global;
-    c->timed(1, st, [&] { kc::select_launch(sp, st); });
-    CK(cudaEventRecord(c->ev_sel[slot], st));
-    if (side != st) CK(cudaStreamWaitEvent(side, c->ev_sel[slot], 0));
-
     kc_topn_out& o = outs[i];
-    kc::RecallParams rp{};
-    rp.v = c->v_layer(layer);
-    // Offloaded layer: compact the selected rows on the host (pool threads,
-    // stream-ordered via cudaLaunchHostFunc on gather_st), then one DMA.
-    const bool dma = layer >= c->L && c->recall_mode == kRecallDma;
-    const size_t stage_bytes = c->rows * nc * c->h * c->esz;
-    if (dma) {
-      c->idx_host[slot].ensure(c->rows * nc * 4);
-      c->stage_host[slot].ensure(stage_bytes);
-      c->stage_dev[slot].ensure(stage_bytes);
-      if (!c->pool) {
-        int t = c->gather_threads;
-        if (t <= 0) t = std::max(1, std::min(8, (int)std::thread::hardware_concurrency() / 2));
-        c->pool = std::make_unique<kc::GatherPool>(t - 1);
-      }
-      CK(cudaStreamWaitEvent(c->gather_st, c->ev_sel[slot], 0));
-      CK(cudaMemcpyAsync(c->idx_host[slot].p, c->idx[slot].p, c->rows * nc * 4, cudaMemcpyDeviceToHost,
-                         c->gather_st));
-      auto* job = new kc::GatherJob{c->pool.get(),
-                                    (const char*)c->v_host + (layer - c->L) * c->v_layer_bytes,
-                                    c->cfg.max_seq * c->h * c->esz,
-                                    c->h * c->esz,
-                                    static_cast<const uint32_t*>(c->idx_host[slot].p),
-                                    c->rows,
-                                    nc,
-                                    static_cast<char*>(c->stage_host[slot].p)};
-      cudaError_t he = cudaLaunchHostFunc(c->gather_st, kc::gather_host_fn, job);
-      if (he != cudaSuccess) {
-        delete job;
-        CK(he);
-      }
-      CK(cudaEventRecord(c->ev_gath[slot], c->gather_st));
-      CK(cudaStreamWaitEvent(side, c->ev_gath[slot], 0));
-      rp.v = c->stage_dev[slot].p;
+    // Offloaded layer in DMA mode: compact the selected rows on the host (pool
+    // threads, stream-ordered via cudaLaunchHostFunc on gather_st), then one DMA.
+    const bool offl = layer >= c->L;
+    const int mode = c->recall_mode == kRecallAuto ? c->auto_recall_mode : c->recall_mode;
+    // rows [0, host_rows) are host-gathered + DMA'd, [host_rows, rows) zero-copy
+    const int host_rows = !offl ? 0
+                          : mode == kRecallDma ? (int)c->rows
+                          : mode == kRecallHybrid ? (int)std::min<int64_t>((int64_t)c->rows, ((int64_t)c->rows * c->host_frac_pct + 50) / 100)
+                          : 0;
+    const bool dma = host_rows > 0;
+    // Row groups: score -> select -> recall per group of (batch, kv head)
+    // rows, so only one group's fp32 logits are live in L2 at a time (the L2
+    // keeps the GPU page-table lines the zero-copy recall walks).
+    const int n_groups = dma ? 1 : (int)std::max<int64_t>(1, std::min<int64_t>(c->score_groups, (int64_t)c->rows));
+    // Candidate mode (MHA): scoring emits only each split's possible top-N
+    // positions instead of 4 B of fp32 logit per position -- the dense logits
+    // (32 MiB per C2 layer) would evict the GPU page-table lines the zero-copy
+    // recall walks from L2.
+    const bool cand = c->select_cand && !c->select_global &&
+                      kc::score_cand_supported(c->dtype, (int)c->h, (int)c->G, g.chunk, g.nc);
+    if (cand) {
+      c->cand.ensure(checked_mul({c->rows, (uint64_t)c->lstride, 8}));
+      c->cand_meta.ensure(checked_mul({c->rows, (uint64_t)c->max_splits, 8}));
+      c->fb_flags.ensure(c->rows * 4);
     }
-    rp.staged = dma ? 1 : 0;
-    rp.grid = c->recall_ctas;
-    rp.idx = c->idx[slot].as<uint32_t>();
-    rp.w = c->w[slot].as<float>();
-    rp.norm = c->norm[slot].as<float>();
-    rp.out = io_device ? o.out : c->out_tmp[slot].as<float>();
-    rp.max_seq = (int64_t)c->cfg.max_seq;
-    rp.nc = g.nc;
-    rp.h = (int)c->h;
-    rp.n_kv = (int)c->n_kv;
-    rp.G = (int)c->G;
-    rp.rows = (int)c->rows;
-    rp.renormalize = (flags & KC_RENORMALIZE) ? 1 : 0;
-    rp.reverse = (flags & KC_REVERSE_ACCUM) ? 1 : 0;
-    rp.row_offset = 0;
-    c->timed(2, side, [&] {
-      if (dma)
-        CK(cudaMemcpyAsync(c->stage_dev[slot].p, c->stage_host[slot].p, stage_bytes,
-                           cudaMemcpyHostToDevice, side));
-      kc::recall_launch(rp, c->dtype, side);
-    });
+    const int gsz = (int)((c->rows + n_groups - 1) / n_groups);
+    for (int gi = 0; gi < n_groups; ++gi) {
+      const int r0 = gi * gsz;
+      const int nr = std::min<int>(gsz, (int)c->rows - r0);
+      if (nr <= 0) break;
+      if (!(c->debug_skip & 1)) enqueue_score(c, layer, q32, g, st, r0, nr, cand);
+      if (gi == 0 && i >= (uint64_t)kRing && side != st) CK(cudaStreamWaitEvent(st, c->ev_rec[slot], 0));
+
+      kc::SelectParams sp{};
+      sp.logits = c->logits.as<float>();
+      sp.partials = c->partials.as<float2>();
+      sp.keys = c->keys.as<uint32_t>();
+      sp.idx = c->idx[slot].as<uint32_t>();
+      sp.w = c->w[slot].as<float>();
+      sp.dropped = c->dropped[slot].as<double>();
+      sp.norm = c->norm[slot].as<float>();
+      sp.lstride = c->lstride;
+      sp.kstride = c->kstride;
+      sp.s = g.s;
+      sp.nc = g.nc;
+      sp.n_kv = (int)c->n_kv;
+      sp.G = (int)c->G;
+      sp.n_splits = g.n_splits;
+      sp.max_splits = c->max_splits;
+      sp.row0 = r0;
+      sp.rows = nr;
+      sp.force_global = c->select_global;
+      if (cand) {
+        sp.cand = c->cand.as<uint2>();
+        sp.cand_meta = c->cand_meta.as<uint2>();
+        sp.fb_flags = c->fb_flags.as<uint32_t>();
+        sp.chunk = g.chunk;
+        sp.k = c->k_layer(layer);
+        sp.q = q32;
+        sp.max_seq = (int64_t)c->cfg.max_seq;
+        sp.h = (int)c->h;
+        sp.kdtype = c->dtype;
+        sp.scale = 1.0f / std::sqrt(static_cast<float>(c->h));  // attention.hpp:15-17
+        sp.force_fallback = c->cand_force_fallback;
+      }
+      if (!(c->debug_skip & 2))
+        c->timed(1, st, [&] {
+          if (!cand || !kc::select_cand_launch(sp, st)) {
+            sp.cand = nullptr;
+            sp.fb_flags = nullptr;
+            if (cand) fail(KC_ECUDA, "candidate selection unavailable for this shape");
+            kc::select_launch(sp, st);
+          }
+        });
+      CK(cudaEventRecord(c->ev_sel[slot], st));
+      if (side != st) CK(cudaStreamWaitEvent(side, c->ev_sel[slot], 0));
+
+      kc::RecallParams rp{};
+      rp.v = c->v_layer(layer);
+      const size_t stage_bytes = (size_t)host_rows * nc * c->h * c->esz;
+      if (dma) {
+        c->idx_host[slot].ensure((size_t)host_rows * nc * 4);
+        c->stage_host[slot].ensure(stage_bytes);
+        c->stage_dev[slot].ensure(stage_bytes);
+        if (!c->pool) {
+          int t = c->gather_threads;
+          if (t <= 0) t = std::max(1, (int)std::thread::hardware_concurrency() * 3 / 4);
+          c->pool = std::make_unique<kc::GatherPool>(t - 1);
+        }
+        CK(cudaStreamWaitEvent(c->gather_st, c->ev_sel[slot], 0));
+        CK(cudaMemcpyAsync(c->idx_host[slot].p, c->idx[slot].p, (size_t)host_rows * nc * 4, cudaMemcpyDeviceToHost,
+                           c->gather_st));
+        auto* job = new kc::GatherJob{c->pool.get(),
+                                      (const char*)c->v_host + (layer - c->L) * c->v_layer_bytes,
+                                      c->cfg.max_seq * c->h * c->esz,
+                                      c->h * c->esz,
+                                      static_cast<const uint32_t*>(c->idx_host[slot].p),
+                                      (uint64_t)host_rows,
+                                      nc,
+                                      static_cast<char*>(c->stage_host[slot].p)};
+        cudaError_t he = cudaLaunchHostFunc(c->gather_st, kc::gather_host_fn, job);
+        if (he != cudaSuccess) {
+          delete job;
+          CK(he);
+        }
+        CK(cudaEventRecord(c->ev_gath[slot], c->gather_st));
+      }
+      rp.staged = 0;
+      rp.grid = c->recall_ctas;
+      rp.idx = c->idx[slot].as<uint32_t>();
+      rp.w = c->w[slot].as<float>();
+      rp.norm = c->norm[slot].as<float>();
+      rp.out = io_device ? o.out : c->out_tmp[slot].as<float>();
+      rp.max_seq = (int64_t)c->cfg.max_seq;
+      rp.nc = g.nc;
+      rp.h = (int)c->h;
+      rp.n_kv = (int)c->n_kv;
+      rp.G = (int)c->G;
+      rp.rows = dma ? nr - host_rows : nr;
+      rp.renormalize = (flags & KC_RENORMALIZE) ? 1 : 0;
+      rp.reverse = (flags & KC_REVERSE_ACCUM) ? 1 : 0;
+      rp.row_offset = dma ? host_rows : r0;
+      rp.discard_len = c->discard && (c->h * c->esz) % 128 == 0 ? (int)std::min<uint64_t>(c->layers[layer].clean_len, (uint64_t)g.s) : 0;
+      if (c->l2_cleanse_mb > 0) {
+        const auto buf = l2_scratch(c, side);
+        kc::l2_cleanse_launch(buf.first, std::min<size_t>(buf.second, (size_t)c->l2_cleanse_mb << 20), side);
+      }
+      c->timed(2, side, [&] {
+        // zero-copy rows first (they need nothing but the selection), then the
+        // host-gathered rows once their DMA has landed
+        if (rp.rows > 0) kc::recall_launch(rp, c->dtype, side);
+        if (dma) {
+          CK(cudaStreamWaitEvent(side, c->ev_gath[slot], 0));
+          CK(cudaMemcpyAsync(c->stage_dev[slot].p, c->stage_host[slot].p, stage_bytes, cudaMemcpyHostToDevice,
+                             side));
+          kc::RecallParams hp = rp;
+          hp.v = c->stage_dev[slot].p;
+          hp.staged = 1;
+          hp.row_offset = 0;
+          hp.rows = host_rows;
+          hp.discard_len = 0;
+          kc::recall_launch(hp, c->dtype, side);
+        }
+      });
+    }
 
     const uint32_t* idx_slots = c->idx[slot].as<uint32_t>();
     if (c->G > 1 && (o.indices || !io_device)) {
@@ -819,7 +909,7 @@ int kc_decode_full(kc_cache* c, uint64_t layer, const void* q, int q_dtype, uint
     const StepGeom g = geom(c, 1);
     maybe_flush_l2(c, &layer, 1, st);
     const float* q32 = stage_q(c, 0, q, q_dtype, io_device, st);
-    enqueue_score(c, layer, q32, g, st);
+    enqueue_score(c, layer, q32, g, st, 0, (int)c->rows);
     const uint64_t slots = c->batch * c->n_q;
     c->part_out.ensure(checked_mul({slots, (uint64_t)g.n_splits, c->h, 4}));
     if (!io_device) c->out_tmp[0].ensure(slots * c->h * 4);
@@ -858,7 +948,7 @@ int kc_score_probs(kc_cache* c, uint64_t layer, const void* q, int q_dtype, floa
     const StepGeom g = geom(c, 1);
     maybe_flush_l2(c, &layer, 1, st);
     const float* q32 = stage_q(c, 0, q, q_dtype, false, st);
-    enqueue_score(c, layer, q32, g, st);
+    enqueue_score(c, layer, q32, g, st, 0, (int)c->rows);
     const uint64_t slots = c->batch * c->n_q;
     c->gather_out.ensure(checked_mul({slots, (uint64_t)g.s, 4}));
     kc::SelectParams sp{};
@@ -1002,8 +1092,20 @@ int kc_set_tuning(kc_cache* c, const char* key, int64_t value) {
     else if (k == "score_stages") c->score_stages = (int)value;
     else if (k == "score_ctas_per_sm") c->score_ctas_per_sm = (int)value;
     else if (k == "recall_ctas") c->recall_ctas = (int)value;
-    else if (k == "recall_mode") {
-      if (value < 0 || value > 2) fail(KC_EARG, "recall_mode: 0 auto, 1 zero-copy, 2 dma");
+    else if (k == "l2_cleanse_mb") c->l2_cleanse_mb = (int)value;
+    else if (k == "debug_skip") c->debug_skip = (int)value;
+    else if (k == "select_cand") c->select_cand = value ? 1 : 0;
+    else if (k == "k_policy") c->k_policy = (int)value;
+    else if (k == "cand_force_fallback") c->cand_force_fallback = value ? 1 : 0;
+    else if (k == "score_groups") {
+      if (value < 1) fail(KC_EARG, "score_groups must be >= 1");
+      c->score_groups = (int)value;
+    }
+    else if (k == "host_frac_pct") {
+      if (value < 0 || value > 100) fail(KC_EARG, "host_frac_pct: 0..100");
+      c->host_frac_pct = (int)value;
+    } else if (k == "recall_mode") {
+      if (value < 0 || value > 3) fail(KC_EARG, "recall_mode: 0 auto, 1 zero-copy, 2 dma, 3 hybrid");
       c->recall_mode = (int)value;
     } else if (k == "gather_threads") {
       if (c->main_st) cudaStreamSynchronize(c->main_st);

@@ -139,6 +139,19 @@ __device__ __forceinline__ uint64_t l2_evict_first_policy() {
   return pol;
 }
 
+// Other L2 policies for the K stream (tuning experiments).
+__device__ __forceinline__ uint64_t l2_policy(int kind) {
+  uint64_t pol;
+  switch (kind) {
+    case 1: asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol)); break;
+    case 2: asm volatile("createpolicy.fractional.L2::evict_unchanged.b64 %0, 1.0;" : "=l"(pol)); break;
+    case 3: asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol)); break;
+    case 4: asm volatile("createpolicy.fractional.L2::evict_first.L2::evict_unchanged.b64 %0, 0.5;" : "=l"(pol)); break;
+    default: asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol)); break;
+  }
+  return pol;
+}
+
 // 1-D TMA bulk copy global -> shared, completion signalled on `bar` as
 // transaction bytes (SASS: UBLKCP). bytes % 16 == 0, both addresses 16-B aligned.
 __device__ __forceinline__ void tma_bulk_g2s(void* dst_smem, const void* src_gmem, uint32_t bytes,

@@ -31,14 +31,27 @@ struct ScoreParams {
   int discard_len;      // K positions < discard_len are clean: drop their L2 lines after use
   int stages;           // TMA ring depth (4, 6 or 8 stages of 64 positions)
   int ctas_per_sm;      // persistent grid = ctas_per_sm x SMs (0: one CTA per item)
+  int row0;             // first row of this launch (row groups); rows = rows in this launch
+  // candidate mode (MHA, h=128 16-bit fast path, cand_nc > 0): instead of the
+  // dense logits, every split writes the positions that can still be in the
+  // row's top-cand_nc -- a provable superset, see kc_score.cu -- as (score
+  // bits, position) pairs at cand[row][pos0..], plus {count, exclusion bound}
+  // at cand_meta[row][split]. Positions with score < bound were dropped.
+  uint2* cand;          // [rows][lstride]
+  uint2* cand_meta;     // [rows][max_splits]
+  int cand_nc;          // 0: dense logits
+  int k_policy;         // L2 policy of the K stream (0 evict_first; see l2_policy)
 };
 // Read `bytes` of a scratch buffer larger than L2: evicts (and so writes back)
 // every dirty L2 line, after which all stored K is clean in DRAM.
 void l2_flush_launch(const void* scratch, size_t bytes, cudaStream_t st);
+void l2_cleanse_launch(const void* scratch, size_t bytes, cudaStream_t st);
 // dtype: KC_F32 / KC_F16 / KC_BF16 (storage)
 void score_launch(const ScoreParams& p, int dtype, cudaStream_t st);
 // positions per CTA for a given shape (tuning override when > 0)
 int score_pick_chunk(int s, int rows, int override_chunk);
+// whether the candidate-mode scoring kernel covers this shape
+bool score_cand_supported(int dtype, int h, int G, int chunk, int nc);
 
 struct SelectParams {
   const float* logits;    // [batch][n_q][lstride]
@@ -58,8 +71,27 @@ struct SelectParams {
   int max_splits;
   int rows;
   int force_global;       // 1: the global-memory-keys kernel even when s fits registers
+  int row0;               // first row of this launch (row groups); rows = rows in this launch
+  // candidate mode (ScoreParams::cand_nc): select from the scoring kernel's
+  // per-split candidates; rows whose candidate set cannot be proven complete
+  // are flagged in fb_flags and redone densely by select_fallback_launch,
+  // which recomputes the row's scores bit-identically from q and K.
+  const uint2* cand;      // [rows][lstride]
+  const uint2* cand_meta; // [rows][max_splits] {count, bound bits}
+  uint32_t* fb_flags;     // [rows]
+  int chunk;              // scoring split length (candidate slots start at split*chunk)
+  const void* k;          // layer's K [rows][max_seq][h] (fallback recompute)
+  const float* q;         // [batch][n_q][h] fp32
+  int64_t max_seq;
+  int h;
+  int kdtype;             // KC_F16 / KC_BF16
+  float scale;
+  int force_fallback;     // test hook: flag every row for the dense redo
 };
 void select_launch(const SelectParams& p, cudaStream_t st);
+// candidate-mode selection (MHA, fast scoring path) + the dense redo of any
+// row it flags; returns false when the shape is outside candidate mode
+bool select_cand_launch(const SelectParams& p, cudaStream_t st);
 
 // p = exp(s - M)/Z for every position of every (batch, q head) -> probs
 // [batch*n_q][s] (ScoreObserver debug path).
@@ -86,6 +118,7 @@ struct RecallParams {
   int row_offset;         // first row of this launch (pipelined chunks)
   int staged;             // v is the compacted [rows][nc][h] block (DMA recall)
   int grid;               // CTAs (0: one per row); CTAs loop over rows
+  int discard_len;        // positions < discard_len are clean: drop their lines from L2 after use
 };
 void recall_launch(const RecallParams& p, int dtype, cudaStream_t st);
 

@@ -72,7 +72,16 @@ __global__ void __launch_bounds__(kRecallThreads) recall_pv_kernel(const RecallP
 #pragma unroll
         for (int u = 0; u < kBatch; ++u) {
           const int v = v0 + u * kRecallThreads;
-          if (v < total) dst[v] = tmp[u];
+          if (v < total) {
+            dst[v] = tmp[u];
+            // the row's 128-B line has landed: drop it from L2 (sysmem lines
+            // left in L2 slow every later zero-copy gather)
+            const int r = v / vpr, part = v - r * vpr;
+            if (!p.staged && (part & 7) == 0) {
+              const uint32_t pos = idx[c0 + r];
+              if ((int)pos < p.discard_len) discard_l2_line(reinterpret_cast<const uint4*>(vslot + (size_t)pos * h) + part);
+            }
+          }
         }
       }
     } else {

@@ -22,6 +22,8 @@
 // After a stage is consumed the producer warp drops its K lines from L2 (see
 // DESIGN.md section 5).
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 
 #include "kc_device.cuh"
 #include "kc_kernels.cuh"
@@ -34,6 +36,7 @@ namespace {
 constexpr int kRows = 64;     // positions per pipeline stage
 constexpr int kCWarps = 8;    // consumer warps
 constexpr int kH = 128;       // head_dim of the fast path
+constexpr int kMaxCandChunk = 2048;  // candidate mode: positions per split held in smem
 
 __device__ __forceinline__ void named_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
@@ -48,7 +51,63 @@ __device__ __forceinline__ int chunk_of(int ci, int rl, int sub) {
   }
 }
 
-template <typename T, int G, int LPR, int STAGES>
+// Candidate epilogue of one split (MHA): scb[0..npos) holds the split's
+// scores. tau = the nc-th largest of the 256 consumer threads' block maxima is
+// a lower bound of the split's nc-th largest score (nc threads each hold a
+// score >= tau), so every position below tau has >= nc positions of this
+// split strictly above it in p (p = exp(s - M)/Z is monotone in s) and can
+// never be selected -- except through a p-tie, which needs |s - tau| within a
+// few ulps: the bound keeps a window of 2^-9 (1 + |tau| + |max|) below tau.
+// The selection kernel re-checks that window against the row's actual N-th
+// score and recomputes the row densely if it is ever too narrow.
+__device__ __forceinline__ void emit_candidates(const float* scb, float* mx, uint32_t* wcnt, int npos,
+                                                int nc, int pos0, uint2* cand, uint2* meta) {
+  const int ct = threadIdx.x;  // 0..255 (consumer warps)
+  const int lane = ct & 31, warp = ct >> 5;
+  float bound = -INFINITY;
+  if (npos > nc) {
+    const int ppt = (npos + kCWarps * 32 - 1) / (kCWarps * 32);
+    const int a = ct * ppt, e = min(npos, a + ppt);
+    float m = -INFINITY;
+    for (int j = a; j < e; ++j) m = fmaxf(m, scb[j]);
+    mx[ct] = m;
+    named_sync(1, kCWarps * 32);
+    int r = 0;
+    float smax = -INFINITY;
+    for (int u = 0; u < kCWarps * 32; ++u) {
+      const float v = mx[u];
+      r += (v > m || (v == m && u < ct)) ? 1 : 0;
+      smax = fmaxf(smax, v);
+    }
+    named_sync(1, kCWarps * 32);  // every rank is computed before mx[0] is reused
+    if (r == nc - 1) mx[0] = m;   // ranks are a permutation: exactly one writer
+    named_sync(1, kCWarps * 32);
+    const float tau = mx[0];
+    if (tau > -INFINITY) bound = tau - 0x1p-9f * (1.0f + fabsf(tau) + fabsf(smax));
+  }
+  uint32_t run = 0;
+  for (int base = 0; base < npos; base += kCWarps * 32) {
+    const int j = base + ct;
+    const float v = j < npos ? scb[j] : 0.0f;
+    const bool keep = j < npos && v >= bound;
+    const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+    if (lane == 0) wcnt[warp] = __popc(bal);
+    named_sync(1, kCWarps * 32);
+    uint32_t off = run, tot = 0;
+#pragma unroll
+    for (int w = 0; w < kCWarps; ++w) {
+      const uint32_t c = wcnt[w];
+      off += (w < warp) ? c : 0u;
+      tot += c;
+    }
+    if (keep) cand[off + __popc(bal & lanemask_lt())] = make_uint2(__float_as_uint(v), (uint32_t)(pos0 + j));
+    run += tot;
+    named_sync(1, kCWarps * 32);  // wcnt is rewritten by the next block
+  }
+  if (ct == 0) *meta = make_uint2(run, __float_as_uint(bound));
+}
+
+template <typename T, int G, int LPR, int STAGES, bool CAND>
 __global__ void __launch_bounds__((kCWarps + 1) * 32)
     score_fast_kernel(const ScoreParams p) {
   constexpr int CPL = 16 / LPR;            // 16-B chunks per lane per row
@@ -62,6 +121,11 @@ __global__ void __launch_bounds__((kCWarps + 1) * 32)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * kRows * ROWB);
   uint64_t* empty = full + STAGES;
   float2* red = reinterpret_cast<float2*>(empty + STAGES);  // [kCWarps][G]
+  // candidate mode: the split's scores, block maxima, warp counts
+  float* scb = reinterpret_cast<float*>(red + kCWarps * G);  // [chunk]
+  float* mx = scb + (CAND ? p.chunk : 0);                     // [256]
+  uint32_t* wcnt = reinterpret_cast<uint32_t*>(mx + kCWarps * 32);
+  static_assert(!CAND || G == 1, "candidate mode ranks raw scores: MHA only");
 
   const int n_items = p.rows * p.n_splits;
   const int warp = threadIdx.x >> 5;
@@ -79,11 +143,12 @@ __global__ void __launch_bounds__((kCWarps + 1) * 32)
 
   if (warp == kCWarps) {
     // ---------------- producer warp: lane 0 streams K with TMA ----------------
-    // Once a stage has been consumed the warp drops that stage's K lines from
+    // Once a stage has landed in shared memory the warp drops its K lines from
     // L2 (discard.global.L2, positions < discard_len, which the store keeps
-    // clean): a decode step streams the whole K cache once, and an L2 left full
-    // of dead K lines makes the following zero-copy V recall ~1.5x slower.
-    const uint64_t pol = l2_evict_first_policy();
+    // clean): a decode step streams the whole K cache once, and L2 lines held
+    // by dead K evict the GPU page-table lines the zero-copy V recall walks
+    // (DESIGN.md section 5).
+    const uint64_t pol = l2_policy(p.k_policy);
     const char* held[STAGES];  // what each ring slot holds: start + line count
     int held_lines[STAGES];
 #pragma unroll
@@ -93,18 +158,23 @@ __global__ void __launch_bounds__((kCWarps + 1) * 32)
       for (int l = lane; l < held_lines[st]; l += 32) discard_l2_line(base + (size_t)l * 128);
     };
     uint32_t g = 0;  // global stage counter across items
+    // drop stage j's lines as soon as its bytes have landed in shared memory
+    // (the L2 copy is dead from then on); lag STAGES-1 behind the issue point
+    // so the ring stays full
+    auto land_and_drop = [&](uint32_t j) {
+      const int sj = (int)(j % STAGES);
+      mbar_wait(&full[sj], (j / STAGES) & 1);
+      drop(sj);
+    };
     for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-      const int row = item / p.n_splits;
-      const int pos0 = (item - row * p.n_splits) * p.chunk;
+      const int row = p.row0 + item / p.n_splits;
+      const int pos0 = (item - (row - p.row0) * p.n_splits) * p.chunk;
       const int npos = min(p.chunk, p.s - pos0);
       const int n_it = (npos + kRows - 1) / kRows;
       const T* kslot = static_cast<const T*>(p.k) + (size_t)row * p.max_seq * kH;
       for (int it = 0; it < n_it; ++it, ++g) {
         const int st = (int)(g % STAGES);
-        if (g >= (uint32_t)STAGES) {
-          mbar_wait(&empty[st], ((g / STAGES) - 1) & 1);
-          drop(st);
-        }
+        if (g >= (uint32_t)STAGES) mbar_wait(&empty[st], ((g / STAGES) - 1) & 1);
         const int pstart = pos0 + it * kRows;
         const int rows = min(kRows, npos - it * kRows);
         held[st] = reinterpret_cast<const char*>(kslot + (size_t)pstart * kH);
@@ -115,15 +185,11 @@ __global__ void __launch_bounds__((kCWarps + 1) * 32)
           tma_bulk_g2s(ring + st * kRows * ROWB, kslot + (size_t)pstart * kH, bytes, &full[st], pol);
         }
         __syncwarp();
+        if (g >= (uint32_t)(STAGES - 1)) land_and_drop(g - (STAGES - 1));
       }
     }
-    // drain: the last STAGES stages
-    const uint32_t first = g > (uint32_t)STAGES ? g - STAGES : 0;
-    for (uint32_t x = first; x < g; ++x) {
-      const int st = (int)(x % STAGES);
-      mbar_wait(&empty[st], (x / STAGES) & 1);
-      drop(st);
-    }
+    // drain: the last STAGES-1 stages
+    for (uint32_t j = g > (uint32_t)(STAGES - 1) ? g - (STAGES - 1) : 0; j < g; ++j) land_and_drop(j);
     return;
   }
 
@@ -133,8 +199,8 @@ __global__ void __launch_bounds__((kCWarps + 1) * 32)
   const int n_q = p.n_kv * G;
   uint32_t g = 0;
   for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-    const int row = item / p.n_splits;
-    const int split = item - row * p.n_splits;
+    const int row = p.row0 + item / p.n_splits;
+    const int split = item - (row - p.row0) * p.n_splits;
     const int b = row / p.n_kv;
     const int kvh = row - b * p.n_kv;
     const int pos0 = split * p.chunk;
@@ -189,7 +255,11 @@ __global__ void __launch_bounds__((kCWarps + 1) * 32)
         for (int gh = 1; gh < G; ++gh) mine = (sub == gh) ? acc[gh] : mine;
         const float sc = mine * p.scale;
         if (pl < npos && sub < G) {
-          lrow[pl] = sc;
+          if constexpr (CAND) {
+            scb[pl] = sc;
+          } else {
+            lrow[pl] = sc;
+          }
           if (sc > m_run) {
             l_run = l_run * expf(m_run - sc) + 1.0f;
             m_run = sc;
@@ -217,7 +287,10 @@ __global__ void __launch_bounds__((kCWarps + 1) * 32)
       for (int w = 0; w < kCWarps; ++w) ml_combine(m, l, red[w * G + gh].x, red[w * G + gh].y);
       p.partials[((size_t)b * n_q + kvh * G + gh) * p.max_splits + split] = make_float2(m, l);
     }
-    named_sync(1, kCWarps * 32);  // red is reused by the next item
+    if constexpr (CAND)
+      emit_candidates(scb, mx, wcnt, npos, p.cand_nc, pos0, p.cand + (size_t)row * p.lstride + pos0,
+                      p.cand_meta + (size_t)row * p.max_splits + split);
+    named_sync(1, kCWarps * 32);  // red / scb are reused by the next item
   }
 }
 
@@ -226,7 +299,7 @@ template <typename T>
 __global__ void __launch_bounds__(256) score_generic_kernel(const ScoreParams p) {
   extern __shared__ float2 wstat[];  // [8][G]
   const int split = blockIdx.x;
-  const int row = blockIdx.y;
+  const int row = p.row0 + blockIdx.y;
   const int b = row / p.n_kv;
   const int kvh = row - b * p.n_kv;
   const int G = p.G, h = p.h, n_q = p.n_kv * G;
@@ -269,42 +342,48 @@ int num_sms() {
   return n[dev & 63] > 0 ? n[dev & 63] : 148;
 }
 
-template <typename T, int G, int LPR, int STAGES>
+template <typename T, int G, int LPR, int STAGES, bool CAND>
 void launch_fast_s(const ScoreParams& p, cudaStream_t st) {
   constexpr int ROWB = kH * (int)sizeof(T);
   const size_t smem = STAGES * kRows * ROWB + 2 * STAGES * sizeof(uint64_t) +
-                      kCWarps * G * sizeof(float2);
+                      kCWarps * G * sizeof(float2) +
+                      (CAND ? (size_t)kMaxCandChunk * 4 + kCWarps * 32 * 4 + kCWarps * 4 : 0);
   static unsigned long long configured = 0;  // one bit per device
   int dev = 0;
   cudaGetDevice(&dev);
   if (!(configured >> (dev & 63) & 1ull)) {
-    cudaFuncSetAttribute(score_fast_kernel<T, G, LPR, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
+    cudaFuncSetAttribute(score_fast_kernel<T, G, LPR, STAGES, CAND>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     configured |= 1ull << (dev & 63);
   }
   const int n_items = p.rows * p.n_splits;
   const int per_sm = p.ctas_per_sm > 0 ? p.ctas_per_sm : 1 << 20;  // 0: one CTA per item
   const int grid = (int)std::min<long long>(n_items, (long long)per_sm * num_sms());
-  score_fast_kernel<T, G, LPR, STAGES><<<grid, (kCWarps + 1) * 32, smem, st>>>(p);
+  score_fast_kernel<T, G, LPR, STAGES, CAND><<<grid, (kCWarps + 1) * 32, smem, st>>>(p);
 }
 
-template <typename T, int G, int LPR>
+template <typename T, int G, int LPR, bool CAND>
 void launch_fast(const ScoreParams& p, cudaStream_t st) {
   switch (p.stages) {
-    case 6: launch_fast_s<T, G, LPR, 6>(p, st); break;
-    case 8: launch_fast_s<T, G, LPR, 8>(p, st); break;
-    default: launch_fast_s<T, G, LPR, 4>(p, st); break;
+    case 6: launch_fast_s<T, G, LPR, 6, CAND>(p, st); break;
+    case 8: launch_fast_s<T, G, LPR, 8, CAND>(p, st); break;
+    default: launch_fast_s<T, G, LPR, 4, CAND>(p, st); break;
   }
 }
 
 template <typename T>
 bool try_fast(const ScoreParams& p, cudaStream_t st) {
   if (p.h != kH || (p.chunk % kRows) != 0) return false;
+  if (p.cand_nc > 0) {
+    if (p.G != 1 || p.chunk > kMaxCandChunk || p.cand_nc > kCWarps * 32) return false;
+    launch_fast<T, 1, 4, true>(p, st);
+    return true;
+  }
   switch (p.G) {
-    case 1: launch_fast<T, 1, 4>(p, st); return true;
-    case 2: launch_fast<T, 2, 4>(p, st); return true;
-    case 4: launch_fast<T, 4, 8>(p, st); return true;
-    case 8: launch_fast<T, 8, 16>(p, st); return true;
+    case 1: launch_fast<T, 1, 4, false>(p, st); return true;
+    case 2: launch_fast<T, 2, 4, false>(p, st); return true;
+    case 4: launch_fast<T, 4, 8, false>(p, st); return true;
+    case 8: launch_fast<T, 8, 16, false>(p, st); return true;
     default: return false;
   }
 }
@@ -316,7 +395,22 @@ __global__ void l2_flush_kernel(const uint4* p, size_t n16, uint32_t* sink) {
   if (acc == 0x9e3779b9u) sink[0] = acc;  // keeps the loads alive
 }
 
+// read + discard: leaves the swept range's L2 lines invalid (diagnostic knob)
+__global__ void l2_cleanse_kernel(const uint4* p, size_t n16, uint32_t* sink) {
+  uint32_t acc = 0;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n16; i += (size_t)gridDim.x * blockDim.x) {
+    acc ^= p[i].x;
+    if ((i & 7) == 0) discard_l2_line(p + i);
+  }
+  if (acc == 0x9e3779b9u) sink[0] = acc;
+}
+
 }  // namespace
+
+void l2_cleanse_launch(const void* scratch, size_t bytes, cudaStream_t st) {
+  l2_cleanse_kernel<<<148 * 4, 256, 0, st>>>(static_cast<const uint4*>(scratch), bytes / 16,
+                                             (uint32_t*)scratch + (bytes / 4 - 1));
+}
 
 void l2_flush_launch(const void* scratch, size_t bytes, cudaStream_t st) {
   l2_flush_kernel<<<148 * 8, 256, 0, st>>>(static_cast<const uint4*>(scratch), bytes / 16,
@@ -334,9 +428,18 @@ int score_pick_chunk(int s, int rows, int override_chunk) {
   return (int)c;
 }
 
+bool score_cand_supported(int dtype, int h, int G, int chunk, int nc) {
+  return (dtype == KC_F16 || dtype == KC_BF16) && h == kH && G == 1 && chunk % kRows == 0 &&
+         chunk <= kMaxCandChunk && nc >= 1 && nc <= kCWarps * 32;
+}
+
 void score_launch(const ScoreParams& p, int dtype, cudaStream_t st) {
   if (dtype == KC_F16 && try_fast<__half>(p, st)) return;
   if (dtype == KC_BF16 && try_fast<__nv_bfloat16>(p, st)) return;
+  if (p.cand_nc > 0) {  // the caller checked score_cand_supported: never silently dense
+    fprintf(stderr, "kcache: candidate-mode scoring requested for an unsupported shape\n");
+    abort();
+  }
   dim3 grid(p.n_splits, p.rows);
   const size_t smem = 8 * (size_t)p.G * sizeof(float2);
   switch (dtype) {

@@ -26,8 +26,11 @@
 // s <= 32768: keys stay in registers (select_reg_kernel, thread t owns
 // positions [t*KPT, t*KPT+KPT)); longer rows use a global-memory key scratch
 // (select_kernel).
+#include <cfloat>
+
 #include "kc_device.cuh"
 #include "kc_kernels.cuh"
+#include "kcache_c.h"
 
 namespace kc {
 
@@ -174,6 +177,68 @@ __device__ __forceinline__ uint32_t ordered_bits(float x) {
   return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
 }
 
+__device__ __forceinline__ float from_ordered(uint32_t k) {
+  return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
+}
+
+// The p-tie window around a score Ts: outside it p = expf(s - M)/Z differs
+// from p(Ts) strictly, provided p(Ts) is a normal float (see
+// score_fast_kernel's candidate bound).
+__device__ __forceinline__ float tie_window(float Ts, float M) {
+  return 4e-5f * (1.0f + fabsf(Ts) + fabsf(M));
+}
+
+// Candidate-mode fallback: recompute one MHA row's scores into the dense
+// logits row, bit-identical to score_fast_kernel<T, 1, 4, ...>: the same lane
+// roles (4 lanes per position, 16-B chunk c = ((ci ^ (pos & 1)) << 2) | sub),
+// the same fmaf sequence, the same xor-shuffle tree and the multiply by scale
+// after the sum.
+template <typename T>
+__device__ void recompute_row_t(const SelectParams& p, int row) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int rl = lane >> 2, sub = lane & 3;
+  const int b = row / p.n_kv, kvh = row - b * p.n_kv;
+  const float* qh = p.q + ((size_t)b * p.n_kv + kvh) * 128;
+  float qf[4][8];
+#pragma unroll
+  for (int ci = 0; ci < 4; ++ci) {
+    const int c = ((ci ^ (rl & 1)) << 2) | sub;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) qf[ci][e] = qh[c * 8 + e];
+  }
+  const T* kslot = static_cast<const T*>(p.k) + (size_t)row * p.max_seq * 128;
+  float* lrow = const_cast<float*>(p.logits) + ((size_t)b * p.n_kv + kvh) * p.lstride;
+  for (int base = warp * 8; base < p.s; base += kNW * 8) {
+    const int pos = base + rl;
+    float acc = 0.0f;
+    if (pos < p.s) {
+      const uint4* krow = reinterpret_cast<const uint4*>(kslot + (size_t)pos * 128);
+#pragma unroll
+      for (int ci = 0; ci < 4; ++ci) {
+        const int c = ((ci ^ (rl & 1)) << 2) | sub;
+        float kf[8];
+        unpack8<T>(krow[c], kf);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc = fmaf(qf[ci][e], kf[e], acc);
+      }
+    }
+    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+    if (pos < p.s && sub == 0) lrow[pos] = acc * p.scale;
+  }
+}
+
+// Dense-redo prologue of the selection kernels (candidate-mode fallback):
+// false when this row needs no redo.
+__device__ __forceinline__ bool fallback_prologue(const SelectParams& p, int row) {
+  if (!p.fb_flags) return true;
+  if (p.fb_flags[row] == 0) return false;
+  if (p.kdtype == KC_BF16) recompute_row_t<__nv_bfloat16>(p, row);
+  else recompute_row_t<__half>(p, row);
+  __syncthreads();
+  return true;
+}
+
 __device__ __forceinline__ void load_stats(SelShared& S, const SelectParams& p, int b, int kvh) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int n_q = p.n_kv * p.G;
@@ -244,7 +309,8 @@ __device__ __forceinline__ void drop_rows(const float* base, int64_t stride, int
 template <int KPT>
 __global__ void __launch_bounds__(kT, 1) select_reg_kernel(const SelectParams p) {
   __shared__ SelShared S;
-  const int row = blockIdx.x;
+  const int row = p.row0 + blockIdx.x;
+  if (!fallback_prologue(p, row)) return;
   const int b = row / p.n_kv;
   const int kvh = row - b * p.n_kv;
   const int G = p.G;
@@ -301,6 +367,12 @@ __global__ void __launch_bounds__(kT, 1) select_reg_kernel(const SelectParams p)
       if (j0 + i < s) tmax = max(tmax, key[i]);
     uint32_t tau, dummy;
     radix_threshold<1>(S, [&](int, bool& v) { v = true; return tmax; }, nc, kT, tau, dummy);
+    if (G == 1) {
+      // a score just below tau can still share the N-th score's p (p-tie):
+      // lower the bound by the tie window (keys are ordered logit bits)
+      const float ts = from_ordered(tau);
+      if (ts > -INFINITY) tau = ordered_bits(ts - 2.0f * tie_window(ts, S.M[0]));
+    }
     uint32_t ccount = 0;
 #pragma unroll
     for (int i = 0; i < KPT; ++i) ccount += (j0 + i < s && key[i] >= tau) ? 1u : 0u;
@@ -332,14 +404,15 @@ __global__ void __launch_bounds__(kT, 1) select_reg_kernel(const SelectParams p)
         gt = have ? 1u : 0u;  // exactly nc candidates: all of them survive
       } else if (have) {
         if (G == 1) {
-          const float Ts = __uint_as_float((T & 0x80000000u) ? (T & 0x7fffffffu) : ~T);
+          const float Ts = from_ordered(T);
           const float M = S.M[0], Z = S.Z[0];
           const float pT = expf(Ts - M) / Z;
-          const float win = 4e-5f * (1.0f + fabsf(Ts) + fabsf(M));
-          const float sj = __uint_as_float((ck & 0x80000000u) ? (ck & 0x7fffffffu) : ~ck);
+          const float win = tie_window(Ts, M);
+          const bool exact_all = !(pT >= FLT_MIN);  // p(T) subnormal or 0: ties are wide
+          const float sj = from_ordered(ck);
           if (sj > Ts + win) {
             gt = 1;
-          } else if (sj >= Ts - win) {
+          } else if (exact_all || sj >= Ts - win) {
             const float pj = expf(sj - M) / Z;
             gt = pj > pT;
             eq = pj == pT;
@@ -378,17 +451,18 @@ __global__ void __launch_bounds__(kT, 1) select_reg_kernel(const SelectParams p)
   if (G == 1 && nc < s) {
     // p is monotone in s: only logits close to T_s can share T's probability.
     // Inside the window compare exact p (the same expression the weights use).
-    const float Ts = __uint_as_float((T & 0x80000000u) ? (T & 0x7fffffffu) : ~T);
+    const float Ts = from_ordered(T);
     const float M = S.M[0], Z = S.Z[0];
     const float pT = expf(Ts - M) / Z;
-    const float win = 4e-5f * (1.0f + fabsf(Ts) + fabsf(M));
+    const float win = tie_window(Ts, M);
+    const bool exact_all = !(pT >= FLT_MIN);  // p(T) subnormal or 0: ties are wide
 #pragma unroll
     for (int i = 0; i < KPT; ++i) {
       if (j0 + i >= s) continue;
-      const float sj = __uint_as_float((key[i] & 0x80000000u) ? (key[i] & 0x7fffffffu) : ~key[i]);
+      const float sj = from_ordered(key[i]);
       if (sj > Ts + win) {
         cls_gt |= 1u << i;
-      } else if (sj >= Ts - win) {
+      } else if (exact_all || sj >= Ts - win) {
         const float pj = expf(sj - M) / Z;
         if (pj > pT) cls_gt |= 1u << i;
         else if (pj == pT) cls_eq |= 1u << i;
@@ -442,7 +516,8 @@ __global__ void __launch_bounds__(kT, 1) select_reg_kernel(const SelectParams p)
 // Any length: keys in a global scratch row (L2-resident), same rule.
 __global__ void __launch_bounds__(kT) select_kernel(const SelectParams p) {
   __shared__ SelShared S;
-  const int row = blockIdx.x;
+  const int row = p.row0 + blockIdx.x;
+  if (!fallback_prologue(p, row)) return;
   const int b = row / p.n_kv;
   const int kvh = row - b * p.n_kv;
   const int G = p.G;
@@ -565,6 +640,154 @@ __global__ void __launch_bounds__(kT) select_kernel(const SelectParams p) {
   finish_group(S, p, b, kvh);
 }
 
+// Candidate mode (MHA): the scoring kernel left, per split, the positions
+// that can still be in the row's top-N (kc_score.cu emit_candidates) in
+// position order; concatenated over splits they stay in position order, so
+// the dense kernel's rule applies unchanged to the (score, position) list:
+// radix select of the N-th largest score T, p-exact tie classification,
+// ordered compaction. The row is complete -- no excluded position could rank
+// above or tie with p(T) -- iff every split's exclusion bound lies below T's
+// tie window and p(T) is a normal float; otherwise the row is flagged for the
+// dense redo (select_fallback).
+constexpr int kCandKPT = 16;  // up to 16384 candidates per row
+
+__global__ void __launch_bounds__(kT, 1) select_cand_kernel(const SelectParams p) {
+  __shared__ SelShared S;
+  extern __shared__ uint2 csm[];  // [kT * kCandKPT] candidates, then prefix[n_splits + 1]
+  uint32_t* pre = reinterpret_cast<uint32_t*>(csm + kT * kCandKPT);
+  const int row = p.row0 + blockIdx.x;
+  const int b = row / p.n_kv;
+  const int kvh = row - b * p.n_kv;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nc = p.nc;
+  uint32_t* idx = p.idx + (size_t)row * nc;
+  load_stats(S, p, b, kvh);
+
+  if (warp == 0) {
+    const uint2* meta = p.cand_meta + (size_t)row * p.max_splits;
+    uint32_t run = 0;
+    float bmax = -INFINITY;
+    for (int s0 = 0; s0 < p.n_splits; s0 += 32) {
+      const int sp = s0 + lane;
+      const uint2 m = sp < p.n_splits ? meta[sp] : make_uint2(0u, __float_as_uint(-INFINITY));
+      bmax = fmaxf(bmax, __uint_as_float(m.y));
+      uint32_t v = m.x;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t n = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += n;
+      }
+      if (sp < p.n_splits) pre[sp] = run + v - m.x;
+      run += __shfl_sync(0xffffffffu, v, 31);
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) bmax = fmaxf(bmax, __shfl_xor_sync(0xffffffffu, bmax, o));
+    if (lane == 0) {
+      pre[p.n_splits] = run;
+      S.need = run;
+      S.red_f[0] = bmax;
+    }
+  }
+  __syncthreads();
+  const uint32_t C = S.need;
+  const float bmax = S.red_f[0];
+  __syncthreads();  // S.need / S.red_f are reused below
+  if (C > (uint32_t)(kT * kCandKPT) || C < (uint32_t)nc || p.force_fallback) {
+    if (tid == 0) p.fb_flags[row] = 1u;
+    return;
+  }
+  for (int sp = warp; sp < p.n_splits; sp += kNW) {
+    const uint32_t o = pre[sp], n = pre[sp + 1] - o;
+    const uint2* src = p.cand + (size_t)row * p.lstride + (size_t)sp * p.chunk;
+    for (uint32_t i = lane; i < n; i += 32) csm[o + i] = src[i];
+  }
+  __syncthreads();
+
+  const int j0 = tid * kCandKPT;
+  uint32_t key[kCandKPT];
+#pragma unroll
+  for (int i = 0; i < kCandKPT; ++i) key[i] = j0 + i < (int)C ? ordered_bits(__uint_as_float(csm[j0 + i].x)) : 0u;
+
+  uint32_t T, k_eq;
+  if ((uint32_t)nc < C) {
+    radix_threshold<kCandKPT>(S, [&](int i, bool& v) { v = j0 + i < (int)C; return key[i]; }, nc, (int)C, T, k_eq);
+  } else {
+    // every candidate survives: T = the smallest key
+    uint32_t mn = 0xffffffffu;
+#pragma unroll
+    for (int i = 0; i < kCandKPT; ++i)
+      if (j0 + i < (int)C) mn = min(mn, key[i]);
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    if (lane == 0) S.wa[warp] = mn;
+    __syncthreads();
+    if (warp == 0) {
+      uint32_t x = S.wa[lane];
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) x = min(x, __shfl_xor_sync(0xffffffffu, x, o));
+      if (lane == 0) S.bin = x;
+    }
+    __syncthreads();
+    T = S.bin;
+    __syncthreads();
+  }
+  const float Ts = from_ordered(T);
+  const float M = S.M[0], Z = S.Z[0];
+  const float pT = expf(Ts - M) / Z;
+  const float win = tie_window(Ts, M);
+  const bool exact_all = !(pT >= FLT_MIN);
+  if (bmax > -INFINITY && (bmax > Ts - win || exact_all)) {
+    if (tid == 0) p.fb_flags[row] = 1u;  // an excluded position might rank or tie: redo densely
+    return;
+  }
+
+  uint32_t cls_gt = 0, cls_eq = 0;
+#pragma unroll
+  for (int i = 0; i < kCandKPT; ++i) {
+    if (j0 + i >= (int)C) continue;
+    const float sj = from_ordered(key[i]);
+    if (sj > Ts + win) {
+      cls_gt |= 1u << i;
+    } else if (exact_all || sj >= Ts - win) {
+      const float pj = expf(sj - M) / Z;
+      if (pj > pT) cls_gt |= 1u << i;
+      else if (pj == pT) cls_eq |= 1u << i;
+    }
+  }
+  const uint32_t n_gt_local = __popc(cls_gt);
+  uint32_t n_gt_total;
+  {
+    const uint32_t base = block_excl_scan(n_gt_local, S.wc);
+    if (tid == kT - 1) S.need = base + n_gt_local;
+    __syncthreads();
+    n_gt_total = S.need;
+    __syncthreads();
+  }
+  k_eq = (uint32_t)nc - n_gt_total;
+  const uint32_t ceq = __popc(cls_eq);
+  const uint32_t eq_base = block_excl_scan(ceq, S.wa);
+  const uint32_t take = eq_base >= k_eq ? 0u : min(ceq, k_eq - eq_base);
+  uint32_t o = block_excl_scan(n_gt_local + take, S.wb);
+  uint32_t eqr = eq_base;
+  float* wrow = p.w + ((size_t)b * p.n_kv + kvh) * nc;
+#pragma unroll
+  for (int i = 0; i < kCandKPT; ++i) {
+    bool sel = (cls_gt >> i) & 1u;
+    if ((cls_eq >> i) & 1u) {
+      sel = eqr < k_eq;
+      ++eqr;
+    }
+    if (sel) {
+      idx[o] = csm[j0 + i].y;
+      wrow[o] = expf(from_ordered(key[i]) - M) / Z;
+      ++o;
+    }
+  }
+  if (tid == 0) p.fb_flags[row] = 0u;
+  __syncthreads();
+  finish_group(S, p, b, kvh);
+}
+
 // arg_topk over raw floats: ordered-float keys, lowest index wins ties.
 __global__ void __launch_bounds__(kT)
     arg_topk_kernel(const float* values, int n, int nc, uint32_t* keys, uint32_t* out) {
@@ -665,6 +888,25 @@ void select_launch(const SelectParams& p, cudaStream_t st) {
     if (p.s <= 32 * kT) { select_reg_kernel<32><<<p.rows, kT, 0, st>>>(p); return; }
   }
   select_kernel<<<p.rows, kT, 0, st>>>(p);
+}
+
+bool select_cand_launch(const SelectParams& p, cudaStream_t st) {
+  if (p.G != 1 || !p.cand || !p.fb_flags) return false;
+  const size_t smem = (size_t)kT * kCandKPT * sizeof(uint2) + ((size_t)p.n_splits + 1) * 4;
+  if (smem > 200 * 1024) return false;
+  static unsigned long long configured = 0;  // one bit per device
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!(configured >> (dev & 63) & 1ull)) {
+    cudaFuncSetAttribute(select_cand_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    configured |= 1ull << (dev & 63);
+  }
+  select_cand_kernel<<<p.rows, kT, smem, st>>>(p);
+  // dense redo of the flagged rows (CTAs of unflagged rows exit at once)
+  SelectParams f = p;
+  f.force_global = 0;
+  select_launch(f, st);
+  return true;
 }
 
 void probs_launch(const SelectParams& p, float* probs, cudaStream_t st) {
