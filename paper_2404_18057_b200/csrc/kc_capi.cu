@@ -189,12 +189,11 @@ struct kc_cache {
   int score_ctas_per_sm = 0;
   int host_frac_pct = 50;  // hybrid recall: % of rows gathered by host threads
   int auto_recall_mode = kRecallZeroCopy;  // what recall_mode 0 resolves to
-  int score_groups = 1;
+  int score_groups = 1;   // row groups per layer (score -> select -> recall each)
   int k_policy = 0;        // L2 policy of the K stream (kc_device.cuh l2_policy)
   int select_cand = 0;     // MHA: per-split candidates instead of dense logits
   int cand_force_fallback = 0;  // test hook: every candidate-mode row takes the dense redo
-  int debug_skip = 0;      // diagnostic only: bit 0 skips scoring, bit 1 skips selection (stale outputs)   // row groups per layer (score -> select -> recall each)
-  int l2_cleanse_mb = 0;  // diagnostic: read+discard sweep before each recall
+  int keep_logits = 0;     // leave dead logits in L2 instead of discarding them
   int recall_ctas = 64;  // CTAs of the recall kernel (0: one per (batch, kv head))
   int gather_threads = 0;  // 0: 3/4 of the host cores
 
@@ -409,7 +408,7 @@ StepGeom geom(kc_cache* c, uint64_t top_n) {
 // K becomes clean and the scoring kernel may drop its lines after use. Done
 // at the first decode after appends, then whenever the not-yet-clean tail of
 // a layer exceeds ~8 MB; positions appended since stay un-dropped.
-// per-device scratch of 2.5x L2 for the flush / cleanse sweeps
+// per-device scratch of 2.5x L2 for the flush sweep
 std::pair<void*, size_t> l2_scratch(kc_cache* c, cudaStream_t st) {
   static std::mutex mu;
   static std::vector<std::pair<void*, size_t>> bufs(64, {nullptr, 0});
@@ -566,7 +565,7 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
       const int r0 = gi * gsz;
       const int nr = std::min<int>(gsz, (int)c->rows - r0);
       if (nr <= 0) break;
-      if (!(c->debug_skip & 1)) enqueue_score(c, layer, q32, g, st, r0, nr, cand);
+      enqueue_score(c, layer, q32, g, st, r0, nr, cand);
       if (gi == 0 && i >= (uint64_t)kRing && side != st) CK(cudaStreamWaitEvent(st, c->ev_rec[slot], 0));
 
       kc::SelectParams sp{};
@@ -588,6 +587,7 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
       sp.row0 = r0;
       sp.rows = nr;
       sp.force_global = c->select_global;
+      sp.keep_logits = c->keep_logits;
       if (cand) {
         sp.cand = c->cand.as<uint2>();
         sp.cand_meta = c->cand_meta.as<uint2>();
@@ -601,15 +601,13 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
         sp.scale = 1.0f / std::sqrt(static_cast<float>(c->h));  // attention.hpp:15-17
         sp.force_fallback = c->cand_force_fallback;
       }
-      if (!(c->debug_skip & 2))
-        c->timed(1, st, [&] {
-          if (!cand || !kc::select_cand_launch(sp, st)) {
-            sp.cand = nullptr;
-            sp.fb_flags = nullptr;
-            if (cand) fail(KC_ECUDA, "candidate selection unavailable for this shape");
-            kc::select_launch(sp, st);
-          }
-        });
+      c->timed(1, st, [&] {
+        if (!cand) {
+          kc::select_launch(sp, st);
+        } else if (!kc::select_cand_launch(sp, st)) {
+          fail(KC_ECUDA, "candidate selection unavailable for this shape");
+        }
+      });
       CK(cudaEventRecord(c->ev_sel[slot], st));
       if (side != st) CK(cudaStreamWaitEvent(side, c->ev_sel[slot], 0));
 
@@ -659,10 +657,6 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
       rp.reverse = (flags & KC_REVERSE_ACCUM) ? 1 : 0;
       rp.row_offset = dma ? host_rows : r0;
       rp.discard_len = c->discard && (c->h * c->esz) % 128 == 0 ? (int)std::min<uint64_t>(c->layers[layer].clean_len, (uint64_t)g.s) : 0;
-      if (c->l2_cleanse_mb > 0) {
-        const auto buf = l2_scratch(c, side);
-        kc::l2_cleanse_launch(buf.first, std::min<size_t>(buf.second, (size_t)c->l2_cleanse_mb << 20), side);
-      }
       c->timed(2, side, [&] {
         // zero-copy rows first (they need nothing but the selection), then the
         // host-gathered rows once their DMA has landed
@@ -1092,8 +1086,7 @@ int kc_set_tuning(kc_cache* c, const char* key, int64_t value) {
     else if (k == "score_stages") c->score_stages = (int)value;
     else if (k == "score_ctas_per_sm") c->score_ctas_per_sm = (int)value;
     else if (k == "recall_ctas") c->recall_ctas = (int)value;
-    else if (k == "l2_cleanse_mb") c->l2_cleanse_mb = (int)value;
-    else if (k == "debug_skip") c->debug_skip = (int)value;
+    else if (k == "keep_logits") c->keep_logits = value ? 1 : 0;
     else if (k == "select_cand") c->select_cand = value ? 1 : 0;
     else if (k == "k_policy") c->k_policy = (int)value;
     else if (k == "cand_force_fallback") c->cand_force_fallback = value ? 1 : 0;

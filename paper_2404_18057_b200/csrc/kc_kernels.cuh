@@ -45,7 +45,6 @@ struct ScoreParams {
 // Read `bytes` of a scratch buffer larger than L2: evicts (and so writes back)
 // every dirty L2 line, after which all stored K is clean in DRAM.
 void l2_flush_launch(const void* scratch, size_t bytes, cudaStream_t st);
-void l2_cleanse_launch(const void* scratch, size_t bytes, cudaStream_t st);
 // dtype: KC_F32 / KC_F16 / KC_BF16 (storage)
 void score_launch(const ScoreParams& p, int dtype, cudaStream_t st);
 // positions per CTA for a given shape (tuning override when > 0)
@@ -87,6 +86,7 @@ struct SelectParams {
   int kdtype;             // KC_F16 / KC_BF16
   float scale;
   int force_fallback;     // test hook: flag every row for the dense redo
+  int keep_logits;        // 1: leave the dead logits in L2 (no discard.global.L2)
 };
 void select_launch(const SelectParams& p, cudaStream_t st);
 // candidate-mode selection (MHA, fast scoring path) + the dense redo of any

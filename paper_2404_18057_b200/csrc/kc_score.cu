@@ -395,22 +395,7 @@ __global__ void l2_flush_kernel(const uint4* p, size_t n16, uint32_t* sink) {
   if (acc == 0x9e3779b9u) sink[0] = acc;  // keeps the loads alive
 }
 
-// read + discard: leaves the swept range's L2 lines invalid (diagnostic knob)
-__global__ void l2_cleanse_kernel(const uint4* p, size_t n16, uint32_t* sink) {
-  uint32_t acc = 0;
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n16; i += (size_t)gridDim.x * blockDim.x) {
-    acc ^= p[i].x;
-    if ((i & 7) == 0) discard_l2_line(p + i);
-  }
-  if (acc == 0x9e3779b9u) sink[0] = acc;
-}
-
 }  // namespace
-
-void l2_cleanse_launch(const void* scratch, size_t bytes, cudaStream_t st) {
-  l2_cleanse_kernel<<<148 * 4, 256, 0, st>>>(static_cast<const uint4*>(scratch), bytes / 16,
-                                             (uint32_t*)scratch + (bytes / 4 - 1));
-}
 
 void l2_flush_launch(const void* scratch, size_t bytes, cudaStream_t st) {
   l2_flush_kernel<<<148 * 8, 256, 0, st>>>(static_cast<const uint4*>(scratch), bytes / 16,

@@ -436,7 +436,7 @@ __global__ void __launch_bounds__(kT, 1) select_reg_kernel(const SelectParams p)
               expf(lbase[(size_t)g * p.lstride + cp] - S.M[g]) / S.Z[g];
       }
       __syncthreads();
-      drop_rows(lbase, p.lstride, G, s);
+      if (!p.keep_logits) drop_rows(lbase, p.lstride, G, s);
       finish_group(S, p, b, kvh);
       return;
     }
@@ -509,7 +509,7 @@ __global__ void __launch_bounds__(kT, 1) select_reg_kernel(const SelectParams p)
     }
   }
   __syncthreads();
-  drop_rows(lbase, p.lstride, G, s);
+  if (!p.keep_logits) drop_rows(lbase, p.lstride, G, s);
   finish_group(S, p, b, kvh);
 }
 
@@ -635,7 +635,7 @@ __global__ void __launch_bounds__(kT) select_kernel(const SelectParams p) {
     run_sel += __popc(bsel);
   }
   __syncthreads();
-  drop_rows(lbase, p.lstride, G, s);
+  if (!p.keep_logits) drop_rows(lbase, p.lstride, G, s);
   drop_rows(reinterpret_cast<const float*>(keys), 0, 1, s);
   finish_group(S, p, b, kvh);
 }

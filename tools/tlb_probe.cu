@@ -83,6 +83,18 @@ __global__ void sweep(uint4* p, size_t n16, uint32_t* sink, int mode) {
   if (acc == 0x9e3779b9u) sink[0] = acc;
 }
 
+// scoring-like K stream: CTA i reads chunk i (contiguous) of the 2 GiB region,
+// many CTAs in flight at scattered offsets; optional immediate discard
+__global__ void chunked(const uint4* p, size_t chunk16, uint32_t* sink, int disc) {
+  const uint4* c = p + (size_t)blockIdx.x * chunk16;
+  uint32_t acc = 0;
+  for (size_t i = threadIdx.x; i < chunk16; i += blockDim.x) {
+    acc ^= c[i].x;
+    if (disc && (i & 7) == 0) asm volatile("discard.global.L2 [%0], 128;" ::"l"(c + i) : "memory");
+  }
+  if (acc == 0x9e3779b9u) sink[0] = acc;
+}
+
 __global__ void fill(uint4* p, size_t n16) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n16; i += (size_t)gridDim.x * blockDim.x)
     p[i] = make_uint4((uint32_t)i, 1, 2, 3);
@@ -171,7 +183,7 @@ int main(int argc, char** argv) {
   CK(cudaMemcpy(didx, hidx.data(), hidx.size() * 4, cudaMemcpyHostToDevice));
   // mode 4/5: rotate the 2 GiB read+discard sweep over a larger device buffer
   // (like the scoring kernel streaming a different layer's K each time)
-  const size_t sw_total = do_sweep == 4 ? (64ull << 30) : do_sweep == 5 ? (16ull << 30) : (2ull << 30);
+  const size_t sw_total = (do_sweep == 4 || do_sweep >= 10) ? (64ull << 30) : do_sweep == 5 ? (16ull << 30) : (2ull << 30);
   const size_t sw_bytes = 2ull << 30;
   uint4* sw;
   uint32_t* sink;
@@ -185,7 +197,11 @@ int main(int argc, char** argv) {
   for (int rep = 0; rep < 3; ++rep) {
     double tot = 0;
     for (int w = 0; w < n_win; ++w) {
-      if (do_sweep >= 6) {
+      if (do_sweep == 10 || do_sweep == 11) {
+        const int nch = 6912;
+        chunked<<<nch, 256>>>(sw + sw_off / 16, sw_bytes / 16 / nch, sink, do_sweep == 10);
+        sw_off = (sw_off + sw_bytes) % sw_total;
+      } else if (do_sweep >= 6) {
         // logits-like: 2 GiB read+discard (K), then write `lg` MiB (dirty
         // logits), then read + discard them (selection)
         const size_t lg = (size_t)(do_sweep == 6 || do_sweep == 9 ? 32 : do_sweep == 7 ? 16 : 8) << 20;
