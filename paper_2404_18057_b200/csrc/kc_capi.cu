@@ -166,6 +166,7 @@ struct kc_cache {
   int max_splits = 0;
   DevBuf logits, partials, keys, part_out, stage_src, stage_k, stage_v, sel_rows, sel_pos, gather_out;
   DevBuf cand, cand_meta, fb_flags;  // candidate-mode selection scratch
+  DevBuf part_ml;                    // fused full attention: split (m, l)
   DevBuf q32[kRing], idx[kRing], w[kRing], dropped[kRing], norm[kRing], out_tmp[kRing], idx_exp[kRing];
   PinnedBuf host_in, host_out;
   // DMA recall: pinned copy of the selection, pinned compacted rows, HBM copy
@@ -193,6 +194,7 @@ struct kc_cache {
   int k_policy = 0;        // L2 policy of the K stream (kc_device.cuh l2_policy)
   int select_cand = 0;     // MHA: per-split candidates instead of dense logits
   int cand_force_fallback = 0;  // test hook: every candidate-mode row takes the dense redo
+  int full_fused = 1;      // decode_attention_full: fused K+V pass when V is in HBM
   int keep_logits = 0;     // leave dead logits in L2 instead of discarding them
   int recall_ctas = 64;  // CTAs of the recall kernel (0: one per (batch, kv head))
   int gather_threads = 0;  // 0: 3/4 of the host cores
@@ -316,7 +318,7 @@ void destroy(kc_cache* c) {
   }
   for (DevBuf* b : {&c->logits, &c->partials, &c->keys, &c->part_out, &c->stage_src, &c->stage_k,
                     &c->stage_v, &c->sel_rows, &c->sel_pos, &c->gather_out, &c->cand, &c->cand_meta,
-                    &c->fb_flags})
+                    &c->fb_flags, &c->part_ml})
     b->release();
   for (int i = 0; i < kRing; ++i) {
     c->q32[i].release(); c->idx[i].release(); c->w[i].release(); c->dropped[i].release();
@@ -903,16 +905,49 @@ int kc_decode_full(kc_cache* c, uint64_t layer, const void* q, int q_dtype, uint
     const StepGeom g = geom(c, 1);
     maybe_flush_l2(c, &layer, 1, st);
     const float* q32 = stage_q(c, 0, q, q_dtype, io_device, st);
-    enqueue_score(c, layer, q32, g, st, 0, (int)c->rows);
     const uint64_t slots = c->batch * c->n_q;
-    c->part_out.ensure(checked_mul({slots, (uint64_t)g.n_splits, c->h, 4}));
     if (!io_device) c->out_tmp[0].ensure(slots * c->h * 4);
+    float* out_dev = io_device ? out : c->out_tmp[0].as<float>();
+    bool fused = false;
+    if (c->h == 128 && !c->v_in_slow(layer) && c->full_fused) {
+      // K and V both in HBM: one fused pass (kc_score.cu full_fast_kernel)
+      c->part_out.ensure(checked_mul({slots, (uint64_t)c->max_splits, c->h, 4}));
+      c->part_ml.ensure(checked_mul({slots, (uint64_t)c->max_splits, 8}));
+      kc::FullParams fp{};
+      fp.k = c->k_layer(layer);
+      fp.v = c->v_layer(layer);
+      fp.q = q32;
+      fp.part_out = c->part_out.as<float>();
+      fp.part_ml = c->part_ml.as<float2>();
+      fp.out = out_dev;
+      fp.max_seq = (int64_t)c->cfg.max_seq;
+      fp.s = g.s;
+      fp.n_kv = (int)c->n_kv;
+      fp.G = (int)c->G;
+      fp.rows = (int)c->rows;
+      fp.chunk = g.chunk;
+      fp.n_splits = g.n_splits;
+      fp.max_splits = c->max_splits;
+      fp.scale = 1.0f / std::sqrt(static_cast<float>(c->h));  // attention.hpp:15-17
+      fp.discard_len = c->discard ? (int)std::min<uint64_t>(c->layers[layer].clean_len, (uint64_t)g.s) : 0;
+      c->timed(0, st, [&] { fused = kc::full_fast_launch(fp, c->dtype, st); });
+    }
+    if (fused) {
+      CK(cudaGetLastError());
+      if (!io_device) {
+        CK(cudaMemcpyAsync(out, c->out_tmp[0].p, slots * c->h * 4, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+      }
+      return;
+    }
+    enqueue_score(c, layer, q32, g, st, 0, (int)c->rows);
+    c->part_out.ensure(checked_mul({slots, (uint64_t)g.n_splits, c->h, 4}));
     kc::PvFullParams pp{};
     pp.v = c->v_layer(layer);
     pp.logits = c->logits.as<float>();
     pp.partials = c->partials.as<float2>();
     pp.part_out = c->part_out.as<float>();
-    pp.out = io_device ? out : c->out_tmp[0].as<float>();
+    pp.out = out_dev;
     pp.max_seq = (int64_t)c->cfg.max_seq;
     pp.lstride = c->lstride;
     pp.s = g.s;
@@ -1087,6 +1122,7 @@ int kc_set_tuning(kc_cache* c, const char* key, int64_t value) {
     else if (k == "score_ctas_per_sm") c->score_ctas_per_sm = (int)value;
     else if (k == "recall_ctas") c->recall_ctas = (int)value;
     else if (k == "keep_logits") c->keep_logits = value ? 1 : 0;
+    else if (k == "full_fused") c->full_fused = value ? 1 : 0;
     else if (k == "select_cand") c->select_cand = value ? 1 : 0;
     else if (k == "k_policy") c->k_policy = (int)value;
     else if (k == "cand_force_fallback") c->cand_force_fallback = value ? 1 : 0;

@@ -141,6 +141,31 @@ struct PvFullParams {
 };
 void pv_full_launch(const PvFullParams& p, int dtype, cudaStream_t st);
 
+// decode_attention_full fused (K and V in HBM, h = 128, 16-bit storage):
+// one pass per (row, split) streams the split's K then its V through one TMA
+// ring -- scores and the split's softmax stay in shared memory -- and leaves
+// unnormalised split partials (m, l, sum_j exp(s_j - m) V_j) that
+// full_combine folds in split order. Returns false outside its shapes.
+struct FullParams {
+  const void* k;          // [rows][max_seq][h]
+  const void* v;
+  const float* q;         // [batch][n_q][h] fp32
+  float* part_out;        // [batch*n_q][max_splits][h]
+  float2* part_ml;        // [batch*n_q][max_splits] (m, l)
+  float* out;             // [batch][n_q*h]
+  int64_t max_seq;
+  int s;
+  int n_kv;
+  int G;
+  int rows;
+  int chunk;
+  int n_splits;
+  int max_splits;
+  float scale;
+  int discard_len;        // positions < discard_len are clean in DRAM (K and V)
+};
+bool full_fast_launch(const FullParams& p, int dtype, cudaStream_t st);
+
 // Position-major [rows][n_kv*h] input rows -> [b][n_kv][max_seq][h] storage
 // at positions [pos0, pos0 + rows/batch).
 struct AppendParams {

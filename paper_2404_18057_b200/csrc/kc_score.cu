@@ -334,6 +334,259 @@ __global__ void __launch_bounds__(256) score_generic_kernel(const ScoreParams p)
   }
 }
 
+// ---- decode_attention_full, fused (attention.cpp:91-114) -------------------
+// CTA = (row, split). The producer lane streams the split's K stages and then
+// its V stages through one STAGES-deep TMA ring (both 64 positions x 256 B);
+// consumers score K exactly like score_fast_kernel into shared memory, take
+// the split max m and p_j = exp(s_j - m), l = sum p_j, then accumulate
+// sum_j p_j V_j: thread (pg, ch) owns the 16-B column chunk ch of positions
+// pg, pg+16, pg+32, pg+48 of each V stage (a half-warp reads one 256-B row:
+// conflict-free). Partials are reduced across position groups in a fixed
+// order; full_combine_kernel rescales the splits by exp(m_i - M).
+template <typename T, int G, int LPR, int STAGES>
+__global__ void __launch_bounds__((kCWarps + 1) * 32)
+    full_fast_kernel(const FullParams p) {
+  constexpr int CPL = 16 / LPR;
+  constexpr int RPP = 32 / LPR;
+  constexpr int PASSES = (kRows / kCWarps) / RPP;
+  constexpr int ROWB = kH * (int)sizeof(T);
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint8_t* ring = smem;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * kRows * ROWB);
+  uint64_t* empty = full + STAGES;
+  float* mls = reinterpret_cast<float*>(empty + STAGES);  // [G] m, [G] l
+  float* sc = mls + 2 * G;                                // [G][chunk] scores -> p
+  float* red = reinterpret_cast<float*>(ring);            // [kCWarps][G][kH], after the last stage
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int row = blockIdx.x / p.n_splits;
+  const int split = blockIdx.x - row * p.n_splits;
+  const int b = row / p.n_kv, kvh = row - b * p.n_kv;
+  const int n_q = p.n_kv * G;
+  const int pos0 = split * p.chunk;
+  const int npos = min(p.chunk, p.s - pos0);
+  const int n_it = (npos + kRows - 1) / kRows;  // stages per tensor
+  const size_t slot_off = (size_t)row * p.max_seq * kH;
+
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int st = 0; st < STAGES; ++st) {
+      mbar_init(&full[st], 1);
+      mbar_init(&empty[st], kCWarps);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp == kCWarps) {
+    const uint64_t pol = l2_evict_first_policy();
+    const char* held[STAGES];
+    int held_lines[STAGES];
+#pragma unroll
+    for (int st = 0; st < STAGES; ++st) held_lines[st] = 0;
+    auto land_and_drop = [&](uint32_t j) {
+      const int sj = (int)(j % STAGES);
+      mbar_wait(&full[sj], (j / STAGES) & 1);
+      for (int l = lane; l < held_lines[sj]; l += 32) discard_l2_line(held[sj] + (size_t)l * 128);
+    };
+    const uint32_t total = 2u * (uint32_t)n_it;
+    for (uint32_t g = 0; g < total; ++g) {
+      const int st = (int)(g % STAGES);
+      if (g >= (uint32_t)STAGES) mbar_wait(&empty[st], ((g / STAGES) - 1) & 1);
+      const int it = (int)(g % (uint32_t)n_it);
+      const T* base = static_cast<const T*>(g < (uint32_t)n_it ? p.k : p.v) + slot_off;
+      const int pstart = pos0 + it * kRows;
+      const int rows = min(kRows, npos - it * kRows);
+      held[st] = reinterpret_cast<const char*>(base + (size_t)pstart * kH);
+      held_lines[st] = max(0, min(pstart + rows, p.discard_len) - pstart) * (ROWB / 128);
+      if (lane == 0) {
+        const uint32_t bytes = (uint32_t)(rows * ROWB);
+        mbar_arrive_expect_tx(&full[st], bytes);
+        tma_bulk_g2s(ring + st * kRows * ROWB, base + (size_t)pstart * kH, bytes, &full[st], pol);
+      }
+      __syncwarp();
+      if (g >= (uint32_t)(STAGES - 1)) land_and_drop(g - (STAGES - 1));
+    }
+    for (uint32_t j = total > (uint32_t)(STAGES - 1) ? total - (STAGES - 1) : 0; j < total; ++j) land_and_drop(j);
+    return;
+  }
+
+  // ---- phase 1: scores of the split's positions -> sc ----
+  const int sub = lane % LPR, rl = lane / LPR;
+  float qf[G][CPL][8];
+#pragma unroll
+  for (int gh = 0; gh < G; ++gh) {
+    const float* qh = p.q + ((size_t)b * n_q + kvh * G + gh) * kH;
+#pragma unroll
+    for (int ci = 0; ci < CPL; ++ci) {
+      const int c = chunk_of<LPR>(ci, rl, sub);
+      const float4 a = *reinterpret_cast<const float4*>(qh + c * 8);
+      const float4 bq = *reinterpret_cast<const float4*>(qh + c * 8 + 4);
+      qf[gh][ci][0] = a.x; qf[gh][ci][1] = a.y; qf[gh][ci][2] = a.z; qf[gh][ci][3] = a.w;
+      qf[gh][ci][4] = bq.x; qf[gh][ci][5] = bq.y; qf[gh][ci][6] = bq.z; qf[gh][ci][7] = bq.w;
+    }
+  }
+  uint32_t g = 0;
+  for (int it = 0; it < n_it; ++it, ++g) {
+    const int st = (int)(g % STAGES);
+    mbar_wait(&full[st], (g / STAGES) & 1);
+    const uint8_t* sb = ring + st * kRows * ROWB;
+#pragma unroll
+    for (int pass = 0; pass < PASSES; ++pass) {
+      const int r = warp * (kRows / kCWarps) + pass * RPP + rl;
+      const int pl = it * kRows + r;
+      const uint4* srow = reinterpret_cast<const uint4*>(sb + r * ROWB);
+      float acc[G];
+#pragma unroll
+      for (int gh = 0; gh < G; ++gh) acc[gh] = 0.0f;
+#pragma unroll
+      for (int ci = 0; ci < CPL; ++ci) {
+        const uint4 raw = srow[chunk_of<LPR>(ci, rl, sub)];
+        float kf[8];
+        unpack8<T>(raw, kf);
+#pragma unroll
+        for (int gh = 0; gh < G; ++gh) {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) acc[gh] = fmaf(qf[gh][ci][e], kf[e], acc[gh]);
+        }
+      }
+#pragma unroll
+      for (int o = LPR / 2; o >= 1; o >>= 1) {
+#pragma unroll
+        for (int gh = 0; gh < G; ++gh) acc[gh] += __shfl_xor_sync(0xffffffffu, acc[gh], o);
+      }
+      float mine = acc[0];
+#pragma unroll
+      for (int gh = 1; gh < G; ++gh) mine = (sub == gh) ? acc[gh] : mine;
+      if (pl < npos && sub < G) sc[sub * p.chunk + pl] = mine * p.scale;
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
+  }
+  named_sync(1, kCWarps * 32);
+  // ---- split softmax: m, p_j = exp(s_j - m), l = sum p_j (warp per head) ----
+  for (int gh = warp; gh < G; gh += kCWarps) {
+    float* sg = sc + gh * p.chunk;
+    float m = -INFINITY;
+    for (int j = lane; j < npos; j += 32) m = fmaxf(m, sg[j]);
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    float l = 0.0f;
+    for (int j = lane; j < npos; j += 32) {
+      const float e = expf(sg[j] - m);
+      sg[j] = e;
+      l += e;
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
+    if (lane == 0) {
+      mls[gh] = m;
+      mls[G + gh] = l;
+    }
+  }
+  named_sync(1, kCWarps * 32);
+  // ---- phase 2: sum_j p_j V_j ----
+  const int ct = threadIdx.x;
+  const int ch = ct & 15, pg = ct >> 4;
+  float acc[G][8];
+#pragma unroll
+  for (int gh = 0; gh < G; ++gh)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[gh][e] = 0.0f;
+  for (int it = 0; it < n_it; ++it, ++g) {
+    const int st = (int)(g % STAGES);
+    mbar_wait(&full[st], (g / STAGES) & 1);
+    const uint8_t* sb = ring + st * kRows * ROWB;
+#pragma unroll
+    for (int k4 = 0; k4 < kRows / 16; ++k4) {
+      const int j = pg + 16 * k4;
+      const int pl = it * kRows + j;
+      if (pl < npos) {
+        float vf[8];
+        unpack8<T>(reinterpret_cast<const uint4*>(sb + j * ROWB)[ch], vf);
+#pragma unroll
+        for (int gh = 0; gh < G; ++gh) {
+          const float w = sc[gh * p.chunk + pl];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) acc[gh][e] = fmaf(w, vf[e], acc[gh][e]);
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
+  }
+  // position groups pg and pg^1 share a warp (lanes ch, ch + 16)
+#pragma unroll
+  for (int gh = 0; gh < G; ++gh)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[gh][e] += __shfl_xor_sync(0xffffffffu, acc[gh][e], 16);
+  // the ring is free once every stage is consumed and every TMA has landed
+  named_sync(1, kCWarps * 32);
+  if (lane < 16) {
+#pragma unroll
+    for (int gh = 0; gh < G; ++gh)
+#pragma unroll
+      for (int e = 0; e < 8; ++e) red[(warp * G + gh) * kH + ch * 8 + e] = acc[gh][e];
+  }
+  named_sync(1, kCWarps * 32);
+  for (int o = ct; o < G * kH; o += kCWarps * 32) {
+    const int gh = o / kH, c = o - gh * kH;
+    float a = 0.0f;
+#pragma unroll
+    for (int w = 0; w < kCWarps; ++w) a += red[(w * G + gh) * kH + c];
+    const size_t slot = (size_t)b * n_q + kvh * G + gh;
+    p.part_out[(slot * p.max_splits + split) * kH + c] = a;
+    if (c == 0) p.part_ml[slot * p.max_splits + split] = make_float2(mls[gh], mls[G + gh]);
+  }
+}
+
+// out = sum_i exp(m_i - M) acc_i / sum_i exp(m_i - M) l_i, splits in order
+__global__ void full_combine_kernel(const FullParams p) {
+  const int slot = blockIdx.x;
+  const int c = threadIdx.x;  // kH threads
+  const float2* ml = p.part_ml + (size_t)slot * p.max_splits;
+  float M = -INFINITY;
+  for (int i = 0; i < p.n_splits; ++i) M = fmaxf(M, ml[i].x);
+  float num = 0.0f, den = 0.0f;
+  for (int i = 0; i < p.n_splits; ++i) {
+    const float f = expf(ml[i].x - M);
+    num = fmaf(f, p.part_out[((size_t)slot * p.max_splits + i) * kH + c], num);
+    den = fmaf(f, ml[i].y, den);
+  }
+  p.out[(size_t)slot * kH + c] = num / den;
+}
+
+template <typename T, int G, int LPR>
+void launch_full(const FullParams& p, cudaStream_t st) {
+  constexpr int STAGES = 4;
+  constexpr int ROWB = kH * (int)sizeof(T);
+  const size_t smem = STAGES * kRows * ROWB + 2 * STAGES * sizeof(uint64_t) +
+                      (2 * G + (size_t)G * p.chunk) * sizeof(float);
+  static unsigned long long configured = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!(configured >> (dev & 63) & 1ull)) {
+    cudaFuncSetAttribute(full_fast_kernel<T, G, LPR, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         200 * 1024);
+    configured |= 1ull << (dev & 63);
+  }
+  full_fast_kernel<T, G, LPR, STAGES><<<p.rows * p.n_splits, (kCWarps + 1) * 32, smem, st>>>(p);
+  full_combine_kernel<<<(p.rows / p.n_kv) * p.n_kv * G, kH, 0, st>>>(p);
+}
+
+template <typename T>
+bool try_full(const FullParams& p, cudaStream_t st) {
+  // red ([8][G][128] floats) aliases the ring; sc must fit beside it
+  if ((p.chunk % kRows) != 0 || (size_t)p.G * p.chunk * 4 > 96 * 1024) return false;
+  switch (p.G) {
+    case 1: launch_full<T, 1, 4>(p, st); return true;
+    case 2: launch_full<T, 2, 4>(p, st); return true;
+    case 4: launch_full<T, 4, 8>(p, st); return true;
+    case 8: launch_full<T, 8, 16>(p, st); return true;
+    default: return false;
+  }
+}
+
 int num_sms() {
   static int n[64] = {0};
   int dev = 0;
@@ -411,6 +664,12 @@ int score_pick_chunk(int s, int rows, int override_chunk) {
   c = std::max<long long>(256, std::min<long long>(2048, c));
   c = ((c + kRows - 1) / kRows) * kRows;
   return (int)c;
+}
+
+bool full_fast_launch(const FullParams& p, int dtype, cudaStream_t st) {
+  if (dtype == KC_F16) return try_full<__half>(p, st);
+  if (dtype == KC_BF16) return try_full<__nv_bfloat16>(p, st);
+  return false;
 }
 
 bool score_cand_supported(int dtype, int h, int G, int chunk, int nc) {

@@ -471,6 +471,15 @@ class TieredKVCache:
         _check(self._lib.kc_decode_topn_layers(self._h, n, arr_l, arr_q, dt, top_n, flags, arr_o, st))
         return [(arr_o[i].nc, arr_o[i].h2d_bytes) for i in range(n)]
 
+    def decode_full_device(self, layer: int, q, out, stream=None) -> None:
+        """decode_attention_full with device q (torch fp32/fp16/bf16 [batch,
+        n_heads*h]) and device out (torch fp32 [batch, d]); asynchronous on
+        `stream` (default: torch's current stream)."""
+        import torch
+        dt = {torch.float32: KC_F32, torch.float16: KC_F16, torch.bfloat16: KC_BF16}[q.dtype]
+        st = stream.cuda_stream if stream is not None else torch.cuda.current_stream().cuda_stream
+        _check(self._lib.kc_decode_full(self._h, layer, q.data_ptr(), dt, KC_IO_DEVICE, out.data_ptr(), st))
+
     def decode_topn_layers_host(self, layers: Sequence[int], qs: Sequence[np.ndarray], top_n: int,
                                 outs: Sequence[dict], renormalize=False) -> list:
         """Same with host numpy buffers (H2D of q and D2H of every output inside
