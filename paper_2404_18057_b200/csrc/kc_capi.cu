@@ -192,7 +192,9 @@ struct kc_cache {
   int auto_recall_mode = kRecallZeroCopy;  // what recall_mode 0 resolves to
   int score_groups = 1;   // row groups per layer (score -> select -> recall each)
   int k_policy = 0;        // L2 policy of the K stream (kc_device.cuh l2_policy)
-  int select_cand = 0;     // MHA: per-split candidates instead of dense logits
+  // MHA candidate selection: 0 auto (rows longer than the register-resident
+  // dense select), 1 always, 2 never
+  int select_cand = 0;
   int cand_force_fallback = 0;  // test hook: every candidate-mode row takes the dense redo
   int full_fused = 1;      // decode_attention_full: fused K+V pass when V is in HBM
   int keep_logits = 0;     // leave dead logits in L2 instead of discarding them
@@ -555,8 +557,8 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
     // positions instead of 4 B of fp32 logit per position -- the dense logits
     // (32 MiB per C2 layer) would evict the GPU page-table lines the zero-copy
     // recall walks from L2.
-    const bool cand = c->select_cand && !c->select_global &&
-                      kc::score_cand_supported(c->dtype, (int)c->h, (int)c->G, g.chunk, g.nc);
+    const bool cand = (c->select_cand == 1 || (c->select_cand == 0 && g.s > kc::kDenseRegMaxS)) &&
+                      !c->select_global && kc::score_cand_supported(c->dtype, (int)c->h, (int)c->G, g.chunk, g.nc);
     if (cand) {
       c->cand.ensure(checked_mul({c->rows, (uint64_t)c->lstride, 8}));
       c->cand_meta.ensure(checked_mul({c->rows, (uint64_t)c->max_splits, 8}));
@@ -1123,7 +1125,10 @@ int kc_set_tuning(kc_cache* c, const char* key, int64_t value) {
     else if (k == "recall_ctas") c->recall_ctas = (int)value;
     else if (k == "keep_logits") c->keep_logits = value ? 1 : 0;
     else if (k == "full_fused") c->full_fused = value ? 1 : 0;
-    else if (k == "select_cand") c->select_cand = value ? 1 : 0;
+    else if (k == "select_cand") {
+      if (value < 0 || value > 2) fail(KC_EARG, "select_cand: 0 auto, 1 on, 2 off");
+      c->select_cand = (int)value;
+    }
     else if (k == "k_policy") c->k_policy = (int)value;
     else if (k == "cand_force_fallback") c->cand_force_fallback = value ? 1 : 0;
     else if (k == "score_groups") {

@@ -89,6 +89,8 @@ struct SelectParams {
   int keep_logits;        // 1: leave the dead logits in L2 (no discard.global.L2)
 };
 void select_launch(const SelectParams& p, cudaStream_t st);
+// longest row the dense selection keeps in registers (select_reg_kernel)
+constexpr int kDenseRegMaxS = 32 * 1024;
 // candidate-mode selection (MHA, fast scoring path) + the dense redo of any
 // row it flags; returns false when the shape is outside candidate mode
 bool select_cand_launch(const SelectParams& p, cudaStream_t st);

@@ -62,49 +62,63 @@ __device__ __forceinline__ int chunk_of(int ci, int rl, int sub) {
 // score and recomputes the row densely if it is ever too narrow.
 __device__ __forceinline__ void emit_candidates(const float* scb, float* mx, uint32_t* wcnt, int npos,
                                                 int nc, int pos0, uint2* cand, uint2* meta) {
+  constexpr int NT = kCWarps * 32;
   const int ct = threadIdx.x;  // 0..255 (consumer warps)
   const int lane = ct & 31, warp = ct >> 5;
+  float* mred = mx + NT;  // [kCWarps]
+  // thread ct owns the contiguous positions [a, e) of the split
+  const int ppt = (npos + NT - 1) / NT;
+  const int a = min(npos, ct * ppt), e = min(npos, a + ppt);
   float bound = -INFINITY;
   if (npos > nc) {
-    const int ppt = (npos + kCWarps * 32 - 1) / (kCWarps * 32);
-    const int a = ct * ppt, e = min(npos, a + ppt);
     float m = -INFINITY;
     for (int j = a; j < e; ++j) m = fmaxf(m, scb[j]);
     mx[ct] = m;
-    named_sync(1, kCWarps * 32);
+    named_sync(1, NT);
+    // r = maxima strictly above m: the nc-th largest maximum is the smallest
+    // m with r < nc (no tie-break needed)
     int r = 0;
     float smax = -INFINITY;
-    for (int u = 0; u < kCWarps * 32; ++u) {
-      const float v = mx[u];
-      r += (v > m || (v == m && u < ct)) ? 1 : 0;
-      smax = fmaxf(smax, v);
+    const float4* mx4 = reinterpret_cast<const float4*>(mx);
+#pragma unroll 8
+    for (int u = 0; u < NT / 4; ++u) {
+      const float4 v = mx4[u];
+      r += (v.x > m) + (v.y > m) + (v.z > m) + (v.w > m);
+      smax = fmaxf(smax, fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w)));
     }
-    named_sync(1, kCWarps * 32);  // every rank is computed before mx[0] is reused
-    if (r == nc - 1) mx[0] = m;   // ranks are a permutation: exactly one writer
-    named_sync(1, kCWarps * 32);
-    const float tau = mx[0];
+    float t = r < nc ? m : INFINITY;
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) t = fminf(t, __shfl_xor_sync(0xffffffffu, t, o));
+    if (lane == 0) mred[warp] = t;
+    named_sync(1, NT);
+    float tau = mred[0];
+#pragma unroll
+    for (int w = 1; w < kCWarps; ++w) tau = fminf(tau, mred[w]);
     if (tau > -INFINITY) bound = tau - 0x1p-9f * (1.0f + fabsf(tau) + fabsf(smax));
   }
-  uint32_t run = 0;
-  for (int base = 0; base < npos; base += kCWarps * 32) {
-    const int j = base + ct;
-    const float v = j < npos ? scb[j] : 0.0f;
-    const bool keep = j < npos && v >= bound;
-    const uint32_t bal = __ballot_sync(0xffffffffu, keep);
-    if (lane == 0) wcnt[warp] = __popc(bal);
-    named_sync(1, kCWarps * 32);
-    uint32_t off = run, tot = 0;
+  // ordered compaction: count, block exclusive scan, write in position order
+  uint32_t cnt = 0;
+  for (int j = a; j < e; ++j) cnt += scb[j] >= bound ? 1u : 0u;
+  uint32_t v = cnt;
 #pragma unroll
-    for (int w = 0; w < kCWarps; ++w) {
-      const uint32_t c = wcnt[w];
-      off += (w < warp) ? c : 0u;
-      tot += c;
-    }
-    if (keep) cand[off + __popc(bal & lanemask_lt())] = make_uint2(__float_as_uint(v), (uint32_t)(pos0 + j));
-    run += tot;
-    named_sync(1, kCWarps * 32);  // wcnt is rewritten by the next block
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t n = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += n;
   }
-  if (ct == 0) *meta = make_uint2(run, __float_as_uint(bound));
+  if (lane == 31) wcnt[warp] = v;
+  named_sync(1, NT);
+  uint32_t off = v - cnt, tot = 0;
+#pragma unroll
+  for (int w = 0; w < kCWarps; ++w) {
+    const uint32_t c = wcnt[w];
+    off += (w < warp) ? c : 0u;
+    tot += c;
+  }
+  for (int j = a; j < e; ++j) {
+    const float x = scb[j];
+    if (x >= bound) cand[off++] = make_uint2(__float_as_uint(x), (uint32_t)(pos0 + j));
+  }
+  if (ct == 0) *meta = make_uint2(tot, __float_as_uint(bound));
 }
 
 template <typename T, int G, int LPR, int STAGES, bool CAND>
@@ -124,7 +138,7 @@ __global__ void __launch_bounds__((kCWarps + 1) * 32)
   // candidate mode: the split's scores, block maxima, warp counts
   float* scb = reinterpret_cast<float*>(red + kCWarps * G);  // [chunk]
   float* mx = scb + (CAND ? p.chunk : 0);                     // [256]
-  uint32_t* wcnt = reinterpret_cast<uint32_t*>(mx + kCWarps * 32);
+  uint32_t* wcnt = reinterpret_cast<uint32_t*>(mx + kCWarps * 32 + kCWarps);
   static_assert(!CAND || G == 1, "candidate mode ranks raw scores: MHA only");
 
   const int n_items = p.rows * p.n_splits;
@@ -600,7 +614,7 @@ void launch_fast_s(const ScoreParams& p, cudaStream_t st) {
   constexpr int ROWB = kH * (int)sizeof(T);
   const size_t smem = STAGES * kRows * ROWB + 2 * STAGES * sizeof(uint64_t) +
                       kCWarps * G * sizeof(float2) +
-                      (CAND ? (size_t)kMaxCandChunk * 4 + kCWarps * 32 * 4 + kCWarps * 4 : 0);
+                      (CAND ? (size_t)kMaxCandChunk * 4 + kCWarps * 32 * 4 + 2 * kCWarps * 4 : 0);
   static unsigned long long configured = 0;  // one bit per device
   int dev = 0;
   cudaGetDevice(&dev);

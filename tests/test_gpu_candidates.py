@@ -55,7 +55,7 @@ def test_candidates_equal_dense_bitwise(kc, oracle, case):
     q = synth_matrix(1, b, n * h, dtype=dtype)
     for renorm in (False, True):
         cand = _run(kc, cache, q, N, renorm)
-        dense = _run(kc, cache, q, N, renorm, select_cand=0)
+        dense = _run(kc, cache, q, N, renorm, select_cand=2)
         redo = _run(kc, cache, q, N, renorm, cand_force_fallback=1)
         _assert_same(cand, dense)
         _assert_same(redo, dense)
@@ -78,7 +78,7 @@ def test_tie_flood_selects_lowest_positions(kc, oracle):
     q = synth_matrix(1, b, n * h)
     res = _run(kc, cache, q, N)
     np.testing.assert_array_equal(res.selection.indices, np.tile(np.arange(N, dtype=np.uint32), (b * n, 1)))
-    dense = _run(kc, cache, q, N, select_cand=0)
+    dense = _run(kc, cache, q, N, select_cand=2)
     _assert_same(res, dense)
     cache.close()
 
@@ -106,7 +106,7 @@ def test_underflow_ties_take_lowest_positions(kc, oracle):
     for slot in range(b * n):
         np.testing.assert_array_equal(o_idx[slot], want)
         np.testing.assert_array_equal(res.selection.indices[slot], want)
-    _assert_same(res, _run(kc, cache, q, N, select_cand=0))
+    _assert_same(res, _run(kc, cache, q, N, select_cand=2))
     cache.close()
 
 
