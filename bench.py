@@ -166,6 +166,61 @@ def run_reference_arm(args, cfg):
     print(json.dumps(line), flush=True)
 
 
+def full_kv_step(kc, torch, cfg, dev, local_rank, rank, args, barrier):
+    """decode_attention_full over every layer with K and V resident in HBM
+    (C2: 128 GiB), timed like the KCache step. Returns the per-step numbers."""
+    L, b, n, n_kv, h, s = (cfg[k] for k in ("n_layers", "batch", "n_heads", "n_kv", "h", "s"))
+    d = n * h
+    mcfg = kc.ModelConfig(L, d, n, h, kc.ModelConfig.default_ffn_hidden(d), 32000, s, n_kv)
+    cache = kc.TieredKVCache(mcfg, b, kc.TierPlacement.kcache(L, L, 2, "f16"), device=local_rank)
+    kbuf = torch.empty(s * b, n_kv * h, dtype=torch.float16, device=dev)
+    vbuf = torch.empty_like(kbuf)
+    seed_off = 1_000_003 * rank
+    for layer in range(L):
+        kc.fill_uniform(kbuf, SEED_K + 100 * layer + seed_off)
+        kc.fill_uniform(vbuf, SEED_V + 100 * layer + seed_off)
+        cache.append_kv_device(layer, kbuf, vbuf)
+    torch.cuda.synchronize()
+    del kbuf, vbuf
+    torch.cuda.empty_cache()
+    for layer in range(L):
+        cache.offload_prefill_v(layer)
+    cache.begin_decode()
+    qs = []
+    for layer in range(L):
+        q16 = torch.empty(b, d, dtype=torch.float16, device=dev)
+        kc.fill_uniform(q16, SEED_Q + 100 * layer + seed_off)
+        qs.append(q16.float())
+    outs = [torch.empty(b, d, dtype=torch.float32, device=dev) for _ in range(L)]
+    stream = torch.cuda.Stream(device=dev)
+
+    def step():
+        for layer in range(L):
+            cache.decode_full_device(layer, qs[layer], outs[layer], stream=stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    steps = min(args.steps, 10)
+    for _ in range(steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    ms = e0.elapsed_time(e1) / steps
+    kv_bytes = 2 * 2 * b * n_kv * s * h * L
+    cache.close()
+    del qs, outs
+    torch.cuda.empty_cache()
+    return {"ms_per_step": ms, "steps": steps, "kv_bytes_per_step": kv_bytes,
+            "hbm_gbs": kv_bytes / (ms * 1e-3) / 1e9, "hbm_bytes": kv_bytes}
+
+
 def run_ours(args, cfg):
     import numpy as np
     import torch
@@ -257,7 +312,13 @@ def run_ours(args, cfg):
     select_ms, select_n = cache.profile_read("select")
     recall_ms, recall_n = cache.profile_read("recall")
     all_score_ms, _ = cache.profile_read("score")
+    # each kernel alone (serial schedule): what the pipelined overlap costs it
+    cache.set_tuning("pipeline", 0)
+    cache.profile(True)
+    serial_ms, _ = timed_steps(min(prof_steps, 3))
+    iso = {k: cache.profile_read(k) for k in ("score", "select", "recall")}
     cache.profile(False)
+    cache.set_tuning("pipeline", 1)
     h2d_per_layer = info[0][1]
 
     # ---- end to end: host (pinned) q in, every output back to the host ----
@@ -293,6 +354,16 @@ def run_ours(args, cfg):
     cache.close()
     del qs, outs
     torch.cuda.empty_cache()
+
+    # ---- the comparator: full-KV-in-HBM decode attention on the same workload ----
+    full = None
+    if not args.no_full_kv:
+        full = full_kv_step(kc, torch, cfg, dev, local_rank, rank, args, barrier)
+        if world > 1:
+            t = torch.tensor([full["ms_per_step"]], device=dev)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            full["ms_per_step"] = float(t[0])
+            full["hbm_gbs"] = full["kv_bytes_per_step"] / (full["ms_per_step"] * 1e-3) / 1e9
 
     if rank != 0:
         if world > 1:
@@ -345,11 +416,20 @@ def run_ours(args, cfg):
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": L * b * d * 4,
                 "d2h_bytes_per_step": L * (b * d * 4 + slots * nc * 8 + slots * 8), "ms_per_step": e2e_ms,
                 "path": "kc_decode_topn_layers with pinned host q / outputs (TieredKVCache.decode_topn_layers_host)"},
+        "kernel_isolated_ms_per_launch": {k: iso[k][0] / max(iso[k][1], 1) for k in iso},
+        "serial_step_ms": serial_ms,
         "gpu_launches": launches_per_layer * L * args.steps,
         "clocks": clocks,
         "setup_s": setup_s,
         "e2e_checksum": e2e_check,
     }
+    line["roofline"]["achieved_isolated"] = k_bytes_layer / (iso["score"][0] / max(iso["score"][1], 1) * 1e-3) / 1e9
+    if full is not None:
+        full_ms = full["ms_per_step"]
+        line["full_kv"] = dict(full, value=world * b / (full_ms * 1e-3), unit=UNIT,
+                               kcache_over_full=full_ms / ms,
+                               note="same workload with K and V in HBM, fused flash-decode kernel "
+                                    "(decode_attention_full, attention.cpp:91-114): the paper's comparator")
     if world == 1 and not args.no_cpu_baseline:
         res = cpu_reference_sample(cfg, os.cpu_count() or 1, passes=1)
         if res is not None:
@@ -372,6 +452,7 @@ def main():
     ap.add_argument("--topn", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-full-kv", action="store_true", help="skip the full-KV-in-HBM comparator")
     ap.add_argument("--tune", action="append", default=[], help="kc_set_tuning key=value")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
