@@ -175,7 +175,7 @@ struct kc_cache {
   std::unique_ptr<kc::GatherPool> pool;
   cudaStream_t main_st = nullptr, side_st = nullptr, gather_st = nullptr;
   cudaEvent_t ev_start = nullptr, ev_end = nullptr, ev_sel[kRing] = {}, ev_rec[kRing] = {},
-              ev_gath[kRing] = {};
+              ev_gath[kRing] = {}, ev_scored[kRing] = {};
 
   // tuning
   int score_chunk = 0;
@@ -196,6 +196,7 @@ struct kc_cache {
   // dense select), 1 always, 2 never
   int select_cand = 0;
   int cand_force_fallback = 0;  // test hook: every candidate-mode row takes the dense redo
+  int select_on_side = 0;  // pipelined: selection on the side stream too (measured: no gain)
   int full_fused = 1;      // decode_attention_full: fused K+V pass when V is in HBM
   int keep_logits = 0;     // leave dead logits in L2 instead of discarding them
   int recall_ctas = 64;  // CTAs of the recall kernel (0: one per (batch, kv head))
@@ -229,6 +230,11 @@ struct kc_cache {
     prof[kind].push_back({a, b});
   }
 
+  // scoring buffer lb (0/1) of logits / partials / candidates
+  float* logits_buf(int lb) { return logits.as<float>() + (size_t)lb * batch * n_q * (size_t)lstride; }
+  float2* partials_buf(int lb) { return partials.as<float2>() + (size_t)lb * batch * n_q * (size_t)max_splits; }
+  uint2* cand_buf(int lb) { return cand.as<uint2>() + (size_t)lb * rows * (size_t)lstride; }
+  uint2* cand_meta_buf(int lb) { return cand_meta.as<uint2>() + (size_t)lb * rows * (size_t)max_splits; }
   void* k_layer(uint64_t layer) const { return (char*)k_arena + layer * k_layer_bytes; }
   void* v_layer(uint64_t layer) const {
     return layer < L ? (void*)((char*)v_dev + layer * v_layer_bytes)
@@ -326,6 +332,7 @@ void destroy(kc_cache* c) {
     c->q32[i].release(); c->idx[i].release(); c->w[i].release(); c->dropped[i].release();
     c->norm[i].release(); c->out_tmp[i].release(); c->idx_exp[i].release();
     if (c->ev_sel[i]) cudaEventDestroy(c->ev_sel[i]);
+    if (c->ev_scored[i]) cudaEventDestroy(c->ev_scored[i]);
     if (c->ev_rec[i]) cudaEventDestroy(c->ev_rec[i]);
   }
   c->host_in.release();
@@ -443,18 +450,18 @@ void maybe_flush_l2(kc_cache* c, const uint64_t* layers, uint64_t n, cudaStream_
 }
 
 void enqueue_score(kc_cache* c, uint64_t layer, const float* q32, const StepGeom& g, cudaStream_t st,
-                   int row0, int nrows, bool cand = false) {
+                   int row0, int nrows, bool cand = false, int lb = 0) {
   kc::ScoreParams sp{};
   sp.row0 = row0;
   if (cand) {
-    sp.cand = c->cand.as<uint2>();
-    sp.cand_meta = c->cand_meta.as<uint2>();
+    sp.cand = c->cand_buf(lb);
+    sp.cand_meta = c->cand_meta_buf(lb);
     sp.cand_nc = g.nc;
   }
   sp.k = c->k_layer(layer);
   sp.q = q32;
-  sp.logits = c->logits.as<float>();
-  sp.partials = c->partials.as<float2>();
+  sp.logits = c->logits_buf(lb);
+  sp.partials = c->partials_buf(lb);
   sp.max_seq = (int64_t)c->cfg.max_seq;
   sp.lstride = c->lstride;
   sp.s = g.s;
@@ -530,6 +537,10 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
   if (!io_device) c->host_out.ensure(per_layer * n);
 
   cudaStream_t side = c->pipeline ? c->side_st : st;
+  // the selection runs on the side stream too, so the main stream is scoring
+  // only: scoring(i+1) overlaps selection(i) as well as recall(i)
+  const bool side_select = side != st && c->select_on_side;
+  cudaStream_t selst = side_select ? side : st;
   maybe_flush_l2(c, layers, n, st);
   CK(cudaEventRecord(c->ev_start, st));
   if (side != st) CK(cudaStreamWaitEvent(side, c->ev_start, 0));
@@ -537,6 +548,10 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
   for (uint64_t i = 0; i < n; ++i) {
     const int slot = (int)(i % kRing);
     const uint64_t layer = layers[i];
+    // selection on the side stream: scoring buffer i % 2, free once the
+    // selection of layer i-2 (which also released q32[slot]) has finished
+    const int lb = side_select ? (int)(i & 1) : 0;
+    if (side_select && i >= 2) CK(cudaStreamWaitEvent(st, c->ev_sel[(i - 2) % kRing], 0));
     const float* q32 = stage_q(c, slot, q[i], q_dtype, io_device, st, i, n);
     kc_topn_out& o = outs[i];
     // Offloaded layer in DMA mode: compact the selected rows on the host (pool
@@ -560,8 +575,8 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
     const bool cand = (c->select_cand == 1 || (c->select_cand == 0 && g.s > kc::kDenseRegMaxS)) &&
                       !c->select_global && kc::score_cand_supported(c->dtype, (int)c->h, (int)c->G, g.chunk, g.nc);
     if (cand) {
-      c->cand.ensure(checked_mul({c->rows, (uint64_t)c->lstride, 8}));
-      c->cand_meta.ensure(checked_mul({c->rows, (uint64_t)c->max_splits, 8}));
+      c->cand.ensure(2 * checked_mul({c->rows, (uint64_t)c->lstride, 8}));
+      c->cand_meta.ensure(2 * checked_mul({c->rows, (uint64_t)c->max_splits, 8}));
       c->fb_flags.ensure(c->rows * 4);
     }
     const int gsz = (int)((c->rows + n_groups - 1) / n_groups);
@@ -569,12 +584,17 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
       const int r0 = gi * gsz;
       const int nr = std::min<int>(gsz, (int)c->rows - r0);
       if (nr <= 0) break;
-      enqueue_score(c, layer, q32, g, st, r0, nr, cand);
-      if (gi == 0 && i >= (uint64_t)kRing && side != st) CK(cudaStreamWaitEvent(st, c->ev_rec[slot], 0));
+      enqueue_score(c, layer, q32, g, st, r0, nr, cand, lb);
+      if (side_select) {
+        CK(cudaEventRecord(c->ev_scored[slot], st));
+        CK(cudaStreamWaitEvent(side, c->ev_scored[slot], 0));
+      } else if (gi == 0 && i >= (uint64_t)kRing && side != st) {
+        CK(cudaStreamWaitEvent(st, c->ev_rec[slot], 0));
+      }
 
       kc::SelectParams sp{};
-      sp.logits = c->logits.as<float>();
-      sp.partials = c->partials.as<float2>();
+      sp.logits = c->logits_buf(lb);
+      sp.partials = c->partials_buf(lb);
       sp.keys = c->keys.as<uint32_t>();
       sp.idx = c->idx[slot].as<uint32_t>();
       sp.w = c->w[slot].as<float>();
@@ -593,8 +613,8 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
       sp.force_global = c->select_global;
       sp.keep_logits = c->keep_logits;
       if (cand) {
-        sp.cand = c->cand.as<uint2>();
-        sp.cand_meta = c->cand_meta.as<uint2>();
+        sp.cand = c->cand_buf(lb);
+        sp.cand_meta = c->cand_meta_buf(lb);
         sp.fb_flags = c->fb_flags.as<uint32_t>();
         sp.chunk = g.chunk;
         sp.k = c->k_layer(layer);
@@ -605,15 +625,15 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
         sp.scale = 1.0f / std::sqrt(static_cast<float>(c->h));  // attention.hpp:15-17
         sp.force_fallback = c->cand_force_fallback;
       }
-      c->timed(1, st, [&] {
+      c->timed(1, selst, [&] {
         if (!cand) {
-          kc::select_launch(sp, st);
-        } else if (!kc::select_cand_launch(sp, st)) {
+          kc::select_launch(sp, selst);
+        } else if (!kc::select_cand_launch(sp, selst)) {
           fail(KC_ECUDA, "candidate selection unavailable for this shape");
         }
       });
-      CK(cudaEventRecord(c->ev_sel[slot], st));
-      if (side != st) CK(cudaStreamWaitEvent(side, c->ev_sel[slot], 0));
+      CK(cudaEventRecord(c->ev_sel[slot], selst));
+      if (side != selst) CK(cudaStreamWaitEvent(side, c->ev_sel[slot], 0));
 
       kc::RecallParams rp{};
       rp.v = c->v_layer(layer);
@@ -798,8 +818,10 @@ int kc_cache_create(const kc_config* cfg, uint64_t batch, uint64_t resident_laye
       c->lstride = (int64_t)((cfg->max_seq + 31) & ~31ull);
       c->kstride = c->lstride;
       c->max_splits = (int)((cfg->max_seq + 63) / 64);
-      c->logits.ensure(checked_mul({batch, c->n_q, (uint64_t)c->lstride, 4}));
-      c->partials.ensure(checked_mul({batch, c->n_q, (uint64_t)c->max_splits, 8}));
+      // two scoring buffers: scoring of layer i+1 writes one while the
+      // selection of layer i reads the other (selection on the side stream)
+      c->logits.ensure(2 * checked_mul({batch, c->n_q, (uint64_t)c->lstride, 4}));
+      c->partials.ensure(2 * checked_mul({batch, c->n_q, (uint64_t)c->max_splits, 8}));
       c->keys.ensure(checked_mul({c->rows, (uint64_t)c->kstride, 4}));
       int lo = 0, hi = 0;
       CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
@@ -810,6 +832,7 @@ int kc_cache_create(const kc_config* cfg, uint64_t batch, uint64_t resident_laye
       CK(cudaEventCreateWithFlags(&c->ev_end, cudaEventDisableTiming));
       for (int i = 0; i < kRing; ++i) {
         CK(cudaEventCreateWithFlags(&c->ev_sel[i], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&c->ev_scored[i], cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&c->ev_rec[i], cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&c->ev_gath[i], cudaEventDisableTiming));
       }
@@ -1125,6 +1148,7 @@ int kc_set_tuning(kc_cache* c, const char* key, int64_t value) {
     else if (k == "recall_ctas") c->recall_ctas = (int)value;
     else if (k == "keep_logits") c->keep_logits = value ? 1 : 0;
     else if (k == "full_fused") c->full_fused = value ? 1 : 0;
+    else if (k == "select_on_side") c->select_on_side = value ? 1 : 0;
     else if (k == "select_cand") {
       if (value < 0 || value > 2) fail(KC_EARG, "select_cand: 0 auto, 1 on, 2 off");
       c->select_cand = (int)value;

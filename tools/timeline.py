@@ -24,6 +24,8 @@ def main():
     ap.add_argument("--s", type=int, default=32768)
     ap.add_argument("--topn", type=int, default=128)
     ap.add_argument("--tune", action="append", default=[])
+    ap.add_argument("--steps", type=int, default=1)
+    ap.add_argument("--verbose", action="store_true")
     args = ap.parse_args()
     L, b, n, n_kv, h, s, N = args.layers, args.batch, args.heads, args.kv, 128, args.s, args.topn
     d = n * h
@@ -55,17 +57,23 @@ def main():
     for _ in range(3):
         cache.decode_topn_layers_device(list(range(L)), qs, N, outs)
     torch.cuda.synchronize()
-    cache.profile(True)
-    cache.decode_topn_layers_device(list(range(L)), qs, N, outs)
-    torch.cuda.synchronize()
-    sp = {k: cache.profile_spans(k) for k in ("score", "select", "recall")}
-    t0 = sp["score"][0][0]
-    print("layer   score(start-end)      select(start-end)     recall(start-end)   [us]")
-    for l in range(L):
-        row = [f"{(a - t0) * 1e3:8.1f}-{(e - t0) * 1e3:8.1f}" for a, e in (sp[k][l] for k in ("score", "select", "recall"))]
-        print(f"{l:5d}  " + "   ".join(row))
-    end = max(e for k in sp for _, e in sp[k])
-    print(f"step span {(end - t0) * 1e3:.1f} us, per layer {(end - t0) * 1e3 / L:.1f} us")
+    ap_steps = args.steps
+    for step in range(ap_steps):
+        cache.profile(True)
+        cache.decode_topn_layers_device(list(range(L)), qs, N, outs)
+        torch.cuda.synchronize()
+        sp = {k: cache.profile_spans(k) for k in ("score", "select", "recall")}
+        cache.profile(False)
+        t0 = sp["score"][0][0]
+        end = max(e for k in sp for _, e in sp[k])
+        if args.verbose or step == 0:
+            print("layer   score(start-end)      select(start-end)     recall(start-end)   [us]")
+            for l in range(L):
+                row = [f"{(a - t0) * 1e3:8.1f}-{(e - t0) * 1e3:8.1f}" for a, e in (sp[k][l] for k in ("score", "select", "recall"))]
+                print(f"{l:5d}  " + "   ".join(row))
+        dur = {k: sum(e - a for a, e in sp[k]) / L * 1e3 for k in sp}
+        print(f"step {step}: span {(end - t0) * 1e3:.1f} us, per layer {(end - t0) * 1e3 / L:.1f} us; mean durations "
+              + ", ".join(f"{k} {v:.1f}" for k, v in dur.items()), flush=True)
 
 
 if __name__ == "__main__":

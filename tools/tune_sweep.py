@@ -31,6 +31,7 @@ def main():
     ap.add_argument("--resident", type=int, default=0, help="V-resident layers (0 = all offloaded)")
     ap.add_argument("--run-layers", default="", help="comma list: decode only these layers (default all)")
     ap.add_argument("--profile", action="store_true", help="also print per-kernel event times (perturbs overlap)")
+    ap.add_argument("--per-step", action="store_true", help="print every step's time")
     args = ap.parse_args()
     L, b, n, n_kv, h, s, N = args.layers, args.batch, args.heads, args.kv, 128, args.s, args.topn
     d = n * h
@@ -69,16 +70,18 @@ def main():
         for _ in range(3):
             cache.decode_topn_layers_device(run, qs, N, outs, stream=stream)
         torch.cuda.synchronize()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(args.steps):
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+        evs[0].record(stream)
+        for i in range(args.steps):
             cache.decode_topn_layers_device(run, qs, N, outs, stream=stream)
-        e1.record(stream)
+            evs[i + 1].record(stream)
         torch.cuda.synchronize()
-        ms = e0.elapsed_time(e1) / args.steps
+        ms = evs[0].elapsed_time(evs[-1]) / args.steps
+        per_step = [round(evs[i].elapsed_time(evs[i + 1]), 2) for i in range(args.steps)]
         rec = {"tune": dict(zip(keys, combo)), "step_ms": round(ms, 4), "per_layer_us": round(1e3 * ms / len(run), 1),
                "k_only_gbs": round(k_bytes / (ms * 1e-3) / 1e9, 1)}
+        if args.per_step:
+            rec["per_step_ms"] = per_step
         if args.profile:
             cache.profile(True)
             for _ in range(2):
