@@ -30,10 +30,10 @@ METRICS = [
 ]
 
 
-def raw_metrics(rep):
+def raw_metrics(rep, launch=0):
     txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(txt)))
-    hdr, units, vals = rows[0], rows[1], rows[2]
+    hdr, units, vals = rows[0], rows[1], rows[2 + launch]
     out = {}
     for m in METRICS:
         if m in hdr:
@@ -75,14 +75,23 @@ def main():
                 f.write(f"{k},{n},{t:.1f},{t / n:.1f},{t / total:.3f}\n")
         print(open(os.path.join(PROF, f"{tag}_launches.csv")).read())
     summary = {}
-    for k in ("score_fast", "select_reg", "recall_pv"):
-        rep = os.path.join(OUT, f"prof_{k}.ncu-rep")
+    captures = [("score_fast", "prof_score_fast", 0, "python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --no-full-kv (C2)"),
+                ("select_reg", "prof_select_reg", 0, "same (C2)"),
+                ("recall_pv", "prof_recall_pv", 0, "same (C2)"),
+                ("full_fast", "prof_full_fast", 0, "python bench.py ... (C2 full-KV comparator leg, K+V in HBM)"),
+                ("score_fast_cand64k", "prof_cand64k", 0, "python tools/c5_crossover.py --contexts 65536 --topns 128 --layers 2"),
+                ("select_cand64k", "prof_cand64k", 1, "same (64k, N=128)")]
+    for k, repname, launch, cmd in captures:
+        rep = os.path.join(OUT, f"{repname}.ncu-rep")
         if not os.path.exists(rep):
             continue
-        m = raw_metrics(rep)
+        try:
+            m = raw_metrics(rep, launch)
+        except IndexError:
+            continue
         with open(os.path.join(PROF, f"{tag}_ncu_{k}.txt"), "w") as f:
             f.write(f"# ncu --set full --clock-control none, one launch of {m['kernel']}\n")
-            f.write("# command: python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e (C2)\n")
+            f.write(f"# command: {cmd}\n")
             for key in METRICS:
                 if key in m:
                     f.write(f"{key} = {m[key][0]} {m[key][1]}\n")
