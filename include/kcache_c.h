@@ -125,6 +125,32 @@ int kc_decode_topn_layers(kc_cache* cache, uint64_t n, const uint64_t* layers,
 int kc_decode_full(kc_cache* cache, uint64_t layer, const void* q, int q_dtype, uint32_t flags,
                    float* out, void* stream);
 
+/* Engine::forward_decode's attention block for one layer
+ * (proj/core/src/engine.cpp:139-160): append this step's K/V rows (k_new,
+ * v_new: [batch][n_kv_heads*head_dim] of `dtype`; an offloaded layer's new V
+ * goes to the pinned arena with the D2H ledger event, kv_cache.cpp:107-112),
+ * then decode_attention_topn -- or decode_attention_full with KC_FULL -- with
+ * q ([batch][n_heads*head_dim] of `dtype`), writing out [batch][d_model].
+ * TopN calls accumulate the step statistics (StepStats, engine.hpp:37-45)
+ * on the device: H2D bytes, the dropped mass summed over the selections in
+ * slot order, and the 8-bin histogram of selected positions
+ * (bin = min(7, idx*8/len), engine.cpp:150-156). KC_IO_DEVICE: q, k_new,
+ * v_new and out are device pointers and the call is asynchronous. */
+#define KC_FULL 8u
+#define KC_POSITION_HISTOGRAM_BINS 8
+typedef struct kc_step_stats {
+  uint64_t h2d_bytes;
+  uint64_t d2h_bytes;
+  uint64_t selections;     /* dropped-mass terms summed (q-head slots x TopN layers) */
+  double dropped_sum;      /* mean_dropped_mass = dropped_sum / selections */
+  uint64_t position_histogram[KC_POSITION_HISTOGRAM_BINS];
+} kc_step_stats;
+int kc_decode_step(kc_cache* cache, uint64_t layer, const void* q, const void* k_new, const void* v_new,
+                   int dtype, uint64_t top_n, uint32_t flags, float* out, void* stream);
+/* Statistics accumulated by kc_decode_step since the last reset (waits for
+ * the cache's queued work); reset != 0 starts a new step. */
+int kc_step_stats_read(kc_cache* cache, kc_step_stats* out, int reset);
+
 /* Full softmax rows of every (batch, q head) -- the ScoreObserver debug path
  * (attention.hpp:34-35, attention.cpp:137-139): probs [batch*n_heads][len]
  * fp32, host. Not on the hot path. */

@@ -303,6 +303,35 @@ Matrix decode_attention_full(const Matrix& q, const TieredKVCache& cache, std::s
   return out;
 }
 
+Matrix decode_step_attention(const Matrix& q, const Matrix& k_rows, const Matrix& v_rows,
+                             TieredKVCache& cache, std::size_t layer, bool use_topn,
+                             std::size_t top_n, bool renormalize) {
+  if (use_topn && top_n == 0) throw std::invalid_argument("decode_attention_topn: top_n must be >= 1");
+  const std::size_t width = cache.config().kv_heads() * cache.config().head_dim;
+  if (k_rows.cols != width || v_rows.cols != width)
+    throw ShapeError("append_kv: row width must equal d_model");
+  if (k_rows.rows != cache.batch() || v_rows.rows != cache.batch())
+    throw ShapeError("append_kv: need a positive multiple of batch rows for K and V");
+  if (q.rows != cache.batch() || q.cols != cache.config().d_model)
+    throw ShapeError("decode attention: q must be batch x d_model");
+  Matrix out(q.rows, q.cols);
+  const std::uint32_t flags = (renormalize ? KC_RENORMALIZE : 0u) | (use_topn ? 0u : KC_FULL);
+  check(kc_decode_step(cache.handle(), layer, q.data.data(), k_rows.data.data(), v_rows.data.data(), KC_F32,
+                       top_n, flags, out.data.data(), nullptr));
+  return out;
+}
+
+StepStats read_step_stats(TieredKVCache& cache) {
+  kc_step_stats s{};
+  check(kc_step_stats_read(cache.handle(), &s, 1));
+  StepStats out;
+  out.h2d_bytes = s.h2d_bytes;
+  out.d2h_bytes = s.d2h_bytes;
+  out.mean_dropped_mass = s.selections ? s.dropped_sum / static_cast<double>(s.selections) : 0.0;
+  for (std::size_t i = 0; i < kPositionHistogramBins; ++i) out.position_histogram[i] = s.position_histogram[i];
+  return out;
+}
+
 TopNResult decode_attention_topn(const Matrix& q, TieredKVCache& cache, std::size_t layer,
                                  std::size_t top_n, bool renormalize, bool ordered_accumulation,
                                  const ScoreObserver& observer) {

@@ -167,6 +167,8 @@ struct kc_cache {
   DevBuf logits, partials, keys, part_out, stage_src, stage_k, stage_v, sel_rows, sel_pos, gather_out;
   DevBuf cand, cand_meta, fb_flags;  // candidate-mode selection scratch
   DevBuf part_ml;                    // fused full attention: split (m, l)
+  DevBuf step_dev;                   // kc_decode_step: StepStatsDev accumulator
+  kc_step_stats step_host{};         // kc_decode_step: host-known counters
   DevBuf q32[kRing], idx[kRing], w[kRing], dropped[kRing], norm[kRing], out_tmp[kRing], idx_exp[kRing];
   PinnedBuf host_in, host_out;
   // DMA recall: pinned copy of the selection, pinned compacted rows, HBM copy
@@ -326,7 +328,7 @@ void destroy(kc_cache* c) {
   }
   for (DevBuf* b : {&c->logits, &c->partials, &c->keys, &c->part_out, &c->stage_src, &c->stage_k,
                     &c->stage_v, &c->sel_rows, &c->sel_pos, &c->gather_out, &c->cand, &c->cand_meta,
-                    &c->fb_flags, &c->part_ml})
+                    &c->fb_flags, &c->part_ml, &c->step_dev})
     b->release();
   for (int i = 0; i < kRing; ++i) {
     c->q32[i].release(); c->idx[i].release(); c->w[i].release(); c->dropped[i].release();
@@ -904,6 +906,77 @@ int kc_decode_topn(kc_cache* c, uint64_t layer, const void* q, int q_dtype, uint
     if (!out || !q) fail(KC_EARG, "kc_decode_topn: null argument");
     const void* qs[1] = {q};
     decode_topn_impl(c, 1, &layer, qs, q_dtype, top_n, flags, out, (cudaStream_t)stream);
+  });
+}
+
+int kc_decode_step(kc_cache* c, uint64_t layer, const void* q, const void* k_new, const void* v_new,
+                   int dtype, uint64_t top_n, uint32_t flags, float* out, void* stream) {
+  return guarded([&] {
+    if (!q || !k_new || !v_new || !out) fail(KC_EARG, "kc_decode_step: null argument");
+    const size_t esz = dtype_size(dtype);
+    if (!(flags & KC_FULL) && top_n == 0) fail(KC_EARG, "decode_attention_topn: top_n must be >= 1");
+    const bool io_device = flags & KC_IO_DEVICE;
+    set_dev(c);
+    cudaStream_t st = io_device ? (cudaStream_t)stream : c->main_st;
+    // engine.cpp:143 -- this step's K/V row of every batch row
+    const uint64_t rows = c->batch;
+    append_checks(c, layer, rows);
+    const uint64_t d2h0 = c->d2h_total;
+    const void* ks = k_new;
+    const void* vs = v_new;
+    if (!io_device) {
+      const size_t bytes = rows * c->dkv * esz;
+      c->stage_k.ensure(bytes);
+      c->stage_v.ensure(bytes);
+      CK(cudaMemcpyAsync(c->stage_k.p, k_new, bytes, cudaMemcpyHostToDevice, st));
+      CK(cudaMemcpyAsync(c->stage_v.p, v_new, bytes, cudaMemcpyHostToDevice, st));
+      ks = c->stage_k.p;
+      vs = c->stage_v.p;
+    }
+    enqueue_append(c, layer, ks, vs, dtype, rows, st);
+    append_account(c, layer, rows);
+    c->step_host.d2h_bytes += c->d2h_total - d2h0;
+    if (flags & KC_FULL) {
+      const int rc = kc_decode_full(c, layer, q, dtype, flags & KC_IO_DEVICE, out, st);
+      if (rc != KC_OK) fail(rc, kc_last_error());
+      return;
+    }
+    kc_topn_out o{};
+    o.out = out;
+    const void* qs[1] = {q};
+    decode_topn_impl(c, 1, &layer, qs, dtype, top_n, flags & (KC_RENORMALIZE | KC_IO_DEVICE), &o, st);
+    // engine.cpp:146-156 on the device: ring slot 0 holds this call's selection
+    const uint64_t slots = c->batch * c->n_q;
+    if (!c->step_dev.p) {
+      c->step_dev.ensure(sizeof(kc::StepStatsDev));
+      CK(cudaMemsetAsync(c->step_dev.p, 0, sizeof(kc::StepStatsDev), st));
+    }
+    kc::step_stats_launch(c->idx[0].as<uint32_t>(), c->dropped[0].as<double>(), (int)c->rows, (int)c->G,
+                          (int)o.nc, c->current_len(), (int)slots,
+                          static_cast<kc::StepStatsDev*>(c->step_dev.p), st);
+    CK(cudaGetLastError());
+    c->step_host.h2d_bytes += o.h2d_bytes;
+    c->step_host.selections += slots;
+    if (!io_device) CK(cudaStreamSynchronize(st));
+  });
+}
+
+int kc_step_stats_read(kc_cache* c, kc_step_stats* out, int reset) {
+  return guarded([&] {
+    if (!out) fail(KC_EARG, "kc_step_stats_read: null argument");
+    set_dev(c);
+    CK(cudaStreamSynchronize(c->main_st));
+    CK(cudaStreamSynchronize(c->side_st));
+    CK(cudaDeviceSynchronize());
+    kc::StepStatsDev d{};
+    if (c->step_dev.p) CK(cudaMemcpy(&d, c->step_dev.p, sizeof d, cudaMemcpyDeviceToHost));
+    *out = c->step_host;
+    out->dropped_sum = d.dropped_sum;
+    for (int i = 0; i < KC_POSITION_HISTOGRAM_BINS; ++i) out->position_histogram[i] = d.hist[i];
+    if (reset) {
+      c->step_host = kc_step_stats{};
+      if (c->step_dev.p) CK(cudaMemset(c->step_dev.p, 0, sizeof(kc::StepStatsDev)));
+    }
   });
 }
 

@@ -124,6 +124,14 @@ struct RecallParams {
 };
 void recall_launch(const RecallParams& p, int dtype, cudaStream_t st);
 
+// StepStats accumulation of one TopN layer call (engine.cpp:146-156)
+struct StepStatsDev {
+  double dropped_sum;
+  unsigned long long hist[8];
+};
+void step_stats_launch(const uint32_t* idx, const double* dropped, int rows, int G, int nc, uint64_t len,
+                       int slots, StepStatsDev* acc, cudaStream_t st);
+
 struct PvFullParams {
   const void* v;          // [rows][max_seq][h]
   const float* logits;

@@ -314,7 +314,37 @@ int grid_for(int64_t n) {
   return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 8));
 }
 
+// One CTA: the histogram of this call's selected positions (each kv-row
+// index set counts once per q head of its group, like the reference's per-slot
+// loop) and the dropped mass added in slot order after the running sum of
+// the previous layers -- the reference's accumulation order, so the double
+// sum is reproducible.
+__global__ void step_stats_kernel(const uint32_t* idx, const double* dropped, int rows, int G, int nc,
+                                  uint64_t len, int slots, StepStatsDev* acc) {
+  __shared__ unsigned long long hist[8];
+  if (threadIdx.x < 8) hist[threadIdx.x] = 0ull;
+  __syncthreads();
+  const int64_t n = (int64_t)rows * nc;
+  for (int64_t e = threadIdx.x; e < n; e += blockDim.x) {
+    const uint64_t q8 = (uint64_t)idx[e] * 8ull / len;
+    const uint64_t bin = q8 < 7ull ? q8 : 7ull;
+    atomicAdd(&hist[bin], (unsigned long long)G);
+  }
+  __syncthreads();
+  if (threadIdx.x < 8) acc->hist[threadIdx.x] += hist[threadIdx.x];
+  if (threadIdx.x == 0) {
+    double s = acc->dropped_sum;
+    for (int i = 0; i < slots; ++i) s += dropped[i];
+    acc->dropped_sum = s;
+  }
+}
+
 }  // namespace
+
+void step_stats_launch(const uint32_t* idx, const double* dropped, int rows, int G, int nc, uint64_t len,
+                       int slots, StepStatsDev* acc, cudaStream_t st) {
+  step_stats_kernel<<<1, 256, 0, st>>>(idx, dropped, rows, G, nc, len, slots, acc);
+}
 
 void recall_launch(const RecallParams& p, int dtype, cudaStream_t st) {
   const size_t esz = dtype == KC_F32 ? 4 : 2;

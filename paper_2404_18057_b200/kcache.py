@@ -32,7 +32,7 @@ LIB_PATH = os.path.join(_HERE, "libkcache_b200.so")
 
 KC_OK, KC_ESHAPE, KC_ESTATE, KC_ECAPACITY, KC_EARG, KC_ERANGE, KC_ECUDA, KC_EOVERFLOW = range(8)
 KC_F32, KC_F16, KC_BF16 = 0, 1, 2
-KC_RENORMALIZE, KC_REVERSE_ACCUM, KC_IO_DEVICE = 1, 2, 4
+KC_RENORMALIZE, KC_REVERSE_ACCUM, KC_IO_DEVICE, KC_FULL = 1, 2, 4, 8
 DTYPES = {"f32": KC_F32, "f16": KC_F16, "bf16": KC_BF16}
 
 
@@ -61,6 +61,11 @@ class _TopnOut(C.Structure):
                 ("dropped_mass", C.c_void_p), ("nc", C.c_uint64), ("h2d_bytes", C.c_uint64)]
 
 
+class _StepStats(C.Structure):
+    _fields_ = [("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64), ("selections", C.c_uint64),
+                ("dropped_sum", C.c_double), ("position_histogram", C.c_uint64 * 8)]
+
+
 _lib = None
 
 
@@ -86,6 +91,8 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         "kc_decode_topn": (i32, [vp, u64, vp, i32, u64, u32, C.POINTER(_TopnOut), vp]),
         "kc_decode_topn_layers": (i32, [vp, u64, p64, C.POINTER(vp), i32, u64, u32, C.POINTER(_TopnOut), vp]),
         "kc_decode_full": (i32, [vp, u64, vp, i32, u32, vp, vp]),
+        "kc_decode_step": (i32, [vp, u64, vp, vp, vp, i32, u64, u32, vp, vp]),
+        "kc_step_stats_read": (i32, [vp, C.POINTER(_StepStats), i32]),
         "kc_score_probs": (i32, [vp, u64, vp, i32, vp]),
         "kc_gather_v": (i32, [vp, u64, vp, vp, vp, p64]),
         "kc_read_row": (i32, [vp, u64, u64, u64, i32, vp]),
@@ -479,6 +486,40 @@ class TieredKVCache:
         dt = {torch.float32: KC_F32, torch.float16: KC_F16, torch.bfloat16: KC_BF16}[q.dtype]
         st = stream.cuda_stream if stream is not None else torch.cuda.current_stream().cuda_stream
         _check(self._lib.kc_decode_full(self._h, layer, q.data_ptr(), dt, KC_IO_DEVICE, out.data_ptr(), st))
+
+    # ---- engine decode-step attention block (engine.cpp:139-160) ----
+    def decode_step(self, layer: int, q, k_new, v_new, top_n: int, renormalize: bool = False,
+                    full: bool = False) -> np.ndarray:
+        """Append this step's K/V rows ([batch, kv_width] host fp32) to `layer`
+        and run its attention (TopN, or full with full=True) for host q;
+        returns out [batch, d_model]. TopN calls accumulate step_stats()."""
+        q, k_new, v_new = _f32(q), _f32(k_new), _f32(v_new)
+        if k_new.shape != (self.batch, self.kv_width) or v_new.shape != k_new.shape:
+            raise ShapeError("append_kv: row width must equal d_model")
+        out = np.zeros((self.batch, self.config.d_model), np.float32)
+        flags = (KC_RENORMALIZE if renormalize else 0) | (KC_FULL if full else 0)
+        _check(self._lib.kc_decode_step(self._h, layer, _ptr(q), _ptr(k_new), _ptr(v_new), KC_F32, top_n,
+                                        flags, _ptr(out), None))
+        return out
+
+    def decode_step_device(self, layer: int, q, k_new, v_new, out, top_n: int, renormalize: bool = False,
+                           full: bool = False, stream=None) -> None:
+        """Same with device torch tensors (one dtype for q / k_new / v_new), asynchronous."""
+        import torch
+        dt = {torch.float32: KC_F32, torch.float16: KC_F16, torch.bfloat16: KC_BF16}[q.dtype]
+        flags = KC_IO_DEVICE | (KC_RENORMALIZE if renormalize else 0) | (KC_FULL if full else 0)
+        st = stream.cuda_stream if stream is not None else torch.cuda.current_stream().cuda_stream
+        _check(self._lib.kc_decode_step(self._h, layer, q.data_ptr(), k_new.data_ptr(), v_new.data_ptr(), dt,
+                                        top_n, flags, out.data_ptr(), st))
+
+    def step_stats(self, reset: bool = True) -> dict:
+        """StepStats (engine.hpp:37-45) accumulated by decode_step since the last reset."""
+        st = _StepStats()
+        _check(self._lib.kc_step_stats_read(self._h, C.byref(st), 1 if reset else 0))
+        return {"h2d_bytes": st.h2d_bytes, "d2h_bytes": st.d2h_bytes, "selections": st.selections,
+                "dropped_sum": st.dropped_sum,
+                "mean_dropped_mass": st.dropped_sum / st.selections if st.selections else 0.0,
+                "position_histogram": list(st.position_histogram)}
 
     def decode_topn_layers_host(self, layers: Sequence[int], qs: Sequence[np.ndarray], top_n: int,
                                 outs: Sequence[dict], renormalize=False) -> list:

@@ -195,8 +195,48 @@ static void arg_topk_cases() {
   CHECK_THROWS_AS(arg_topk(vals, 0), std::invalid_argument);
 }
 
+// Engine::forward_decode's attention block (engine.cpp:139-160) as one call:
+// append + TopN/full + StepStats; the output equals a separate
+// append_kv + decode_attention_topn on an identical cache.
+static void engine_step_cases() {
+  const ModelConfig c = small_config(2, 64, 4);
+  SeededRng rng(21);
+  const std::size_t s = 40, batch = 2, N = 8;
+  const Matrix k = random_matrix(s * batch, c.d_model, rng);
+  const Matrix v = random_matrix(s * batch, c.d_model, rng);
+  TieredKVCache a = make_cache(c, batch, 1, k, v);
+  TieredKVCache b = make_cache(c, batch, 1, k, v);
+  read_step_stats(a);
+  for (std::size_t layer = 0; layer < c.n_layers; ++layer) {
+    const Matrix kr = random_matrix(batch, c.d_model, rng);
+    const Matrix vr = random_matrix(batch, c.d_model, rng);
+    const Matrix q = random_matrix(batch, c.d_model, rng);
+    const bool topn = layer >= 1;
+    const Matrix got = decode_step_attention(q, kr, vr, a, layer, topn, N, false);
+    b.append_kv(layer, kr, vr);
+    if (topn) {
+      const TopNResult want = decode_attention_topn(q, b, layer, N, false);
+      CHECK(got.data == want.out.data);
+    } else {
+      CHECK(got.data == decode_attention_full(q, b, layer).data);
+    }
+  }
+  const StepStats st = read_step_stats(a);
+  CHECK(st.h2d_bytes == 2ull * batch * c.n_heads * N * c.head_dim);
+  CHECK(st.d2h_bytes == 2ull * batch * c.d_model);  // layer 1's new V row goes to the slow tier
+  std::uint64_t total = 0;
+  for (auto x : st.position_histogram) total += x;
+  CHECK(total == batch * c.n_heads * N);
+  CHECK(st.mean_dropped_mass > 0.0 && st.mean_dropped_mass < 1.0);
+  CHECK(a.current_len() == s + 1);
+  CHECK_THROWS_AS(decode_step_attention(random_matrix(batch, c.d_model, rng), random_matrix(batch, 16, rng),
+                                        random_matrix(batch, c.d_model, rng), a, 0, true, N, false),
+                  ShapeError);
+}
+
 int main() {
   hand_checkable();
+  engine_step_cases();
   topn_equals_full();
   h2d_accounting_and_errors();
   kv_cache_cases();
