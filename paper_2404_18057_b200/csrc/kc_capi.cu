@@ -192,7 +192,7 @@ struct kc_cache {
   int score_ctas_per_sm = 0;
   int host_frac_pct = 50;  // hybrid recall: % of rows gathered by host threads
   int auto_recall_mode = kRecallZeroCopy;  // what recall_mode 0 resolves to
-  int score_groups = 1;   // row groups per layer (score -> select -> recall each)
+  int score_groups = 0;   // row groups per layer (score -> select -> recall each); 0 = auto
   int k_policy = 0;        // L2 policy of the K stream (kc_device.cuh l2_policy)
   // MHA candidate selection: 0 auto (rows longer than the register-resident
   // dense select), 1 always, 2 never
@@ -569,7 +569,11 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
     // Row groups: score -> select -> recall per group of (batch, kv head)
     // rows, so only one group's fp32 logits are live in L2 at a time (the L2
     // keeps the GPU page-table lines the zero-copy recall walks).
-    const int n_groups = dma ? 1 : (int)std::max<int64_t>(1, std::min<int64_t>(c->score_groups, (int64_t)c->rows));
+    // score_groups 0 = auto: one group when layers pipeline against each
+    // other, two for a single-layer call (the engine's per-layer block),
+    // where only the intra-layer overlap is available (r01: 730 -> 690 us)
+    const int64_t want_groups = c->score_groups > 0 ? c->score_groups : (n == 1 ? 2 : 1);
+    const int n_groups = dma ? 1 : (int)std::max<int64_t>(1, std::min<int64_t>(want_groups, (int64_t)c->rows));
     // Candidate mode (MHA): scoring emits only each split's possible top-N
     // positions instead of 4 B of fp32 logit per position -- the dense logits
     // (32 MiB per C2 layer) would evict the GPU page-table lines the zero-copy
@@ -1229,7 +1233,7 @@ int kc_set_tuning(kc_cache* c, const char* key, int64_t value) {
     else if (k == "k_policy") c->k_policy = (int)value;
     else if (k == "cand_force_fallback") c->cand_force_fallback = value ? 1 : 0;
     else if (k == "score_groups") {
-      if (value < 1) fail(KC_EARG, "score_groups must be >= 1");
+      if (value < 0) fail(KC_EARG, "score_groups must be >= 0 (0 = auto)");
       c->score_groups = (int)value;
     }
     else if (k == "host_frac_pct") {

@@ -321,17 +321,27 @@ int grid_for(int64_t n) {
 // sum is reproducible.
 __global__ void step_stats_kernel(const uint32_t* idx, const double* dropped, int rows, int G, int nc,
                                   uint64_t len, int slots, StepStatsDev* acc) {
-  __shared__ unsigned long long hist[8];
-  if (threadIdx.x < 8) hist[threadIdx.x] = 0ull;
+  __shared__ unsigned int hist[8];
+  if (threadIdx.x < 8) hist[threadIdx.x] = 0u;
   __syncthreads();
+  // per-thread counts, then one shared atomic per warp and bin
+  unsigned int mine[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   const int64_t n = (int64_t)rows * nc;
   for (int64_t e = threadIdx.x; e < n; e += blockDim.x) {
     const uint64_t q8 = (uint64_t)idx[e] * 8ull / len;
-    const uint64_t bin = q8 < 7ull ? q8 : 7ull;
-    atomicAdd(&hist[bin], (unsigned long long)G);
+    const unsigned b = q8 < 7ull ? (unsigned)q8 : 7u;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) mine[k] += (b == (unsigned)k) ? 1u : 0u;
+  }
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    unsigned v = mine[k];
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(&hist[k], v);
   }
   __syncthreads();
-  if (threadIdx.x < 8) acc->hist[threadIdx.x] += hist[threadIdx.x];
+  if (threadIdx.x < 8) acc->hist[threadIdx.x] += (unsigned long long)hist[threadIdx.x] * (unsigned long long)G;
   if (threadIdx.x == 0) {
     double s = acc->dropped_sum;
     for (int i = 0; i < slots; ++i) s += dropped[i];
@@ -343,7 +353,7 @@ __global__ void step_stats_kernel(const uint32_t* idx, const double* dropped, in
 
 void step_stats_launch(const uint32_t* idx, const double* dropped, int rows, int G, int nc, uint64_t len,
                        int slots, StepStatsDev* acc, cudaStream_t st) {
-  step_stats_kernel<<<1, 256, 0, st>>>(idx, dropped, rows, G, nc, len, slots, acc);
+  step_stats_kernel<<<1, 1024, 0, st>>>(idx, dropped, rows, G, nc, len, slots, acc);
 }
 
 void recall_launch(const RecallParams& p, int dtype, cudaStream_t st) {

@@ -16,7 +16,7 @@ from tests.test_gpu_parity import build_cache, compare_all
 
 pytestmark = pytest.mark.gpu
 
-DEFAULTS = {"select_cand": 0, "cand_force_fallback": 0, "score_groups": 1, "recall_mode": 0, "score_chunk": 0}
+DEFAULTS = {"select_cand": 0, "cand_force_fallback": 0, "score_groups": 0, "recall_mode": 0, "score_chunk": 0}
 
 
 def _run(kc, cache, q, N, renorm=False, **tune):
