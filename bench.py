@@ -240,8 +240,20 @@ def run_ours(args, cfg):
     nc = min(N, s)
     slots = b * n
     mcfg = kc.ModelConfig(L, d, n, h, kc.ModelConfig.default_ffn_hidden(d), 32000, s, n_kv)
+    # every rank pins its own V shard (C2: 64 GiB): refuse cleanly rather than
+    # drive the host out of memory when the node cannot hold all shards
+    from paper_2404_18057_b200.sharding import gpu_numa_node, host_mem_available
+    local_world = int(os.environ.get("LOCAL_WORLD_SIZE", world))
+    v_bytes_rank = 2 * L * b * n_kv * s * h
+    avail = host_mem_available()
+    if avail and local_world * v_bytes_rank > 0.92 * avail:
+        if rank == 0:
+            print(json.dumps({"metric": METRIC, "error": "host memory: %d ranks x %.1f GiB pinned V shards exceed "
+                              "MemAvailable %.1f GiB" % (local_world, v_bytes_rank / 2**30, avail / 2**30)}))
+        sys.exit(3)
+    numa = gpu_numa_node(local_rank)
     t0 = time.time()
-    cache = kc.TieredKVCache(mcfg, b, kc.TierPlacement.kcache(0, L, 2, "f16"), device=local_rank)
+    cache = kc.TieredKVCache(mcfg, b, kc.TierPlacement.kcache(0, L, 2, "f16"), device=local_rank, numa_node=numa)
     for kv in args.tune:
         key, val = kv.split("=")
         cache.set_tuning(key, int(val))
@@ -396,7 +408,8 @@ def run_ours(args, cfg):
         "config": {"workload": cfg["workload"], "config": args.config, "layers": L, "batch_per_gpu": b,
                    "global_batch": b * world, "n_heads": n, "n_kv_heads": n_kv, "head_dim": h, "s": s, "top_n": N,
                    "parallelism": f"partition by request batch x{world}, no data-path collective",
-                   "l2": "inputs larger than L2 (64 GiB K per GPU)", "pipeline": "recall(l) overlaps scoring(l+1)"},
+                   "l2": "inputs larger than L2 (64 GiB K per GPU)", "pipeline": "recall(l) overlaps scoring(l+1)",
+                   "v_arena_numa_node": numa},
         "per_gpu_tokens_per_s": value / world,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": traffic, "peak_kind": peak_kind,

@@ -60,3 +60,30 @@ def gather_rows(local, global_batch: int, group=None):
     parts = [torch.empty_like(buf) for _ in range(world)]
     dist.all_gather(parts, buf, group=group)
     return torch.cat([p[:c] for p, c in zip(parts, counts)], dim=0)
+
+
+def gpu_numa_node(device: int) -> int:
+    """NUMA node of CUDA device ``device`` from sysfs (-1 when unknown): the
+    node its pinned V arena is bound to, so each GPU's recall reads host
+    memory local to its own PCIe root."""
+    try:
+        import torch
+        p = torch.cuda.get_device_properties(device)
+        bdf = "%04x:%02x:%02x.0" % (p.pci_domain_id, p.pci_bus_id, p.pci_device_id)
+        with open(f"/sys/bus/pci/devices/{bdf}/numa_node") as f:
+            node = int(f.read().strip())
+        return node if node >= 0 else -1
+    except Exception:
+        return -1
+
+
+def host_mem_available() -> int:
+    """MemAvailable of this host in bytes (0 when unknown)."""
+    try:
+        with open("/proc/meminfo") as f:
+            for line in f:
+                if line.startswith("MemAvailable:"):
+                    return int(line.split()[1]) * 1024
+    except OSError:
+        pass
+    return 0
