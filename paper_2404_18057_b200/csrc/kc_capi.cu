@@ -193,6 +193,7 @@ struct kc_cache {
   int host_frac_pct = 50;  // hybrid recall: % of rows gathered by host threads
   int auto_recall_mode = kRecallZeroCopy;  // what recall_mode 0 resolves to
   int score_groups = 0;   // row groups per layer (score -> select -> recall each); 0 = auto
+  int score_mma = 1;       // GQA scoring on the tensor cores (TF32 split-q mma.sync)
   int k_policy = 0;        // L2 policy of the K stream (kc_device.cuh l2_policy)
   // MHA candidate selection: 0 auto (rows longer than the register-resident
   // dense select), 1 always, 2 never
@@ -404,11 +405,13 @@ struct StepGeom {
   int s, nc, chunk, n_splits;
 };
 
-StepGeom geom(kc_cache* c, uint64_t top_n) {
+// chunk_g: the group size the split length is tuned for (the GQA scoring
+// kernel wants long items; the fused full-attention kernel the MHA sizing)
+StepGeom geom(kc_cache* c, uint64_t top_n, int chunk_g = -1) {
   StepGeom g{};
   g.s = (int)c->current_len();
   g.nc = (int)std::min<uint64_t>(top_n, (uint64_t)g.s);
-  g.chunk = kc::score_pick_chunk(g.s, (int)c->rows, c->score_chunk);
+  g.chunk = kc::score_pick_chunk(g.s, (int)c->rows, c->score_chunk, chunk_g < 0 ? (int)c->G : chunk_g);
   g.n_splits = (g.s + g.chunk - 1) / g.chunk;
   if (g.n_splits > c->max_splits) {
     g.chunk = ((g.s + c->max_splits - 1) / c->max_splits + 63) / 64 * 64;
@@ -480,6 +483,7 @@ void enqueue_score(kc_cache* c, uint64_t layer, const float* q32, const StepGeom
   sp.stages = c->score_stages;
   sp.ctas_per_sm = c->score_ctas_per_sm;
   sp.k_policy = c->k_policy;
+  sp.use_mma = c->score_mma;
   c->timed(0, st, [&] { kc::score_launch(sp, c->dtype, st); });
 }
 
@@ -1004,7 +1008,7 @@ int kc_decode_full(kc_cache* c, uint64_t layer, const void* q, int q_dtype, uint
     set_dev(c);
     const bool io_device = flags & KC_IO_DEVICE;
     cudaStream_t st = io_device ? (cudaStream_t)stream : c->main_st;
-    const StepGeom g = geom(c, 1);
+    const StepGeom g = geom(c, 1, 1);  // fused full kernel: MHA split sizing
     maybe_flush_l2(c, &layer, 1, st);
     const float* q32 = stage_q(c, 0, q, q_dtype, io_device, st);
     const uint64_t slots = c->batch * c->n_q;
@@ -1231,6 +1235,7 @@ int kc_set_tuning(kc_cache* c, const char* key, int64_t value) {
       c->select_cand = (int)value;
     }
     else if (k == "k_policy") c->k_policy = (int)value;
+    else if (k == "score_mma") c->score_mma = value ? 1 : 0;
     else if (k == "cand_force_fallback") c->cand_force_fallback = value ? 1 : 0;
     else if (k == "score_groups") {
       if (value < 0) fail(KC_EARG, "score_groups must be >= 0 (0 = auto)");

@@ -57,6 +57,21 @@ __device__ __forceinline__ void unpack8<__nv_bfloat16>(const uint4& raw, float (
   }
 }
 
+// Packed fp32 FMA (sm_100 FFMA2): (a.x*b.x + c.x, a.y*b.y + c.y), each
+// lane rounded like fmaf.
+__device__ __forceinline__ float2 ffma2(float a0, float a1, float b0, float b1, float2 c) {
+  float2 d;
+  asm("{ .reg .b64 ra, rb, rc, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\t"
+      "mov.b64 rb, {%4, %5};\n\t"
+      "mov.b64 rc, {%6, %7};\n\t"
+      "fma.rn.f32x2 rd, ra, rb, rc;\n\t"
+      "mov.b64 {%0, %1}, rd; }"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a0), "f"(a1), "f"(b0), "f"(b1), "f"(c.x), "f"(c.y));
+  return d;
+}
+
 // ---- softmax partial-stat combine (m = running max, l = sum exp(s - m)) ----
 __device__ __forceinline__ void ml_combine(float& m, float& l, float m2, float l2) {
   const float M = fmaxf(m, m2);

@@ -41,6 +41,7 @@ struct ScoreParams {
   uint2* cand_meta;     // [rows][max_splits]
   int cand_nc;          // 0: dense logits
   int k_policy;         // L2 policy of the K stream (0 evict_first; see l2_policy)
+  int use_mma;          // GQA (2 <= G <= 8): tensor-core scoring (score_mma_kernel)
 };
 // Read `bytes` of a scratch buffer larger than L2: evicts (and so writes back)
 // every dirty L2 line, after which all stored K is clean in DRAM.
@@ -48,7 +49,7 @@ void l2_flush_launch(const void* scratch, size_t bytes, cudaStream_t st);
 // dtype: KC_F32 / KC_F16 / KC_BF16 (storage)
 void score_launch(const ScoreParams& p, int dtype, cudaStream_t st);
 // positions per CTA for a given shape (tuning override when > 0)
-int score_pick_chunk(int s, int rows, int override_chunk);
+int score_pick_chunk(int s, int rows, int override_chunk, int G = 1);
 // whether the candidate-mode scoring kernel covers this shape
 bool score_cand_supported(int dtype, int h, int G, int chunk, int nc);
 

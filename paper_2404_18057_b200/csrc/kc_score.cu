@@ -51,6 +51,62 @@ __device__ __forceinline__ int chunk_of(int ci, int rl, int sub) {
   }
 }
 
+// ---- the K stream shared by the scoring kernels ----------------------------
+// Producer warp: lane 0 streams the items' K runs (one contiguous run of
+// chunk*h elements per (row, split) in the [b][kv][pos][h] arena) into a
+// STAGES-deep ring of 64-position stages with 1-D TMA bulk copies
+// (cp.async.bulk, L2 evict-first) on mbarriers. As soon as a stage has landed
+// in shared memory the warp drops its K lines from L2 (discard.global.L2,
+// positions < discard_len, which the store keeps clean): a decode step streams
+// the whole K cache once, and L2 lines held by dead K are useless to the
+// concurrent V recall.
+template <typename T, int STAGES>
+__device__ __forceinline__ void produce_k(const ScoreParams& p, uint8_t* ring, uint64_t* full, uint64_t* empty,
+                                          int lane, int n_items) {
+  constexpr int ROWB = kH * (int)sizeof(T);
+  const uint64_t pol = l2_policy(p.k_policy);
+  const char* held[STAGES];  // what each ring slot holds: start + line count
+  int held_lines[STAGES];
+#pragma unroll
+  for (int st = 0; st < STAGES; ++st) held_lines[st] = 0;
+  auto drop = [&](int st) {
+    const char* base = held[st];
+    for (int l = lane; l < held_lines[st]; l += 32) discard_l2_line(base + (size_t)l * 128);
+  };
+  uint32_t g = 0;  // global stage counter across items
+  // drop stage j's lines as soon as its bytes have landed (lag STAGES-1
+  // behind the issue point so the ring stays full)
+  auto land_and_drop = [&](uint32_t j) {
+    const int sj = (int)(j % STAGES);
+    mbar_wait(&full[sj], (j / STAGES) & 1);
+    drop(sj);
+  };
+  for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+    const int row = p.row0 + item / p.n_splits;
+    const int pos0 = (item - (row - p.row0) * p.n_splits) * p.chunk;
+    const int npos = min(p.chunk, p.s - pos0);
+    const int n_it = (npos + kRows - 1) / kRows;
+    const T* kslot = static_cast<const T*>(p.k) + (size_t)row * p.max_seq * kH;
+    for (int it = 0; it < n_it; ++it, ++g) {
+      const int st = (int)(g % STAGES);
+      if (g >= (uint32_t)STAGES) mbar_wait(&empty[st], ((g / STAGES) - 1) & 1);
+      const int pstart = pos0 + it * kRows;
+      const int rows = min(kRows, npos - it * kRows);
+      held[st] = reinterpret_cast<const char*>(kslot + (size_t)pstart * kH);
+      held_lines[st] = max(0, min(pstart + rows, p.discard_len) - pstart) * (ROWB / 128);
+      if (lane == 0) {
+        const uint32_t bytes = (uint32_t)(rows * ROWB);
+        mbar_arrive_expect_tx(&full[st], bytes);
+        tma_bulk_g2s(ring + st * kRows * ROWB, kslot + (size_t)pstart * kH, bytes, &full[st], pol);
+      }
+      __syncwarp();
+      if (g >= (uint32_t)(STAGES - 1)) land_and_drop(g - (STAGES - 1));
+    }
+  }
+  // drain: the last STAGES-1 stages
+  for (uint32_t j = g > (uint32_t)(STAGES - 1) ? g - (STAGES - 1) : 0; j < g; ++j) land_and_drop(j);
+}
+
 // Candidate epilogue of one split (MHA): scb[0..npos) holds the split's
 // scores. tau = the nc-th largest of the 256 consumer threads' block maxima is
 // a lower bound of the split's nc-th largest score (nc threads each hold a
@@ -122,7 +178,7 @@ __device__ __forceinline__ void emit_candidates(const float* scb, float* mx, uin
 }
 
 template <typename T, int G, int LPR, int STAGES, bool CAND>
-__global__ void __launch_bounds__((kCWarps + 1) * 32)
+__global__ void __launch_bounds__((kCWarps + 1) * 32, (G >= 2 ? 2 : 1))
     score_fast_kernel(const ScoreParams p) {
   constexpr int CPL = 16 / LPR;            // 16-B chunks per lane per row
   constexpr int RPP = 32 / LPR;            // rows per warp pass
@@ -156,54 +212,7 @@ __global__ void __launch_bounds__((kCWarps + 1) * 32)
   __syncthreads();
 
   if (warp == kCWarps) {
-    // ---------------- producer warp: lane 0 streams K with TMA ----------------
-    // Once a stage has landed in shared memory the warp drops its K lines from
-    // L2 (discard.global.L2, positions < discard_len, which the store keeps
-    // clean): a decode step streams the whole K cache once, and L2 lines held
-    // by dead K evict the GPU page-table lines the zero-copy V recall walks
-    // (DESIGN.md section 5).
-    const uint64_t pol = l2_policy(p.k_policy);
-    const char* held[STAGES];  // what each ring slot holds: start + line count
-    int held_lines[STAGES];
-#pragma unroll
-    for (int st = 0; st < STAGES; ++st) held_lines[st] = 0;
-    auto drop = [&](int st) {
-      const char* base = held[st];
-      for (int l = lane; l < held_lines[st]; l += 32) discard_l2_line(base + (size_t)l * 128);
-    };
-    uint32_t g = 0;  // global stage counter across items
-    // drop stage j's lines as soon as its bytes have landed in shared memory
-    // (the L2 copy is dead from then on); lag STAGES-1 behind the issue point
-    // so the ring stays full
-    auto land_and_drop = [&](uint32_t j) {
-      const int sj = (int)(j % STAGES);
-      mbar_wait(&full[sj], (j / STAGES) & 1);
-      drop(sj);
-    };
-    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-      const int row = p.row0 + item / p.n_splits;
-      const int pos0 = (item - (row - p.row0) * p.n_splits) * p.chunk;
-      const int npos = min(p.chunk, p.s - pos0);
-      const int n_it = (npos + kRows - 1) / kRows;
-      const T* kslot = static_cast<const T*>(p.k) + (size_t)row * p.max_seq * kH;
-      for (int it = 0; it < n_it; ++it, ++g) {
-        const int st = (int)(g % STAGES);
-        if (g >= (uint32_t)STAGES) mbar_wait(&empty[st], ((g / STAGES) - 1) & 1);
-        const int pstart = pos0 + it * kRows;
-        const int rows = min(kRows, npos - it * kRows);
-        held[st] = reinterpret_cast<const char*>(kslot + (size_t)pstart * kH);
-        held_lines[st] = max(0, min(pstart + rows, p.discard_len) - pstart) * (ROWB / 128);
-        if (lane == 0) {
-          const uint32_t bytes = (uint32_t)(rows * ROWB);
-          mbar_arrive_expect_tx(&full[st], bytes);
-          tma_bulk_g2s(ring + st * kRows * ROWB, kslot + (size_t)pstart * kH, bytes, &full[st], pol);
-        }
-        __syncwarp();
-        if (g >= (uint32_t)(STAGES - 1)) land_and_drop(g - (STAGES - 1));
-      }
-    }
-    // drain: the last STAGES-1 stages
-    for (uint32_t j = g > (uint32_t)(STAGES - 1) ? g - (STAGES - 1) : 0; j < g; ++j) land_and_drop(j);
+    produce_k<T, STAGES>(p, ring, full, empty, lane, n_items);
     return;
   }
 
@@ -246,18 +255,38 @@ __global__ void __launch_bounds__((kCWarps + 1) * 32)
         const int pl = it * kRows + r;
         const uint4* srow = reinterpret_cast<const uint4*>(sb + r * ROWB);
         float acc[G];
+        if constexpr (G == 1) {
+          // MHA: one fmaf chain in element order (the candidate-mode dense
+          // redo in kc_select.cu reproduces this exact sequence)
+          acc[0] = 0.0f;
 #pragma unroll
-        for (int gh = 0; gh < G; ++gh) acc[gh] = 0.0f;
+          for (int ci = 0; ci < CPL; ++ci) {
+            const uint4 raw = srow[chunk_of<LPR>(ci, rl, sub)];
+            float kf[8];
+            unpack8<T>(raw, kf);
 #pragma unroll
-        for (int ci = 0; ci < CPL; ++ci) {
-          const uint4 raw = srow[chunk_of<LPR>(ci, rl, sub)];
-          float kf[8];
-          unpack8<T>(raw, kf);
-#pragma unroll
-          for (int gh = 0; gh < G; ++gh) {
-#pragma unroll
-            for (int e = 0; e < 8; ++e) acc[gh] = fmaf(qf[gh][ci][e], kf[e], acc[gh]);
+            for (int e = 0; e < 8; ++e) acc[0] = fmaf(qf[0][ci][e], kf[e], acc[0]);
           }
+        } else {
+          // GQA is issue-bound (G dot products per K element): packed FFMA2
+          // over even/odd element pairs, the two chains summed at the end
+          float2 acc2[G];
+#pragma unroll
+          for (int gh = 0; gh < G; ++gh) acc2[gh] = make_float2(0.0f, 0.0f);
+#pragma unroll
+          for (int ci = 0; ci < CPL; ++ci) {
+            const uint4 raw = srow[chunk_of<LPR>(ci, rl, sub)];
+            float kf[8];
+            unpack8<T>(raw, kf);
+#pragma unroll
+            for (int gh = 0; gh < G; ++gh) {
+#pragma unroll
+              for (int e = 0; e < 8; e += 2)
+                acc2[gh] = ffma2(qf[gh][ci][e], qf[gh][ci][e + 1], kf[e], kf[e + 1], acc2[gh]);
+            }
+          }
+#pragma unroll
+          for (int gh = 0; gh < G; ++gh) acc[gh] = acc2[gh].x + acc2[gh].y;
         }
 #pragma unroll
         for (int o = LPR / 2; o >= 1; o >>= 1) {
@@ -305,6 +334,242 @@ __global__ void __launch_bounds__((kCWarps + 1) * 32)
       emit_candidates(scb, mx, wcnt, npos, p.cand_nc, pos0, p.cand + (size_t)row * p.lstride + pos0,
                       p.cand_meta + (size_t)row * p.max_splits + split);
     named_sync(1, kCWarps * 32);  // red / scb are reused by the next item
+  }
+}
+
+// ---- GQA scoring on the tensor cores ---------------------------------------
+// For G q heads per kv head the scoring is a [G x 128] x [128 x positions]
+// product per (row, split); on CUDA cores it is issue-bound (G FMAs per K
+// element). Here each consumer warp computes its 8 positions of a stage with
+// mma.sync m16n8k16 (fp32 accumulation): A = the group's q (heads as rows,
+// padded to 16), B = K^T straight from shared memory (8 positions as
+// columns, no conversion). K is exact in the MMA's input type; q carries
+// fp32 precision as a sum of parts: fp16 K -> q*2^e = hi + lo in fp16 (e puts
+// the head's max |q| at 2^14, so both parts are normal and hi+lo keeps ~22
+// significand bits of every element relative to the largest), bf16 K ->
+// q = p1 + p2 + p3 in bf16 (24 bits). One MMA per part and k-step.
+// The k dimension is permuted so a lane's operands are contiguous: lane
+// (gid, tig) loads 16-B chunks tig, tig+4, tig+8, tig+12 of position gid's
+// row; k-step j uses 4 dims of chunk tig+4(j/2) at offset 4(j%2): b0 = dims
+// +0,+1 (k = 2tig, 2tig+1), b1 = dims +2,+3 (k = 2tig+8, +9). Two positions
+// per quarter-warp share banks pairwise (2-way conflict). q is permuted the
+// same way.
+template <typename T>
+__device__ __forceinline__ void mma_16816(float (&d)[4], uint32_t a0, uint32_t a2, uint32_t b0, uint32_t b1);
+template <>
+__device__ __forceinline__ void mma_16816<__half>(float (&d)[4], uint32_t a0, uint32_t a2, uint32_t b0,
+                                                  uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(0u), "r"(a2), "r"(0u), "r"(b0), "r"(b1));
+}
+template <>
+__device__ __forceinline__ void mma_16816<__nv_bfloat16>(float (&d)[4], uint32_t a0, uint32_t a2, uint32_t b0,
+                                                         uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(0u), "r"(a2), "r"(0u), "r"(b0), "r"(b1));
+}
+
+// q split into NP parts of T; returns the scale to undo (2^-e for fp16)
+template <typename T>
+struct QSplit;
+template <>
+struct QSplit<__half> {
+  static constexpr int NP = 2;
+  __device__ static float prescale(float amax) {
+    if (!(amax > 0.0f) || !isfinite(amax)) return 1.0f;
+    return ldexpf(1.0f, 14 - ilogbf(amax));
+  }
+  __device__ static uint32_t pack(float x, float y) {
+    const __half2 h = __floats2half2_rn(x, y);
+    return *reinterpret_cast<const uint32_t*>(&h);
+  }
+  __device__ static float2 unpack(uint32_t w) {
+    return __half22float2(*reinterpret_cast<const __half2*>(&w));
+  }
+};
+template <>
+struct QSplit<__nv_bfloat16> {
+  static constexpr int NP = 3;
+  __device__ static float prescale(float) { return 1.0f; }
+  __device__ static uint32_t pack(float x, float y) {
+    const __nv_bfloat162 h = __floats2bfloat162_rn(x, y);
+    return *reinterpret_cast<const uint32_t*>(&h);
+  }
+  __device__ static float2 unpack(uint32_t w) {
+    return __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w));
+  }
+};
+
+template <typename T, int STAGES>
+__global__ void __launch_bounds__((kCWarps + 1) * 32) score_mma_kernel(const ScoreParams p) {
+  using QS = QSplit<T>;
+  constexpr int NP = QS::NP;
+  constexpr int ROWB = kH * (int)sizeof(T);
+  constexpr int kMaxG = 8;
+  constexpr int kHalf = kCWarps / 2;  // warps per stage
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint8_t* ring = smem;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * kRows * ROWB);
+  uint64_t* empty = full + STAGES;
+  float2* red = reinterpret_cast<float2*>(empty + STAGES);  // [kCWarps][kMaxG]
+
+  const int n_items = p.rows * p.n_splits;
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int st = 0; st < STAGES; ++st) {
+      mbar_init(&full[st], 1);
+      mbar_init(&empty[st], kHalf);  // each stage is consumed by one half of the warps
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (warp == kCWarps) {
+    produce_k<T, STAGES>(p, ring, full, empty, lane, n_items);
+    return;
+  }
+
+  const int G = p.G, n_q = p.n_kv * G;
+  const int gid = lane >> 2, tig = lane & 3;
+  const bool hv = gid < G;     // this lane's A row is a real head
+  const int half = warp / kHalf;  // stages with (global index % 2) == half
+  const int wq = warp % kHalf;    // positions 16wq .. 16wq+15 of those stages
+  uint32_t g = 0;
+  for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+    const int row = p.row0 + item / p.n_splits;
+    const int split = item - (row - p.row0) * p.n_splits;
+    const int b = row / p.n_kv;
+    const int kvh = row - b * p.n_kv;
+    const int pos0 = split * p.chunk;
+    const int npos = min(p.chunk, p.s - pos0);
+    const int n_it = (npos + kRows - 1) / kRows;
+    // A fragments of head gid: k-step j -> a0 = dims c*8 + 4(j&1) + {0,1},
+    // a2 = + {2,3}, c = tig + 4(j>>1)
+    const float* qh = p.q + ((size_t)b * n_q + kvh * G + (hv ? gid : 0)) * kH;
+    float qv[32];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int c = tig + 4 * i;
+      const float4 x0 = *reinterpret_cast<const float4*>(qh + c * 8);
+      const float4 x1 = *reinterpret_cast<const float4*>(qh + c * 8 + 4);
+      qv[8 * i + 0] = x0.x; qv[8 * i + 1] = x0.y; qv[8 * i + 2] = x0.z; qv[8 * i + 3] = x0.w;
+      qv[8 * i + 4] = x1.x; qv[8 * i + 5] = x1.y; qv[8 * i + 6] = x1.z; qv[8 * i + 7] = x1.w;
+    }
+    float amax = 0.0f;
+#pragma unroll
+    for (int e = 0; e < 32; ++e) amax = fmaxf(amax, fabsf(qv[e]));
+    amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 1));
+    amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 2));
+    const float pre = QS::prescale(amax);
+    const float post = 1.0f / pre;  // exact: a power of two
+    uint32_t af[NP][8][2];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int e0 = 8 * (j >> 1) + 4 * (j & 1) + 2 * u;
+        float x = hv ? qv[e0] * pre : 0.0f, y = hv ? qv[e0 + 1] * pre : 0.0f;
+#pragma unroll
+        for (int k = 0; k < NP; ++k) {
+          const uint32_t w = QS::pack(x, y);
+          af[k][j][u] = w;
+          const float2 back = QS::unpack(w);
+          x -= back.x;
+          y -= back.y;
+        }
+      }
+    }
+    float m_run = -INFINITY, l_run = 0.0f;
+    float* lrow = p.logits + ((size_t)b * n_q + kvh * G + (hv ? gid : 0)) * p.lstride + pos0;
+    for (int it = 0; it < n_it; ++it, ++g) {
+      if ((int)(g & 1u) != half) continue;
+      const int st = (int)(g % STAGES);
+      mbar_wait(&full[st], (g / STAGES) & 1);
+      const uint8_t* sb = ring + st * kRows * ROWB;
+      // two n-tiles: positions 16wq + gid and 16wq + 8 + gid
+      uint4 kc[2][4];
+#pragma unroll
+      for (int t = 0; t < 2; ++t)
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          kc[t][i] = *reinterpret_cast<const uint4*>(sb + (16 * wq + 8 * t + gid) * ROWB + 16 * (tig + 4 * i));
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+      float dd[2][NP][4];
+#pragma unroll
+      for (int t = 0; t < 2; ++t)
+#pragma unroll
+        for (int k = 0; k < NP; ++k)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) dd[t][k][e] = 0.0f;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          const uint4 c = kc[t][j >> 1];
+          const uint32_t b0 = (j & 1) ? c.z : c.x;
+          const uint32_t b1 = (j & 1) ? c.w : c.y;
+#pragma unroll
+          for (int k = 0; k < NP; ++k) mma_16816<T>(dd[t][k], af[k][j][0], af[k][j][1], b0, b1);
+        }
+      }
+      // dd[t][.][0..1] = head gid at the stage's positions 16wq + 8t + 2tig, +1
+      if (hv) {
+        float sc[4];
+        float smax = -INFINITY;
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          const int pl = it * kRows + 16 * wq + 8 * t + 2 * tig;
+          float a0 = 0.0f, a1 = 0.0f;
+#pragma unroll
+          for (int k = NP - 1; k >= 0; --k) {  // small parts first
+            a0 += dd[t][k][0];
+            a1 += dd[t][k][1];
+          }
+          sc[2 * t] = pl < npos ? (a0 * post) * p.scale : -INFINITY;
+          sc[2 * t + 1] = pl + 1 < npos ? (a1 * post) * p.scale : -INFINITY;
+          if (pl + 1 < npos) {
+            *reinterpret_cast<float2*>(lrow + pl) = make_float2(sc[2 * t], sc[2 * t + 1]);
+          } else if (pl < npos) {
+            lrow[pl] = sc[2 * t];
+          }
+          smax = fmaxf(smax, fmaxf(sc[2 * t], sc[2 * t + 1]));
+        }
+        // one rescale per stage; the sum-exp terms use the fast exp (the
+        // split's l only normalises -- p itself is recomputed exactly)
+        if (smax > -INFINITY) {
+          const float mn = fmaxf(m_run, smax);
+          float acc = (m_run == -INFINITY) ? 0.0f : l_run * __expf(m_run - mn);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) acc += (sc[e] == -INFINITY) ? 0.0f : __expf(sc[e] - mn);
+          m_run = mn;
+          l_run = acc;
+        }
+      }
+    }
+    // per-split (max, sum exp) per head: the 4 lanes of a head, then warps
+#pragma unroll
+    for (int o = 1; o <= 2; o <<= 1) {
+      const float m2 = __shfl_xor_sync(0xffffffffu, m_run, o);
+      const float l2 = __shfl_xor_sync(0xffffffffu, l_run, o);
+      ml_combine(m_run, l_run, m2, l2);
+    }
+    if (tig == 0 && hv) red[warp * kMaxG + gid] = make_float2(m_run, l_run);
+    named_sync(1, kCWarps * 32);
+    if (threadIdx.x < G) {
+      const int gh = threadIdx.x;
+      float m = -INFINITY, l = 0.0f;
+      for (int w = 0; w < kCWarps; ++w) ml_combine(m, l, red[w * kMaxG + gh].x, red[w * kMaxG + gh].y);
+      p.partials[((size_t)b * n_q + kvh * G + gh) * p.max_splits + split] = make_float2(m, l);
+    }
+    named_sync(1, kCWarps * 32);  // red is reused by the next item
   }
 }
 
@@ -638,9 +903,34 @@ void launch_fast(const ScoreParams& p, cudaStream_t st) {
   }
 }
 
+template <typename T, int STAGES>
+void launch_mma_s(const ScoreParams& p, cudaStream_t st) {
+  constexpr int ROWB = kH * (int)sizeof(T);
+  const size_t smem = STAGES * kRows * ROWB + 2 * STAGES * sizeof(uint64_t) + kCWarps * 8 * sizeof(float2);
+  static unsigned long long configured = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!(configured >> (dev & 63) & 1ull)) {
+    cudaFuncSetAttribute(score_mma_kernel<T, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    configured |= 1ull << (dev & 63);
+  }
+  const int n_items = p.rows * p.n_splits;
+  const int per_sm = p.ctas_per_sm > 0 ? p.ctas_per_sm : 1 << 20;
+  const int grid = (int)std::min<long long>(n_items, (long long)per_sm * num_sms());
+  score_mma_kernel<T, STAGES><<<grid, (kCWarps + 1) * 32, smem, st>>>(p);
+}
+
 template <typename T>
 bool try_fast(const ScoreParams& p, cudaStream_t st) {
   if (p.h != kH || (p.chunk % kRows) != 0) return false;
+  if (p.G >= 2 && p.G <= 8 && p.cand_nc == 0 && p.use_mma) {
+    switch (p.stages) {
+      case 6: launch_mma_s<T, 6>(p, st); break;
+      case 8: launch_mma_s<T, 8>(p, st); break;
+      default: launch_mma_s<T, 4>(p, st); break;
+    }
+    return true;
+  }
   if (p.cand_nc > 0) {
     if (p.G != 1 || p.chunk > kMaxCandChunk || p.cand_nc > kCWarps * 32) return false;
     launch_fast<T, 1, 4, true>(p, st);
@@ -669,13 +959,20 @@ void l2_flush_launch(const void* scratch, size_t bytes, cudaStream_t st) {
                                           (uint32_t*)scratch + (bytes / 4 - 1));
 }
 
-int score_pick_chunk(int s, int rows, int override_chunk) {
+int score_pick_chunk(int s, int rows, int override_chunk, int G) {
   if (override_chunk > 0) return ((override_chunk + kRows - 1) / kRows) * kRows;
-  // enough items for a balanced persistent grid (~24+ per CTA at 2 CTAs/SM),
-  // 256..2048 positions each
   const long long work = (long long)s * rows;
-  long long c = (work + 148LL * 48 - 1) / (148LL * 48);
-  c = std::max<long long>(256, std::min<long long>(2048, c));
+  long long c;
+  if (G >= 2) {
+    // GQA (score_mma_kernel, 1 CTA / SM): per-item q preparation is costly,
+    // so few long items, ~7 per SM: 2048..8192 positions
+    c = (work + 148LL * 7 - 1) / (148LL * 7);
+    c = std::max<long long>(2048, std::min<long long>(8192, c));
+  } else {
+    // MHA: ~48 items per SM (3 CTAs / SM), 256..2048 positions each
+    c = (work + 148LL * 48 - 1) / (148LL * 48);
+    c = std::max<long long>(256, std::min<long long>(2048, c));
+  }
   c = ((c + kRows - 1) / kRows) * kRows;
   return (int)c;
 }

@@ -341,14 +341,29 @@ __global__ void __launch_bounds__(kT, 1) select_reg_kernel(const SelectParams p)
   } else {
 #pragma unroll
     for (int i = 0; i < KPT; ++i) key[i] = 0u;
+    // GQA ranking key sum_g p_g: the fast exp and a reciprocal (ranking only;
+    // the weights below use the exact expf(s - M) / Z)
     for (int g = 0; g < G; ++g) {
       const float* lr = lbase + (size_t)g * p.lstride;
-      const float Mg = S.M[g], Zg = S.Z[g];
+      const float Mg = S.M[g], rZ = 1.0f / S.Z[g];
+      if (j0 + KPT <= s) {
 #pragma unroll
-      for (int i = 0; i < KPT; ++i) {
-        if (j0 + i < s) {
-          const float pg = expf(lr[j0 + i] - Mg) / Zg;
-          key[i] = (g == 0) ? __float_as_uint(pg) : __float_as_uint(__uint_as_float(key[i]) + pg);
+        for (int i = 0; i < KPT; i += 4) {
+          const float4 v = *reinterpret_cast<const float4*>(lr + j0 + i);
+          const float e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const float pg = __expf(e[u] - Mg) * rZ;
+            key[i + u] = (g == 0) ? __float_as_uint(pg) : __float_as_uint(__uint_as_float(key[i + u]) + pg);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < KPT; ++i) {
+          if (j0 + i < s) {
+            const float pg = __expf(lr[j0 + i] - Mg) * rZ;
+            key[i] = (g == 0) ? __float_as_uint(pg) : __float_as_uint(__uint_as_float(key[i]) + pg);
+          }
         }
       }
     }
