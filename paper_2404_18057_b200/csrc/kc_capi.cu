@@ -202,7 +202,8 @@ struct kc_cache {
   int select_on_side = 0;  // pipelined: selection on the side stream too (measured: no gain)
   int full_fused = 1;      // decode_attention_full: fused K+V pass when V is in HBM
   int keep_logits = 0;     // leave dead logits in L2 instead of discarding them
-  int recall_ctas = 64;  // CTAs of the recall kernel (0: one per (batch, kv head))
+  int recall_pipe = 0;    // software-pipelined recall kernel (measured: no gain, page-walk bound)
+  int recall_ctas = 32;  // CTAs of the recall kernel (0: one per (batch, kv head)); 32 measured best at C2
   int gather_threads = 0;  // 0: 3/4 of the host cores
 
   // per-kernel CUDA-event timing (kc_profile): [kind] -> (start, stop) pairs
@@ -677,6 +678,7 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
       }
       rp.staged = 0;
       rp.grid = c->recall_ctas;
+      rp.pipelined = c->recall_pipe;
       rp.idx = c->idx[slot].as<uint32_t>();
       rp.w = c->w[slot].as<float>();
       rp.norm = c->norm[slot].as<float>();
@@ -1227,6 +1229,7 @@ int kc_set_tuning(kc_cache* c, const char* key, int64_t value) {
     else if (k == "score_stages") c->score_stages = (int)value;
     else if (k == "score_ctas_per_sm") c->score_ctas_per_sm = (int)value;
     else if (k == "recall_ctas") c->recall_ctas = (int)value;
+    else if (k == "recall_pipe") c->recall_pipe = value ? 1 : 0;
     else if (k == "keep_logits") c->keep_logits = value ? 1 : 0;
     else if (k == "full_fused") c->full_fused = value ? 1 : 0;
     else if (k == "select_on_side") c->select_on_side = value ? 1 : 0;

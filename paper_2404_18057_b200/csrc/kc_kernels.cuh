@@ -122,6 +122,7 @@ struct RecallParams {
   int staged;             // v is the compacted [rows][nc][h] block (DMA recall)
   int grid;               // CTAs (0: one per row); CTAs loop over rows
   int discard_len;        // positions < discard_len are clean: drop their lines from L2 after use
+  int pipelined;          // use recall_pv_pipe_kernel where the shape allows
 };
 void recall_launch(const RecallParams& p, int dtype, cudaStream_t st);
 

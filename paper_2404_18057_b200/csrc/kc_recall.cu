@@ -24,6 +24,8 @@ namespace {
 
 constexpr int kRecallThreads = 256;
 constexpr int kRecallSmem = 40 * 1024;
+constexpr int kH = 128;
+constexpr int kMaxGroup = 8;
 
 template <typename T>
 __global__ void __launch_bounds__(kRecallThreads) recall_pv_kernel(const RecallParams p, int rc_max) {
@@ -128,6 +130,101 @@ __global__ void __launch_bounds__(kRecallThreads) recall_pv_kernel(const RecallP
     }
   }
   }  // row loop
+}
+
+// Software-pipelined variant for the common shape (h = 128 16-bit rows,
+// nc <= 128): while the CTA reduces row r from one shared-memory buffer, the
+// 16-B zero-copy loads of its next row are already in flight into registers,
+// so a small grid keeps the PCIe read queue full without leaving the SMs to
+// wait on host latency between rows. Same operation order as
+// recall_pv_kernel.
+constexpr int kPipeMaxNc = 128;
+
+template <typename T>
+__global__ void __launch_bounds__(kRecallThreads) recall_pv_pipe_kernel(const RecallParams p) {
+  constexpr int kVpr = 16;  // 16-B chunks per 256-B row
+  constexpr int kLoads = kPipeMaxNc * kVpr / kRecallThreads;  // 8
+  extern __shared__ __align__(16) uint8_t smem[];
+  uint4* vb = reinterpret_cast<uint4*>(smem);                       // [2][nc][16]
+  float* wb = reinterpret_cast<float*>(smem + 2 * kPipeMaxNc * 256);  // [2][G][nc]
+  const int G = p.G, n_q = p.n_kv * G, nc = p.nc;
+  const int tid = threadIdx.x;
+  const int total = nc * kVpr;
+  const int end = p.row_offset + p.rows;
+  uint4 tmp[kLoads];
+  auto vslot_of = [&](int row) {
+    return reinterpret_cast<const uint4*>(static_cast<const T*>(p.v) +
+                                          (size_t)row * (p.staged ? (size_t)nc : (size_t)p.max_seq) * kH);
+  };
+  auto issue = [&](int row) {
+    const uint4* vs = vslot_of(row);
+    const uint32_t* idx = p.idx + (size_t)row * nc;
+#pragma unroll
+    for (int u = 0; u < kLoads; ++u) {
+      const int v = tid + u * kRecallThreads;
+      if (v < total) {
+        const int r = v >> 4, part = v & 15;
+        const size_t pos = p.staged ? (size_t)r : (size_t)idx[r];
+        tmp[u] = vs[pos * kVpr + part];
+      }
+    }
+  };
+  int row = p.row_offset + blockIdx.x;
+  if (row < end) issue(row);
+  int buf = 0;
+  while (row < end) {
+    const int b = row / p.n_kv;
+    const int kvh = row - b * p.n_kv;
+    // land: the rows this thread loaded -> shared memory, then drop their
+    // (clean) L2 lines; the weights of the row's q heads
+    {
+      const uint4* vs = vslot_of(row);
+      const uint32_t* idx = p.idx + (size_t)row * nc;
+      uint4* dst = vb + buf * kPipeMaxNc * kVpr;
+#pragma unroll
+      for (int u = 0; u < kLoads; ++u) {
+        const int v = tid + u * kRecallThreads;
+        if (v < total) {
+          dst[v] = tmp[u];
+          const int r = v >> 4, part = v & 15;
+          if (!p.staged && (part & 7) == 0) {
+            const uint32_t pos = idx[r];
+            if ((int)pos < p.discard_len) discard_l2_line(vs + (size_t)pos * kVpr + part);
+          }
+        }
+      }
+      float* wd = wb + buf * kMaxGroup * kPipeMaxNc;
+      for (int e = tid; e < G * nc; e += kRecallThreads) {
+        const int g = e / nc, r = e - g * nc;
+        const size_t slot = (size_t)b * n_q + kvh * G + g;
+        float w = p.w[slot * nc + r];
+        if (p.renormalize) w = __fmul_rn(w, p.norm[slot]);
+        wd[g * kPipeMaxNc + r] = w;
+      }
+    }
+    __syncthreads();
+    const int next = row + gridDim.x;
+    if (next < end) issue(next);  // in flight during the reduction below
+    const T* vt = reinterpret_cast<const T*>(vb + buf * kPipeMaxNc * kVpr);
+    const float* wd = wb + buf * kMaxGroup * kPipeMaxNc;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {  // G*h <= 1024 outputs
+      const int o = tid + i * kRecallThreads;
+      if (o < G * kH) {
+        const int g = o / kH, c = o - g * kH;
+        const float* wg = wd + g * kPipeMaxNc;
+        float a = 0.0f;
+        if (!p.reverse) {
+          for (int r = 0; r < nc; ++r) a = __fadd_rn(a, __fmul_rn(wg[r], to_f32<T>(vt[r * kH + c])));
+        } else {
+          for (int r = nc - 1; r >= 0; --r) a = __fadd_rn(a, __fmul_rn(wg[r], to_f32<T>(vt[r * kH + c])));
+        }
+        p.out[((size_t)b * n_q + kvh * G + g) * kH + c] = a;
+      }
+    }
+    row = next;
+    buf ^= 1;
+  }
 }
 
 // decode_attention_full P.V: CTA (split, row) accumulates its positions in
@@ -356,7 +453,26 @@ void step_stats_launch(const uint32_t* idx, const double* dropped, int rows, int
   step_stats_kernel<<<1, 1024, 0, st>>>(idx, dropped, rows, G, nc, len, slots, acc);
 }
 
+template <typename T>
+void launch_pipe(const RecallParams& p, cudaStream_t st) {
+  const size_t smem = 2 * kPipeMaxNc * 256 + 2 * kMaxGroup * kPipeMaxNc * sizeof(float);
+  static unsigned long long configured = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!(configured >> (dev & 63) & 1ull)) {
+    cudaFuncSetAttribute(recall_pv_pipe_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    configured |= 1ull << (dev & 63);
+  }
+  const int grid = (p.grid > 0 && p.grid < p.rows) ? p.grid : p.rows;
+  recall_pv_pipe_kernel<T><<<grid, kRecallThreads, smem, st>>>(p);
+}
+
 void recall_launch(const RecallParams& p, int dtype, cudaStream_t st) {
+  if (p.pipelined && p.h == kH && p.nc <= kPipeMaxNc && p.G <= kMaxGroup && dtype != KC_F32) {
+    if (dtype == KC_F16) launch_pipe<__half>(p, st);
+    else launch_pipe<__nv_bfloat16>(p, st);
+    return;
+  }
   const size_t esz = dtype == KC_F32 ? 4 : 2;
   const size_t rowb = (size_t)p.h * esz;
   int rc_max = (int)(kRecallSmem / (rowb + 4 * (size_t)p.G));

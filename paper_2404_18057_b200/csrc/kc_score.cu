@@ -897,6 +897,8 @@ void launch_fast_s(const ScoreParams& p, cudaStream_t st) {
 template <typename T, int G, int LPR, bool CAND>
 void launch_fast(const ScoreParams& p, cudaStream_t st) {
   switch (p.stages) {
+    case 2: launch_fast_s<T, G, LPR, 2, CAND>(p, st); break;
+    case 3: launch_fast_s<T, G, LPR, 3, CAND>(p, st); break;
     case 6: launch_fast_s<T, G, LPR, 6, CAND>(p, st); break;
     case 8: launch_fast_s<T, G, LPR, 8, CAND>(p, st); break;
     default: launch_fast_s<T, G, LPR, 4, CAND>(p, st); break;

@@ -16,7 +16,8 @@ from tests.test_gpu_parity import build_cache, compare_all
 
 pytestmark = pytest.mark.gpu
 
-DEFAULTS = {"select_cand": 0, "cand_force_fallback": 0, "score_groups": 0, "recall_mode": 0, "score_chunk": 0}
+DEFAULTS = {"select_cand": 0, "cand_force_fallback": 0, "score_groups": 0, "recall_mode": 0, "score_chunk": 0,
+            "recall_pipe": 0, "score_mma": 1, "recall_ctas": 32}
 
 
 def _run(kc, cache, q, N, renorm=False, **tune):
@@ -112,8 +113,9 @@ def test_underflow_ties_take_lowest_positions(kc, oracle):
 
 @pytest.mark.parametrize("tune", [dict(score_groups=2), dict(score_groups=5), dict(recall_mode=2),
                                   dict(recall_mode=3), dict(select_cand=1), dict(select_cand=1, score_groups=3),
-                                  dict(score_chunk=4096)],
-                         ids=["groups2", "groups5", "dma", "hybrid", "cand", "cand-groups3", "chunk4096"])
+                                  dict(recall_pipe=1), dict(recall_pipe=1, recall_ctas=0), dict(score_chunk=4096)],
+                         ids=["groups2", "groups5", "dma", "hybrid", "cand", "cand-groups3", "recall-pipe",
+                              "recall-pipe-per-row", "chunk4096"])
 def test_pipeline_variants_bitwise(kc, tune):
     """Row groups, host-gather DMA recall, the hybrid recall and candidate
     selection reproduce the default path bit for bit; another split length
