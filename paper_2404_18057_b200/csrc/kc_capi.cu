@@ -1230,6 +1230,15 @@ int kc_set_tuning(kc_cache* c, const char* key, int64_t value) {
     else if (k == "score_ctas_per_sm") c->score_ctas_per_sm = (int)value;
     else if (k == "recall_ctas") c->recall_ctas = (int)value;
     else if (k == "recall_pipe") c->recall_pipe = value ? 1 : 0;
+    else if (k == "side_priority") {
+      // 1: the recall stream at the device's highest priority (default), 0: normal
+      set_dev(c);
+      CK(cudaStreamSynchronize(c->side_st));
+      CK(cudaStreamDestroy(c->side_st));
+      int lo = 0, hi = 0;
+      CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      CK(cudaStreamCreateWithPriority(&c->side_st, cudaStreamNonBlocking, value ? hi : lo));
+    }
     else if (k == "keep_logits") c->keep_logits = value ? 1 : 0;
     else if (k == "full_fused") c->full_fused = value ? 1 : 0;
     else if (k == "select_on_side") c->select_on_side = value ? 1 : 0;
