@@ -1247,7 +1247,7 @@ int kc_set_tuning(kc_cache* c, const char* key, int64_t value) {
       c->select_cand = (int)value;
     }
     else if (k == "k_policy") c->k_policy = (int)value;
-    else if (k == "score_mma") c->score_mma = value ? 1 : 0;
+    else if (k == "score_mma") c->score_mma = (int)std::max<int64_t>(0, std::min<int64_t>(2, value));
     else if (k == "cand_force_fallback") c->cand_force_fallback = value ? 1 : 0;
     else if (k == "score_groups") {
       if (value < 0) fail(KC_EARG, "score_groups must be >= 0 (0 = auto)");

@@ -406,18 +406,21 @@ struct QSplit<__nv_bfloat16> {
   }
 };
 
-template <typename T, int STAGES>
-__global__ void __launch_bounds__((kCWarps + 1) * 32) score_mma_kernel(const ScoreParams p) {
+// NCW consumer warps: 8 = two halves alternating stages (one CTA per SM at
+// 140 registers), 4 = every warp on every stage (two CTAs per SM)
+template <typename T, int STAGES, int NCW>
+__global__ void __launch_bounds__((NCW + 1) * 32) score_mma_kernel(const ScoreParams p) {
   using QS = QSplit<T>;
   constexpr int NP = QS::NP;
   constexpr int ROWB = kH * (int)sizeof(T);
   constexpr int kMaxG = 8;
-  constexpr int kHalf = kCWarps / 2;  // warps per stage
+  constexpr int kHalf = 4;            // warps per stage (16 positions each)
+  constexpr int kHalves = NCW / kHalf;
   extern __shared__ __align__(128) uint8_t smem[];
   uint8_t* ring = smem;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * kRows * ROWB);
   uint64_t* empty = full + STAGES;
-  float2* red = reinterpret_cast<float2*>(empty + STAGES);  // [kCWarps][kMaxG]
+  float2* red = reinterpret_cast<float2*>(empty + STAGES);  // [NCW][kMaxG]
 
   const int n_items = p.rows * p.n_splits;
   const int warp = threadIdx.x >> 5;
@@ -431,7 +434,7 @@ __global__ void __launch_bounds__((kCWarps + 1) * 32) score_mma_kernel(const Sco
     fence_mbar_init();
   }
   __syncthreads();
-  if (warp == kCWarps) {
+  if (warp == NCW) {
     produce_k<T, STAGES>(p, ring, full, empty, lane, n_items);
     return;
   }
@@ -439,7 +442,7 @@ __global__ void __launch_bounds__((kCWarps + 1) * 32) score_mma_kernel(const Sco
   const int G = p.G, n_q = p.n_kv * G;
   const int gid = lane >> 2, tig = lane & 3;
   const bool hv = gid < G;     // this lane's A row is a real head
-  const int half = warp / kHalf;  // stages with (global index % 2) == half
+  const int half = warp / kHalf;  // stages with (global index % kHalves) == half
   const int wq = warp % kHalf;    // positions 16wq .. 16wq+15 of those stages
   uint32_t g = 0;
   for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
@@ -489,7 +492,7 @@ __global__ void __launch_bounds__((kCWarps + 1) * 32) score_mma_kernel(const Sco
     float m_run = -INFINITY, l_run = 0.0f;
     float* lrow = p.logits + ((size_t)b * n_q + kvh * G + (hv ? gid : 0)) * p.lstride + pos0;
     for (int it = 0; it < n_it; ++it, ++g) {
-      if ((int)(g & 1u) != half) continue;
+      if ((int)(g % kHalves) != half) continue;
       const int st = (int)(g % STAGES);
       mbar_wait(&full[st], (g / STAGES) & 1);
       const uint8_t* sb = ring + st * kRows * ROWB;
@@ -562,14 +565,14 @@ __global__ void __launch_bounds__((kCWarps + 1) * 32) score_mma_kernel(const Sco
       ml_combine(m_run, l_run, m2, l2);
     }
     if (tig == 0 && hv) red[warp * kMaxG + gid] = make_float2(m_run, l_run);
-    named_sync(1, kCWarps * 32);
+    named_sync(1, NCW * 32);
     if (threadIdx.x < G) {
       const int gh = threadIdx.x;
       float m = -INFINITY, l = 0.0f;
-      for (int w = 0; w < kCWarps; ++w) ml_combine(m, l, red[w * kMaxG + gh].x, red[w * kMaxG + gh].y);
+      for (int w = 0; w < NCW; ++w) ml_combine(m, l, red[w * kMaxG + gh].x, red[w * kMaxG + gh].y);
       p.partials[((size_t)b * n_q + kvh * G + gh) * p.max_splits + split] = make_float2(m, l);
     }
-    named_sync(1, kCWarps * 32);  // red is reused by the next item
+    named_sync(1, NCW * 32);  // red is reused by the next item
   }
 }
 
@@ -905,31 +908,38 @@ void launch_fast(const ScoreParams& p, cudaStream_t st) {
   }
 }
 
-template <typename T, int STAGES>
+template <typename T, int STAGES, int NCW>
 void launch_mma_s(const ScoreParams& p, cudaStream_t st) {
   constexpr int ROWB = kH * (int)sizeof(T);
-  const size_t smem = STAGES * kRows * ROWB + 2 * STAGES * sizeof(uint64_t) + kCWarps * 8 * sizeof(float2);
+  const size_t smem = STAGES * kRows * ROWB + 2 * STAGES * sizeof(uint64_t) + NCW * 8 * sizeof(float2);
   static unsigned long long configured = 0;
   int dev = 0;
   cudaGetDevice(&dev);
   if (!(configured >> (dev & 63) & 1ull)) {
-    cudaFuncSetAttribute(score_mma_kernel<T, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(score_mma_kernel<T, STAGES, NCW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
     configured |= 1ull << (dev & 63);
   }
   const int n_items = p.rows * p.n_splits;
   const int per_sm = p.ctas_per_sm > 0 ? p.ctas_per_sm : 1 << 20;
   const int grid = (int)std::min<long long>(n_items, (long long)per_sm * num_sms());
-  score_mma_kernel<T, STAGES><<<grid, (kCWarps + 1) * 32, smem, st>>>(p);
+  score_mma_kernel<T, STAGES, NCW><<<grid, (NCW + 1) * 32, smem, st>>>(p);
 }
 
 template <typename T>
 bool try_fast(const ScoreParams& p, cudaStream_t st) {
   if (p.h != kH || (p.chunk % kRows) != 0) return false;
   if (p.G >= 2 && p.G <= 8 && p.cand_nc == 0 && p.use_mma) {
-    switch (p.stages) {
-      case 6: launch_mma_s<T, 6>(p, st); break;
-      case 8: launch_mma_s<T, 8>(p, st); break;
-      default: launch_mma_s<T, 4>(p, st); break;
+    if (p.use_mma == 2) {  // 8 consumer warps, one CTA per SM
+      switch (p.stages) {
+        case 8: launch_mma_s<T, 8, 8>(p, st); break;
+        default: launch_mma_s<T, 4, 8>(p, st); break;
+      }
+    } else {  // 4 consumer warps, two CTAs per SM
+      switch (p.stages) {
+        case 8: launch_mma_s<T, 8, 4>(p, st); break;
+        default: launch_mma_s<T, 4, 4>(p, st); break;
+      }
     }
     return true;
   }
@@ -966,10 +976,10 @@ int score_pick_chunk(int s, int rows, int override_chunk, int G) {
   const long long work = (long long)s * rows;
   long long c;
   if (G >= 2) {
-    // GQA (score_mma_kernel, 1 CTA / SM): per-item q preparation is costly,
-    // so few long items, ~7 per SM: 2048..8192 positions
-    c = (work + 148LL * 7 - 1) / (148LL * 7);
-    c = std::max<long long>(2048, std::min<long long>(8192, c));
+    // GQA (score_mma_kernel, 2 CTAs / SM): per-item q preparation is
+    // costly, so long items, ~14 per SM: 1024..8192 positions
+    c = (work + 148LL * 14 - 1) / (148LL * 14);
+    c = std::max<long long>(1024, std::min<long long>(8192, c));
   } else {
     // MHA: ~48 items per SM (3 CTAs / SM), 256..2048 positions each
     c = (work + 148LL * 48 - 1) / (148LL * 48);
