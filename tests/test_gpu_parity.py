@@ -242,3 +242,26 @@ def test_fill_uniform_matches_seeded_rng(kc):
         kc.fill_uniform(t, 12345, offset=77, lo=-0.05, hi=0.05)
         want = synth(12345, np.arange(77, 77 + 10007, dtype=np.uint64), -0.05, 0.05, name)
         np.testing.assert_array_equal(t.float().cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("dtype", ["f16", "bf16"])
+@pytest.mark.parametrize("G", [2, 4, 8])
+def test_gqa_tensor_core_scoring_precision(kc, oracle, dtype, G):
+    """The GQA scoring runs on the tensor cores with q split into fp16 hi+lo
+    (scaled so the head's max |q| sits at 2^14) or three bf16 parts; with q
+    elements spread over three decades the result must still meet the parity
+    rules against the fp32 oracle and match the CUDA-core path."""
+    b, n_kv, h, s, N = 2, 2, 128, 1500, 48
+    n = n_kv * G
+    cache, ks, vs = build_cache(kc, b, n, n_kv, h, s, dtype)
+    rng = np.random.default_rng(G)
+    q = (rng.uniform(-1, 1, (b, n * h)) * 10.0 ** rng.uniform(-3, 0, (b, n * h))).astype(np.float32)
+    res = kc.decode_attention_topn(q, cache, 0, N, False)
+    compare_all(oracle, res, q, ks[0], vs[0], b, n, n_kv, h, s, N, False)
+    cache.set_tuning("score_mma", 0)
+    ref = kc.decode_attention_topn(q, cache, 0, N, False)
+    cache.set_tuning("score_mma", 1)
+    same = np.mean([np.array_equal(a, c) for a, c in zip(res.selection.indices, ref.selection.indices)])
+    assert same >= 0.9
+    np.testing.assert_allclose(res.out, ref.out, rtol=1e-3, atol=1e-6)
+    cache.close()
