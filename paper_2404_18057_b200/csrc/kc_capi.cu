@@ -175,9 +175,9 @@ struct kc_cache {
   PinnedBuf idx_host[kRing], stage_host[kRing];
   DevBuf stage_dev[kRing];
   std::unique_ptr<kc::GatherPool> pool;
-  cudaStream_t main_st = nullptr, side_st = nullptr, gather_st = nullptr;
+  cudaStream_t main_st = nullptr, side_st = nullptr, gather_st = nullptr, out_st = nullptr;
   cudaEvent_t ev_start = nullptr, ev_end = nullptr, ev_sel[kRing] = {}, ev_rec[kRing] = {},
-              ev_gath[kRing] = {}, ev_scored[kRing] = {};
+              ev_gath[kRing] = {}, ev_scored[kRing] = {}, ev_out[kRing] = {};
 
   // tuning
   int score_chunk = 0;
@@ -313,6 +313,7 @@ void destroy(kc_cache* c) {
   if (c->main_st) cudaStreamSynchronize(c->main_st);
   if (c->side_st) cudaStreamSynchronize(c->side_st);
   if (c->gather_st) cudaStreamSynchronize(c->gather_st);
+  if (c->out_st) cudaStreamSynchronize(c->out_st);
   cudaDeviceSynchronize();
   c->pool.reset();
   for (int i = 0; i < kRing; ++i) {
@@ -322,6 +323,7 @@ void destroy(kc_cache* c) {
     if (c->ev_gath[i]) cudaEventDestroy(c->ev_gath[i]);
   }
   if (c->gather_st) cudaStreamDestroy(c->gather_st);
+  if (c->out_st) cudaStreamDestroy(c->out_st);
   if (c->k_arena) cudaFree(c->k_arena);
   if (c->v_dev) cudaFree(c->v_dev);
   if (c->v_host) {
@@ -337,6 +339,7 @@ void destroy(kc_cache* c) {
     c->norm[i].release(); c->out_tmp[i].release(); c->idx_exp[i].release();
     if (c->ev_sel[i]) cudaEventDestroy(c->ev_sel[i]);
     if (c->ev_scored[i]) cudaEventDestroy(c->ev_scored[i]);
+    if (c->ev_out[i]) cudaEventDestroy(c->ev_out[i]);
     if (c->ev_rec[i]) cudaEventDestroy(c->ev_rec[i]);
   }
   c->host_in.release();
@@ -724,19 +727,28 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
       if (o.dropped_mass)
         CK(cudaMemcpyAsync(o.dropped_mass, c->dropped[slot].p, o_dr, cudaMemcpyDeviceToDevice, side));
     } else {
-      // D2H straight into pinned user buffers, else into pinned staging
+      // D2H straight into pinned user buffers, else into pinned staging; on
+      // their own stream so the next layer's recall does not queue behind them
+      cudaStream_t ost = side != st ? c->out_st : st;
+      if (ost != side) {
+        CK(cudaEventRecord(c->ev_out[slot], side));
+        CK(cudaStreamWaitEvent(ost, c->ev_out[slot], 0));
+      }
       char* hb = (char*)c->host_out.p + i * per_layer;
       auto d2h = [&](void* user, size_t off, const void* src, size_t bytes) {
         if (!user) return;
         void* dst = host_pinned(user) ? user : (void*)(hb + off);
-        CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, side));
+        CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ost));
       };
       d2h(o.out, 0, c->out_tmp[slot].p, o_out);
       d2h(o.indices, o_out, idx_slots, o_idx);
       d2h(o.weights, o_out + o_idx, c->w[slot].p, o_w);
       d2h(o.dropped_mass, o_out + o_idx + o_w, c->dropped[slot].p, o_dr);
+      // the ring slot is free once its outputs have left the device (the main
+      // stream waits on ev_rec before reusing it)
+      if (ost != side) CK(cudaEventRecord(c->ev_rec[slot], ost));
     }
-    CK(cudaEventRecord(c->ev_rec[slot], side));
+    if (io_device || side == st) CK(cudaEventRecord(c->ev_rec[slot], side));
     CK(cudaGetLastError());
 
     // ledger: gather_v charges bytes * sum(counts) * h for offloaded layers
@@ -752,6 +764,10 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
   if (side != st) {
     CK(cudaEventRecord(c->ev_end, side));
     CK(cudaStreamWaitEvent(st, c->ev_end, 0));
+    if (!io_device) {
+      CK(cudaEventRecord(c->ev_end, c->out_st));
+      CK(cudaStreamWaitEvent(st, c->ev_end, 0));
+    }
   }
   if (!io_device) {
     CK(cudaStreamSynchronize(st));
@@ -840,11 +856,13 @@ int kc_cache_create(const kc_config* cfg, uint64_t batch, uint64_t resident_laye
       CK(cudaStreamCreateWithFlags(&c->main_st, cudaStreamNonBlocking));
       CK(cudaStreamCreateWithPriority(&c->side_st, cudaStreamNonBlocking, hi));
       CK(cudaStreamCreateWithPriority(&c->gather_st, cudaStreamNonBlocking, hi));
+      CK(cudaStreamCreateWithFlags(&c->out_st, cudaStreamNonBlocking));
       CK(cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming));
       CK(cudaEventCreateWithFlags(&c->ev_end, cudaEventDisableTiming));
       for (int i = 0; i < kRing; ++i) {
         CK(cudaEventCreateWithFlags(&c->ev_sel[i], cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&c->ev_scored[i], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&c->ev_out[i], cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&c->ev_rec[i], cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&c->ev_gath[i], cudaEventDisableTiming));
       }
