@@ -193,6 +193,7 @@ struct kc_cache {
   int host_frac_pct = 50;  // hybrid recall: % of rows gathered by host threads
   int auto_recall_mode = kRecallZeroCopy;  // what recall_mode 0 resolves to
   int score_groups = 0;   // row groups per layer (score -> select -> recall each); 0 = auto
+  int tlb_ahead = -1;      // K translation warm-up distance in rows (-1 auto: ~3 CTA waves, 0 off); r01: -2 %
   int score_mma = 1;       // GQA scoring on the tensor cores (TF32 split-q mma.sync)
   int k_policy = 0;        // L2 policy of the K stream (kc_device.cuh l2_policy)
   // MHA candidate selection: 0 auto (rows longer than the register-resident
@@ -488,6 +489,9 @@ void enqueue_score(kc_cache* c, uint64_t layer, const float* q32, const StepGeom
   sp.ctas_per_sm = c->score_ctas_per_sm;
   sp.k_policy = c->k_policy;
   sp.use_mma = c->score_mma;
+  // ~3 waves of CTAs ahead (one CTA per item, 3 per SM)
+  sp.tlb_ahead = c->tlb_ahead >= 0 ? c->tlb_ahead
+                                    : std::max(1, (3 * kc::sm_count() + g.n_splits - 1) / std::max(g.n_splits, 1));
   c->timed(0, st, [&] { kc::score_launch(sp, c->dtype, st); });
 }
 
@@ -1265,6 +1269,7 @@ int kc_set_tuning(kc_cache* c, const char* key, int64_t value) {
       c->select_cand = (int)value;
     }
     else if (k == "k_policy") c->k_policy = (int)value;
+    else if (k == "tlb_ahead") c->tlb_ahead = (int)value;
     else if (k == "score_mma") c->score_mma = (int)std::max<int64_t>(0, std::min<int64_t>(2, value));
     else if (k == "cand_force_fallback") c->cand_force_fallback = value ? 1 : 0;
     else if (k == "score_groups") {

@@ -42,6 +42,7 @@ struct ScoreParams {
   int cand_nc;          // 0: dense logits
   int k_policy;         // L2 policy of the K stream (0 evict_first; see l2_policy)
   int use_mma;          // GQA (2 <= G <= 8): tensor-core scoring (score_mma_kernel)
+  int tlb_ahead;        // rows ahead whose K translations the producer warms (0: off)
 };
 // Read `bytes` of a scratch buffer larger than L2: evicts (and so writes back)
 // every dirty L2 line, after which all stored K is clean in DRAM.
@@ -50,6 +51,8 @@ void l2_flush_launch(const void* scratch, size_t bytes, cudaStream_t st);
 void score_launch(const ScoreParams& p, int dtype, cudaStream_t st);
 // positions per CTA for a given shape (tuning override when > 0)
 int score_pick_chunk(int s, int rows, int override_chunk, int G = 1);
+// SMs of the current device
+int sm_count();
 // whether the candidate-mode scoring kernel covers this shape
 bool score_cand_supported(int dtype, int h, int G, int chunk, int nc);
 

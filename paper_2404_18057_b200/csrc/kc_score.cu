@@ -83,10 +83,23 @@ __device__ __forceinline__ void produce_k(const ScoreParams& p, uint8_t* ring, u
   };
   for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
     const int row = p.row0 + item / p.n_splits;
-    const int pos0 = (item - (row - p.row0) * p.n_splits) * p.chunk;
+    const int split = item - (row - p.row0) * p.n_splits;
+    const int pos0 = split * p.chunk;
     const int npos = min(p.chunk, p.s - pos0);
     const int n_it = (npos + kRows - 1) / kRows;
     const T* kslot = static_cast<const T*>(p.k) + (size_t)row * p.max_seq * kH;
+    if (p.tlb_ahead > 0 && lane == 0) {
+      // warm the address translation of a row the CTAs launched ~3 waves
+      // later will stream (one touch per 2 MB page of its K run): their
+      // first TMA then does not queue behind the recall's page walks
+      const int r2 = row + p.tlb_ahead;
+      const size_t row_bytes = (size_t)p.s * ROWB;
+      const size_t off = (size_t)split << 21;
+      if (r2 < p.row0 + p.rows && off < row_bytes) {
+        const char* a = reinterpret_cast<const char*>(static_cast<const T*>(p.k) + (size_t)r2 * p.max_seq * kH) + off;
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
+      }
+    }
     for (int it = 0; it < n_it; ++it, ++g) {
       const int st = (int)(g % STAGES);
       if (g >= (uint32_t)STAGES) mbar_wait(&empty[st], ((g / STAGES) - 1) & 1);
@@ -988,6 +1001,8 @@ int score_pick_chunk(int s, int rows, int override_chunk, int G) {
   c = ((c + kRows - 1) / kRows) * kRows;
   return (int)c;
 }
+
+int sm_count() { return num_sms(); }
 
 bool full_fast_launch(const FullParams& p, int dtype, cudaStream_t st) {
   if (dtype == KC_F16) return try_full<__half>(p, st);
