@@ -26,6 +26,8 @@ METRICS = [
     "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
     "launch__shared_mem_per_block_dynamic", "launch__occupancy_limit_registers", "launch__occupancy_limit_shared_mem",
     "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", "pcie__read_bytes.sum",
+    "pcie__read_bytes.sum.per_second", "pcie__write_bytes.sum.per_second",
+    "syslts__t_sectors_srcunit_tex_aperture_sysmem_op_read_lookup_miss.sum",
     "pcie__throughput.avg.pct_of_peak_sustained_elapsed", "smsp__average_warp_latency_issue_stalled_long_scoreboard",
 ]
 
