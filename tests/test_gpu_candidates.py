@@ -17,7 +17,7 @@ from tests.test_gpu_parity import build_cache, compare_all
 pytestmark = pytest.mark.gpu
 
 DEFAULTS = {"select_cand": 0, "cand_force_fallback": 0, "score_groups": 0, "recall_mode": 0, "score_chunk": 0,
-            "recall_pipe": 0, "score_mma": 1, "recall_ctas": 32}
+            "recall_pipe": 0, "score_mma": 1, "recall_ctas": 32, "select_on_side": 0, "tlb_ahead": -1}
 
 
 def _run(kc, cache, q, N, renorm=False, **tune):
@@ -113,15 +113,19 @@ def test_underflow_ties_take_lowest_positions(kc, oracle):
 
 @pytest.mark.parametrize("tune", [dict(score_groups=2), dict(score_groups=5), dict(recall_mode=2),
                                   dict(recall_mode=3), dict(select_cand=1), dict(select_cand=1, score_groups=3),
-                                  dict(recall_pipe=1), dict(recall_pipe=1, recall_ctas=0), dict(score_chunk=4096)],
+                                  dict(recall_pipe=1), dict(recall_pipe=1, recall_ctas=0), dict(select_on_side=1),
+                                  dict(tlb_ahead=0), dict(score_chunk=4096)],
                          ids=["groups2", "groups5", "dma", "hybrid", "cand", "cand-groups3", "recall-pipe",
-                              "recall-pipe-per-row", "chunk4096"])
-def test_pipeline_variants_bitwise(kc, tune):
+                              "recall-pipe-per-row", "side-select", "no-tlb-warm", "chunk4096"])
+@pytest.mark.parametrize("n_kv", [8, 2], ids=["mha", "gqa4"])
+def test_pipeline_variants_bitwise(kc, tune, n_kv):
     """Row groups, host-gather DMA recall, the hybrid recall and candidate
     selection reproduce the default path bit for bit; another split length
     changes only the rounding of the softmax statistics."""
     b, n, h, s, N, L = 2, 8, 128, 3000, 64, 3
-    cache, ks, vs = build_cache(kc, b, n, n, h, s, "f16", n_layers=L)
+    if n_kv != n and "select_cand" in tune:
+        pytest.skip("candidate selection is MHA-only")
+    cache, ks, vs = build_cache(kc, b, n, n_kv, h, s, "f16", n_layers=L)
     qs = [synth_matrix(10 + l, b, n * h) for l in range(L)]
     nc = min(N, s)
 
