@@ -380,8 +380,27 @@ __global__ void __launch_bounds__(kT, 1) select_reg_kernel(const SelectParams p)
 #pragma unroll
     for (int i = 0; i < KPT; ++i)
       if (j0 + i < s) tmax = max(tmax, key[i]);
-    uint32_t tau, dummy;
-    radix_threshold<1>(S, [&](int, bool& v) { v = true; return tmax; }, nc, kT, tau, dummy);
+    // tau = min over warps of the warp's kw-th largest thread maximum
+    // (kw = ceil(nc / 32)): every warp holds >= kw maxima >= tau, so >= nc
+    // keys are >= tau. Warp-local (REDUX + BALLOT), one block barrier --
+    // ~2.3x more candidates than the exact nc-th maximum, far fewer barriers.
+    uint32_t tau;
+    {
+      const int lane = tid & 31, warp = tid >> 5;
+      const int kw = (nc + 31) / 32;
+      uint32_t v = tmax, kth = 0;
+      for (int r = 0; r < kw; ++r) {
+        kth = __reduce_max_sync(0xffffffffu, v);
+        const uint32_t ball = __ballot_sync(0xffffffffu, v == kth);
+        if (lane == __ffs(ball) - 1) v = 0u;
+      }
+      if (lane == 0) S.wa[warp] = kth;
+      __syncthreads();
+      tau = S.wa[0];
+#pragma unroll 8
+      for (int w = 1; w < kNW; ++w) tau = min(tau, S.wa[w]);
+      __syncthreads();  // S.wa is reused by the scans below
+    }
     if (G == 1) {
       // a score just below tau can still share the N-th score's p (p-tie):
       // lower the bound by the tie window (keys are ordered logit bits)
