@@ -40,6 +40,7 @@ constexpr int kT = 1024;
 constexpr int kNW = kT / 32;
 constexpr int kBins = 2048;
 constexpr int kMaxG = 32;
+constexpr int kCandSmem = 4096;  // select_kernel fast path: candidates held in shared memory
 
 struct SelShared {
   uint32_t hist[kBins];
@@ -563,15 +564,144 @@ __global__ void __launch_bounds__(kT) select_kernel(const SelectParams p) {
   const int s = p.s, nc = p.nc;
   load_stats(S, p, b, kvh);
 
-  for (int j = tid; j < s; j += kT) {
-    float acc = 0.0f;
-    for (int g = 0; g < G; ++g) {
-      const float pg = expf(lbase[(size_t)g * p.lstride + j] - S.M[g]) / S.Z[g];
-      acc = (g == 0) ? pg : acc + pg;
+  // keys: MHA the exact p (its bits order like p, ties exact); GQA the
+  // ranking key sum_g p_g with the fast exp and a reciprocal (ranking only --
+  // the weights below are recomputed exactly), four positions per thread step
+  uint32_t tmax = 0;
+  if (G == 1) {
+    for (int j = tid; j < s; j += kT) {
+      const uint32_t k = __float_as_uint(expf(lbase[j] - S.M[0]) / S.Z[0]);
+      keys[j] = k;
+      tmax = max(tmax, k);
     }
-    keys[j] = __float_as_uint(acc);
+  } else {
+    for (int j4 = tid * 4; j4 < s; j4 += kT * 4) {
+      float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+      for (int g = 0; g < G; ++g) {
+        const float* lr = lbase + (size_t)g * p.lstride;
+        const float Mg = S.M[g], rZ = 1.0f / S.Z[g];
+        float e[4];
+        if (j4 + 4 <= s) {
+          const float4 v = *reinterpret_cast<const float4*>(lr + j4);
+          e[0] = v.x; e[1] = v.y; e[2] = v.z; e[3] = v.w;
+        } else {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) e[u] = j4 + u < s ? lr[j4 + u] : -INFINITY;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) acc[u] += __expf(e[u] - Mg) * rZ;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (j4 + u < s) {
+          const uint32_t k = __float_as_uint(acc[u]);
+          keys[j4 + u] = k;
+          tmax = max(tmax, k);
+        }
+      }
+    }
   }
   __syncthreads();
+
+  // ---- fast path: bound from the thread maxima, exact select on the few
+  // candidates (keys are bits of p: exact order, no tie window needed) ----
+  if (nc < s && nc <= kT) {
+    __shared__ uint32_t ckey[kCandSmem], cpos[kCandSmem];
+    const int kw = (nc + 31) / 32;
+    uint32_t v = tmax, kth = 0;
+    for (int r = 0; r < kw; ++r) {
+      kth = __reduce_max_sync(0xffffffffu, v);
+      const uint32_t ball = __ballot_sync(0xffffffffu, v == kth);
+      if (lane == __ffs(ball) - 1) v = 0u;
+    }
+    if (lane == 0) S.wa[warp] = kth;
+    __syncthreads();
+    uint32_t tau = S.wa[0];
+    for (int w = 1; w < kNW; ++w) tau = min(tau, S.wa[w]);
+    __syncthreads();
+    // candidates >= tau, compacted in position order (warp segments)
+    const int seg = (((s + kNW - 1) / kNW) + 31) & ~31;
+    const int w0 = warp * seg, w1 = min(s, w0 + seg);
+    uint32_t cnt = 0;
+    for (int j0 = w0; j0 < w1; j0 += 32) {
+      const int j = j0 + lane;
+      cnt += __popc(__ballot_sync(0xffffffffu, j < w1 && keys[j] >= tau));
+    }
+    if (lane == 0) S.wb[warp] = cnt;
+    __syncthreads();
+    uint32_t base = 0, C = 0;
+    for (int w = 0; w < kNW; ++w) {
+      const uint32_t c = S.wb[w];
+      base += (w < warp) ? c : 0u;
+      C += c;
+    }
+    if (C <= (uint32_t)kCandSmem) {
+      const uint32_t lt = lanemask_lt();
+      for (int j0 = w0; j0 < w1; j0 += 32) {
+        const int j = j0 + lane;
+        const uint32_t k = j < w1 ? keys[j] : 0u;
+        const bool take = j < w1 && k >= tau;
+        const uint32_t bal = __ballot_sync(0xffffffffu, take);
+        if (take) {
+          const uint32_t o = base + __popc(bal & lt);
+          ckey[o] = k;
+          cpos[o] = (uint32_t)j;
+        }
+        base += __popc(bal);
+      }
+      __syncthreads();
+      constexpr int CK = kCandSmem / kT;
+      const int c0 = tid * CK;
+      uint32_t key[CK];
+#pragma unroll
+      for (int i = 0; i < CK; ++i) key[i] = c0 + i < (int)C ? ckey[c0 + i] : 0u;
+      uint32_t T2 = 0, k_eq2 = (uint32_t)nc;
+      radix_threshold<CK>(S, [&](int i, bool& vld) { vld = c0 + i < (int)C; return key[i]; }, nc, (int)C, T2, k_eq2);
+      uint32_t cls_gt = 0, cls_eq = 0;
+#pragma unroll
+      for (int i = 0; i < CK; ++i) {
+        if (c0 + i >= (int)C) continue;
+        if ((uint32_t)nc >= C || key[i] > T2) cls_gt |= 1u << i;
+        else if (key[i] == T2) cls_eq |= 1u << i;
+      }
+      const uint32_t n_gt_local = __popc(cls_gt);
+      uint32_t n_gt_total;
+      {
+        const uint32_t b0 = block_excl_scan(n_gt_local, S.wc);
+        if (tid == kT - 1) S.need = b0 + n_gt_local;
+        __syncthreads();
+        n_gt_total = S.need;
+        __syncthreads();
+      }
+      const uint32_t keq = (uint32_t)nc - n_gt_total;
+      const uint32_t ceq = __popc(cls_eq);
+      const uint32_t eq_base = block_excl_scan(ceq, S.wa);
+      const uint32_t takeq = eq_base >= keq ? 0u : min(ceq, keq - eq_base);
+      uint32_t o = block_excl_scan(n_gt_local + takeq, S.wb);
+      uint32_t eqr = eq_base;
+#pragma unroll
+      for (int i = 0; i < CK; ++i) {
+        bool sel = (cls_gt >> i) & 1u;
+        if ((cls_eq >> i) & 1u) {
+          sel = eqr < keq;
+          ++eqr;
+        }
+        if (sel) {
+          const uint32_t j = cpos[c0 + i];
+          idx[o] = j;
+          for (int g = 0; g < G; ++g)
+            p.w[((size_t)b * n_q + kvh * G + g) * nc + o] =
+                expf(lbase[(size_t)g * p.lstride + j] - S.M[g]) / S.Z[g];
+          ++o;
+        }
+      }
+      __syncthreads();
+      if (!p.keep_logits) drop_rows(lbase, p.lstride, G, s);
+      drop_rows(reinterpret_cast<const float*>(keys), 0, 1, s);
+      finish_group(S, p, b, kvh);
+      return;
+    }
+  }
 
   // strided radix passes over the scratch row
   uint32_t T = 0, k_eq = (uint32_t)nc;

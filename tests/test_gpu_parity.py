@@ -265,3 +265,19 @@ def test_gqa_tensor_core_scoring_precision(kc, oracle, dtype, G):
     assert same >= 0.9
     np.testing.assert_allclose(res.out, ref.out, rtol=1e-3, atol=1e-6)
     cache.close()
+
+
+@pytest.mark.parametrize("case", [(1, 8, 2, 40000, 64, "f16"), (1, 4, 4, 36000, 300, "bf16")],
+                         ids=["gqa-40k", "mha-36k-N300"])
+def test_long_rows_global_key_selection(kc, oracle, case):
+    """Rows longer than the register-resident selection (32 k positions) that
+    candidate mode does not cover (GQA, N > 256) go through select_kernel:
+    keys in a global scratch row, bound from the thread maxima, exact
+    selection of the candidates in shared memory."""
+    b, n, n_kv, s, N, dtype = case
+    h = 128
+    cache, ks, vs = build_cache(kc, b, n, n_kv, h, s, dtype)
+    q = synth_matrix(1, b, n * h, dtype=dtype)
+    res = kc.decode_attention_topn(q, cache, 0, N, False)
+    compare_all(oracle, res, q, ks[0], vs[0], b, n, n_kv, h, s, N, False)
+    cache.close()
