@@ -957,7 +957,7 @@ bool try_fast(const ScoreParams& p, cudaStream_t st) {
     return true;
   }
   if (p.cand_nc > 0) {
-    if (p.G != 1 || p.chunk > kMaxCandChunk || p.cand_nc > kCWarps * 32) return false;
+    if (p.G != 1 || p.chunk > kMaxCandChunk || p.cand_nc > kCWarps * 16) return false;
     launch_fast<T, 1, 4, true>(p, st);
     return true;
   }
@@ -1011,8 +1011,10 @@ bool full_fast_launch(const FullParams& p, int dtype, cudaStream_t st) {
 }
 
 bool score_cand_supported(int dtype, int h, int G, int chunk, int nc) {
+  // nc <= 128: the bound is the nc-th largest of the 256 consumer threads'
+  // block maxima; with nc close to 256 it keeps nearly every position
   return (dtype == KC_F16 || dtype == KC_BF16) && h == kH && G == 1 && chunk % kRows == 0 &&
-         chunk <= kMaxCandChunk && nc >= 1 && nc <= kCWarps * 32;
+         chunk <= kMaxCandChunk && nc >= 1 && nc <= kCWarps * 16;
 }
 
 void score_launch(const ScoreParams& p, int dtype, cudaStream_t st) {

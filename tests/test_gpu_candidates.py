@@ -42,7 +42,8 @@ CASES = [
     (2, 4, 128, 300, 32, "f16"),
     (1, 8, 128, 5000, 128, "f16"),     # several splits, ragged last split
     (2, 4, 128, 4097, 1, "bf16"),      # N = 1
-    (1, 4, 128, 3000, 256, "f16"),     # N = 256 (the candidate-mode maximum)
+    (1, 4, 128, 3000, 128, "f16"),     # N = 128 (the candidate-mode maximum)
+    (1, 4, 128, 3000, 256, "f16"),     # N = 256: dense path
     (1, 4, 128, 2000, 300, "f16"),     # N > 256: dense path
     (1, 2, 128, 100, 128, "bf16"),     # N >= s: everything selected
     (2, 4, 128, 40000, 128, "f16"),    # s > 32k: dense fallback is the global-keys kernel
