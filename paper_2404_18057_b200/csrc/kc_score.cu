@@ -994,9 +994,11 @@ int score_pick_chunk(int s, int rows, int override_chunk, int G) {
     c = (work + 148LL * 14 - 1) / (148LL * 14);
     c = std::max<long long>(1024, std::min<long long>(8192, c));
   } else {
-    // MHA: ~48 items per SM (3 CTAs / SM), 256..2048 positions each
+    // MHA: ~48 items per SM (3 CTAs / SM; small items balance best against
+    // the concurrent recall), 1024..2048 positions each (shorter items pay
+    // their ramp-up: 4k context 70 -> 54 us per layer at 1024)
     c = (work + 148LL * 48 - 1) / (148LL * 48);
-    c = std::max<long long>(256, std::min<long long>(2048, c));
+    c = std::max<long long>(1024, std::min<long long>(2048, c));
   }
   c = ((c + kRows - 1) / kRows) * kRows;
   return (int)c;
