@@ -579,17 +579,16 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
                           : 0;
     const bool dma = host_rows > 0;
     // Row groups: score -> select -> recall per group of (batch, kv head)
-    // rows, so only one group's fp32 logits are live in L2 at a time (the L2
-    // keeps the GPU page-table lines the zero-copy recall walks).
+    // rows, so the recall of group g overlaps the scoring of group g+1.
     // score_groups 0 = auto: one group when layers pipeline against each
     // other, two for a single-layer call (the engine's per-layer block),
     // where only the intra-layer overlap is available (r01: 730 -> 690 us)
     const int64_t want_groups = c->score_groups > 0 ? c->score_groups : (n == 1 ? 2 : 1);
     const int n_groups = dma ? 1 : (int)std::max<int64_t>(1, std::min<int64_t>(want_groups, (int64_t)c->rows));
-    // Candidate mode (MHA): scoring emits only each split's possible top-N
-    // positions instead of 4 B of fp32 logit per position -- the dense logits
-    // (32 MiB per C2 layer) would evict the GPU page-table lines the zero-copy
-    // recall walks from L2.
+    // Candidate mode (MHA, N <= 128): scoring emits only each split's
+    // possible top-N positions instead of an fp32 logit per position, and the
+    // selection ranks ~1.3 N per split -- automatic for rows longer than the
+    // register-resident dense selection.
     const bool cand = (c->select_cand == 1 || (c->select_cand == 0 && g.s > kc::kDenseRegMaxS)) &&
                       !c->select_global && kc::score_cand_supported(c->dtype, (int)c->h, (int)c->G, g.chunk, g.nc);
     if (cand) {

@@ -3,12 +3,12 @@
 // contiguous pinned staging block, which one cudaMemcpyAsync then moves to
 // HBM at full DMA rate.
 //
-// Why (measured on the B200 box, tools/h2d_probe2.cu, profiles/): zero-copy
-// SM loads of scattered 256-B rows run at 45 GB/s on an idle GPU but drop to
-// ~24 GB/s right after the scoring kernel streams >= 96 MB through L2, while
-// a contiguous 8 MiB DMA holds 52 GB/s regardless and leaves every SM to
-// scoring. This is the reference's gather_v (proj/core/src/kv_cache.cpp:
-// 150-187) done where the slow tier lives.
+// Why it exists: zero-copy SM loads of scattered 256-B rows cost one GPU
+// page walk per row (tools/tlb_probe.cu), while a
+// contiguous DMA needs none. This is the reference's gather_v
+// (proj/core/src/kv_cache.cpp:150-187) done where the slow tier lives.
+// Measured on the 16-vCPU box the host side is the limit (20-26 GB/s), so it
+// is an option (recall_mode 2 / 3), not the default.
 #pragma once
 
 #include <immintrin.h>

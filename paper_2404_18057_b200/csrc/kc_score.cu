@@ -19,8 +19,8 @@
 // fp32, log2(LPR) xor-shuffles per row. Writes fp32 logits (score * scale, the
 // multiply after the sum like dot_scaled) and a per-split online (max, sum
 // exp) per q head; softmax_stats combines the splits into the global softmax.
-// After a stage is consumed the producer warp drops its K lines from L2 (see
-// DESIGN.md section 5).
+// As soon as a stage has landed the producer warp drops its K lines from L2
+// (produce_k below).
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
