@@ -177,7 +177,8 @@ struct kc_cache {
   std::unique_ptr<kc::GatherPool> pool;
   cudaStream_t main_st = nullptr, side_st = nullptr, gather_st = nullptr, out_st = nullptr;
   cudaEvent_t ev_start = nullptr, ev_end = nullptr, ev_sel[kRing] = {}, ev_rec[kRing] = {},
-              ev_gath[kRing] = {}, ev_scored[kRing] = {}, ev_out[kRing] = {};
+              ev_gath[kRing] = {}, ev_scored[kRing] = {}, ev_out[kRing] = {}, ev_cp[kRing] = {};
+  bool cp_pending[kRing] = {};  // ev_cp[slot] guards a device-mode copy of that slot
 
   // tuning
   int score_chunk = 0;
@@ -341,6 +342,7 @@ void destroy(kc_cache* c) {
     if (c->ev_sel[i]) cudaEventDestroy(c->ev_sel[i]);
     if (c->ev_scored[i]) cudaEventDestroy(c->ev_scored[i]);
     if (c->ev_out[i]) cudaEventDestroy(c->ev_out[i]);
+    if (c->ev_cp[i]) cudaEventDestroy(c->ev_cp[i]);
     if (c->ev_rec[i]) cudaEventDestroy(c->ev_rec[i]);
   }
   c->host_in.release();
@@ -607,6 +609,7 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
         CK(cudaStreamWaitEvent(side, c->ev_scored[slot], 0));
       } else if (gi == 0 && i >= (uint64_t)kRing && side != st) {
         CK(cudaStreamWaitEvent(st, c->ev_rec[slot], 0));
+        if (c->cp_pending[slot]) CK(cudaStreamWaitEvent(st, c->ev_cp[slot], 0));
       }
 
       kc::SelectParams sp{};
@@ -718,17 +721,25 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
       });
     }
 
+    // device mode: the selection outputs depend on the selection only --
+    // expand + copy them on their own stream so the side stream runs nothing
+    // but recalls (the recall writes o.out itself)
+    const bool dev_copies = io_device && (o.indices || o.weights || o.dropped_mass);
+    cudaStream_t cst = (dev_copies && side != st) ? c->out_st : side;
+    if (cst != side) CK(cudaStreamWaitEvent(cst, c->ev_sel[slot], 0));
+    c->cp_pending[slot] = cst != side;
     const uint32_t* idx_slots = c->idx[slot].as<uint32_t>();
     if (c->G > 1 && (o.indices || !io_device)) {
       kc::expand_idx_launch(idx_slots, c->idx_exp[slot].as<uint32_t>(), (int)c->rows, (int)c->G,
-                            g.nc, side);
+                            g.nc, io_device ? cst : side);
       idx_slots = c->idx_exp[slot].as<uint32_t>();
     }
     if (io_device) {
-      if (o.indices) CK(cudaMemcpyAsync(o.indices, idx_slots, o_idx, cudaMemcpyDeviceToDevice, side));
-      if (o.weights) CK(cudaMemcpyAsync(o.weights, c->w[slot].p, o_w, cudaMemcpyDeviceToDevice, side));
+      if (o.indices) CK(cudaMemcpyAsync(o.indices, idx_slots, o_idx, cudaMemcpyDeviceToDevice, cst));
+      if (o.weights) CK(cudaMemcpyAsync(o.weights, c->w[slot].p, o_w, cudaMemcpyDeviceToDevice, cst));
       if (o.dropped_mass)
-        CK(cudaMemcpyAsync(o.dropped_mass, c->dropped[slot].p, o_dr, cudaMemcpyDeviceToDevice, side));
+        CK(cudaMemcpyAsync(o.dropped_mass, c->dropped[slot].p, o_dr, cudaMemcpyDeviceToDevice, cst));
+      if (cst != side) CK(cudaEventRecord(c->ev_cp[slot], cst));
     } else {
       // D2H straight into pinned user buffers, else into pinned staging; on
       // their own stream so the next layer's recall does not queue behind them
@@ -767,10 +778,8 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
   if (side != st) {
     CK(cudaEventRecord(c->ev_end, side));
     CK(cudaStreamWaitEvent(st, c->ev_end, 0));
-    if (!io_device) {
-      CK(cudaEventRecord(c->ev_end, c->out_st));
-      CK(cudaStreamWaitEvent(st, c->ev_end, 0));
-    }
+    CK(cudaEventRecord(c->ev_end, c->out_st));  // host D2H / device selection copies
+    CK(cudaStreamWaitEvent(st, c->ev_end, 0));
   }
   if (!io_device) {
     CK(cudaStreamSynchronize(st));
@@ -866,6 +875,7 @@ int kc_cache_create(const kc_config* cfg, uint64_t batch, uint64_t resident_laye
         CK(cudaEventCreateWithFlags(&c->ev_sel[i], cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&c->ev_scored[i], cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&c->ev_out[i], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&c->ev_cp[i], cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&c->ev_rec[i], cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&c->ev_gath[i], cudaEventDisableTiming));
       }
