@@ -357,12 +357,8 @@ def run_ours(args, cfg):
     e2e_check = float(np.abs(outs_h[0]["out"]).sum())
     del outs_h, qh, qh_np
 
-    ms = ms_local
-    e2e_ms = e2e_ms_local
-    if world > 1:
-        t = torch.tensor([ms_local, e2e_ms_local], device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms, e2e_ms = float(t[0]), float(t[1])
+    from paper_2404_18057_b200.sharding import max_over_ranks
+    ms, e2e_ms = max_over_ranks([ms_local, e2e_ms_local], device=dev)
     cache.close()
     del qs, outs
     torch.cuda.empty_cache()
@@ -372,9 +368,8 @@ def run_ours(args, cfg):
     if not args.no_full_kv:
         full = full_kv_step(kc, torch, cfg, dev, local_rank, rank, args, barrier)
         if world > 1:
-            t = torch.tensor([full["ms_per_step"]], device=dev)
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            full["ms_per_step"] = float(t[0])
+            from paper_2404_18057_b200.sharding import max_over_ranks
+            full["ms_per_step"] = max_over_ranks([full["ms_per_step"]], device=dev)[0]
             full["hbm_gbs"] = full["kv_bytes_per_step"] / (full["ms_per_step"] * 1e-3) / 1e9
 
     if rank != 0:

@@ -87,3 +87,16 @@ def host_mem_available() -> int:
     except OSError:
         pass
     return 0
+
+
+def max_over_ranks(values, device=None):
+    """Element-wise max of per-rank timings over the default process group
+    (bench.py: the job's step time is the slowest rank's). A list of floats
+    in, the reduced list out; identity without an initialised group."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return list(values)
+    t = torch.tensor(list(values), dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return [float(x) for x in t.tolist()]

@@ -81,3 +81,31 @@ def test_gloo_world2_sharded_step_matches_unsharded():
         p.join(timeout=60)
     assert ok
     assert all(p.exitcode == 0 for p in procs)
+
+
+def _max_worker(rank, world, port, out):
+    import torch.distributed as dist
+
+    from paper_2404_18057_b200.sharding import max_over_ranks
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        got = max_over_ranks([10.0 + rank, 5.0 - rank, 1.5])
+        out.put((rank, got))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_bench_timing_is_the_slowest_rank():
+    """bench.py's step time is the element-wise max over ranks (gloo, world 2)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_max_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+    assert res[0] == res[1] == [11.0, 5.0, 1.5]
