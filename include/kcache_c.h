@@ -179,6 +179,12 @@ int kc_ledger_event(const kc_cache* cache, uint64_t i, int* phase, uint64_t* lay
 /* Device pointers of one layer's K and V storage (V may be a mapped host
  * pointer) and the element strides; for tests and tooling. */
 int kc_layer_storage(const kc_cache* cache, uint64_t layer, void** k, void** v, int* v_on_host);
+/* Where offloaded V lives: 0 = host-resident UVM managed memory, one
+ * allocation per layer (default), 1 = mmap + cudaHostRegister pinned arena
+ * (KCACHE_V_ARENA=pinned, or when managed memory is unavailable), 2 = no
+ * offloaded layer, 3 = the first layers managed, the rest pinned (the
+ * driver's managed-memory cap). */
+int kc_v_arena_kind(const kc_cache* cache, int* kind);
 /* Wait for all work the cache enqueued. */
 int kc_sync(kc_cache* cache);
 /* Tuning knobs ("score_chunk", "recall_ctas", ...); DESIGN.md lists them. */

@@ -156,7 +156,14 @@ struct kc_cache {
   void* k_arena = nullptr;
   size_t k_layer_bytes = 0;
   void* v_dev = nullptr;
-  void* v_host = nullptr;       // mmap'd, registered
+  // V of offloaded layers, in host memory. Default: one UVM managed
+  // allocation per layer, preferred location host (the GPU's NUMA node),
+  // remote-mapped into the GPU (AccessedBy) -- the driver maps it with large
+  // GPU pages, so the recall's scattered 256-B reads do not pay a page walk
+  // per 4 KB. KCACHE_V_ARENA=pinned selects the mmap +
+  // cudaHostRegister arena (4 KB GPU pages).
+  std::vector<void*> v_managed;  // [layer - L], same pointer on host and device
+  void* v_host = nullptr;       // pinned arena: mmap'd, registered
   void* v_host_dev = nullptr;   // device alias of v_host
   size_t v_host_bytes = 0;
   size_t v_layer_bytes = 0;
@@ -242,9 +249,19 @@ struct kc_cache {
   uint2* cand_buf(int lb) { return cand.as<uint2>() + (size_t)lb * rows * (size_t)lstride; }
   uint2* cand_meta_buf(int lb) { return cand_meta.as<uint2>() + (size_t)lb * rows * (size_t)max_splits; }
   void* k_layer(uint64_t layer) const { return (char*)k_arena + layer * k_layer_bytes; }
+  // offloaded layer j = layer - L: managed layers first, the rest (beyond the
+  // driver's managed-memory cap) in the pinned arena
   void* v_layer(uint64_t layer) const {
-    return layer < L ? (void*)((char*)v_dev + layer * v_layer_bytes)
-                     : (void*)((char*)v_host_dev + (layer - L) * v_layer_bytes);
+    if (layer < L) return (void*)((char*)v_dev + layer * v_layer_bytes);
+    const uint64_t j = layer - L;
+    if (j < v_managed.size()) return v_managed[j];
+    return (void*)((char*)v_host_dev + (j - v_managed.size()) * v_layer_bytes);
+  }
+  // host view of an offloaded layer's V (host gather path)
+  const char* v_host_layer(uint64_t layer) const {
+    const uint64_t j = layer - L;
+    if (j < v_managed.size()) return static_cast<const char*>(v_managed[j]);
+    return static_cast<const char*>(v_host) + (j - v_managed.size()) * v_layer_bytes;
   }
   bool v_in_slow(uint64_t layer) const { return layer >= L && layers[layer].offloaded; }
   void check_layer(uint64_t layer) const {
@@ -309,6 +326,45 @@ void* alloc_pinned_arena(size_t bytes, int numa_node, void** dev_alias) {
   return p;
 }
 
+// One managed allocation per offloaded layer: preferred location host (the
+// given NUMA node when known), accessed by the cache's GPU (remote mapping,
+// no migration), populated on the host up front. Allocates as many of the n
+// layers as the driver grants (its managed-memory cap was 64 GiB per process
+// on the r01 box) and returns how many; the caller puts the rest in the
+// pinned arena.
+uint64_t alloc_managed_layers(kc_cache* c, uint64_t n, int numa_node) {
+  int concurrent = 0;
+  cudaDeviceGetAttribute(&concurrent, cudaDevAttrConcurrentManagedAccess, c->device);
+  if (!concurrent) return 0;
+  cudaMemLocation host{};
+  host.type = numa_node >= 0 ? cudaMemLocationTypeHostNuma : cudaMemLocationTypeHost;
+  host.id = numa_node >= 0 ? numa_node : 0;
+  cudaMemLocation gpu{};
+  gpu.type = cudaMemLocationTypeDevice;
+  gpu.id = c->device;
+  auto stop = [&](const char* what, cudaError_t e, void* last) {
+    if (last) cudaFree(last);
+    cudaGetLastError();
+    fprintf(stderr, "kcache: %zu of %zu offloaded V layers in managed memory (%s: %s); the rest pinned\n",
+            c->v_managed.size(), (size_t)n, what, cudaGetErrorString(e));
+    return (uint64_t)c->v_managed.size();
+  };
+  for (uint64_t i = 0; i < n; ++i) {
+    void* p = nullptr;
+    cudaError_t e = cudaMallocManaged(&p, c->v_layer_bytes, cudaMemAttachGlobal);
+    if (e != cudaSuccess) return stop("cudaMallocManaged", e, nullptr);
+    if ((e = cudaMemAdvise(p, c->v_layer_bytes, cudaMemAdviseSetPreferredLocation, host)) != cudaSuccess)
+      return stop("SetPreferredLocation", e, p);
+    if ((e = cudaMemAdvise(p, c->v_layer_bytes, cudaMemAdviseSetAccessedBy, gpu)) != cudaSuccess)
+      return stop("SetAccessedBy", e, p);
+    if ((e = cudaMemPrefetchAsync(p, c->v_layer_bytes, host, 0, nullptr)) != cudaSuccess)
+      return stop("prefetch to host", e, p);
+    c->v_managed.push_back(p);
+  }
+  CK(cudaDeviceSynchronize());
+  return n;
+}
+
 void destroy(kc_cache* c) {
   if (!c) return;
   cudaSetDevice(c->device);
@@ -332,6 +388,8 @@ void destroy(kc_cache* c) {
     cudaHostUnregister(c->v_host);
     munmap(c->v_host, c->v_host_bytes);
   }
+  for (void* p : c->v_managed) cudaFree(p);
+  c->v_managed.clear();
   for (DevBuf* b : {&c->logits, &c->partials, &c->keys, &c->part_out, &c->stage_src, &c->stage_k,
                     &c->stage_v, &c->sel_rows, &c->sel_pos, &c->gather_out, &c->cand, &c->cand_meta,
                     &c->fb_flags, &c->part_ml, &c->step_dev})
@@ -671,7 +729,7 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
         CK(cudaMemcpyAsync(c->idx_host[slot].p, c->idx[slot].p, (size_t)host_rows * nc * 4, cudaMemcpyDeviceToHost,
                            c->gather_st));
         auto* job = new kc::GatherJob{c->pool.get(),
-                                      (const char*)c->v_host + (layer - c->L) * c->v_layer_bytes,
+                                      c->v_host_layer(layer),
                                       c->cfg.max_seq * c->h * c->esz,
                                       c->h * c->esz,
                                       static_cast<const uint32_t*>(c->idx_host[slot].p),
@@ -851,8 +909,13 @@ int kc_cache_create(const kc_config* cfg, uint64_t batch, uint64_t resident_laye
       CK(cudaMalloc(&c->k_arena, checked_mul({c->k_layer_bytes, cfg->n_layers})));
       if (c->L > 0) CK(cudaMalloc(&c->v_dev, checked_mul({c->v_layer_bytes, c->L})));
       if (cfg->n_layers > c->L) {
-        c->v_host_bytes = checked_mul({c->v_layer_bytes, cfg->n_layers - c->L});
-        c->v_host = alloc_pinned_arena(c->v_host_bytes, numa_node, &c->v_host_dev);
+        const uint64_t n_off = cfg->n_layers - c->L;
+        const char* kind = getenv("KCACHE_V_ARENA");
+        const uint64_t m = (kind && !strcmp(kind, "pinned")) ? 0 : alloc_managed_layers(c, n_off, numa_node);
+        if (m < n_off) {
+          c->v_host_bytes = checked_mul({c->v_layer_bytes, n_off - m});
+          c->v_host = alloc_pinned_arena(c->v_host_bytes, numa_node, &c->v_host_dev);
+        }
       }
       // rows padded to 128 B: the selection kernel drops them from L2 by line
       c->lstride = (int64_t)((cfg->max_seq + 31) & ~31ull);
@@ -1243,6 +1306,13 @@ int kc_layer_storage(const kc_cache* c, uint64_t layer, void** k, void** v, int*
     *v_on_host = layer >= c->L ? 1 : 0;
   });
 }
+int kc_v_arena_kind(const kc_cache* c, int* kind) {
+  return guarded([&] {
+    if (!kind) fail(KC_EARG, "kc_v_arena_kind: null argument");
+    *kind = c->v_managed.empty() ? (c->v_host ? 1 : 2) : (c->v_host ? 3 : 0);
+  });
+}
+
 int kc_sync(kc_cache* c) {
   return guarded([&] {
     set_dev(c);

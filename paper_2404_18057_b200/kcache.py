@@ -106,6 +106,7 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         "kc_ledger_event": (i32, [vp, u64, C.POINTER(i32), p64, C.POINTER(i32), p64, p64]),
         "kc_layer_storage": (i32, [vp, u64, C.POINTER(vp), C.POINTER(vp), C.POINTER(i32)]),
         "kc_sync": (i32, [vp]),
+        "kc_v_arena_kind": (i32, [vp, C.POINTER(i32)]),
         "kc_set_tuning": (i32, [vp, C.c_char_p, C.c_int64]),
         "kc_profile": (i32, [vp, i32]),
         "kc_profile_read": (i32, [vp, C.c_char_p, C.POINTER(C.c_double), p64]),
@@ -416,6 +417,12 @@ class TieredKVCache:
         k, v, on_host = C.c_void_p(), C.c_void_p(), C.c_int()
         _check(self._lib.kc_layer_storage(self._h, layer, C.byref(k), C.byref(v), C.byref(on_host)))
         return k.value, v.value, bool(on_host.value)
+
+    def v_arena_kind(self) -> str:
+        """'managed' (host-resident UVM, default), 'pinned', 'device' or 'mixed'."""
+        k = C.c_int()
+        _check(self._lib.kc_v_arena_kind(self._h, C.byref(k)))
+        return ("managed", "pinned", "device", "mixed")[k.value]
 
     def set_tuning(self, key: str, value: int) -> None:
         _check(self._lib.kc_set_tuning(self._h, key.encode(), int(value)))

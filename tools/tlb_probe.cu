@@ -114,7 +114,31 @@ int main(int argc, char** argv) {
   CK(cudaSetDevice(0));
   CU(cuInit(0));
   void* dev_ptr = nullptr;
-  if (!strcmp(method, "reg")) {
+  std::vector<char*> wbase;
+  if (!strcmp(method, "managed_split")) {
+    // one managed allocation per 2 GiB window (what the product does per layer)
+    cudaMemLocation cpu{};
+    cpu.type = cudaMemLocationTypeHost;
+    cpu.id = 0;
+    cudaMemLocation gpu{};
+    gpu.type = cudaMemLocationTypeDevice;
+    gpu.id = 0;
+    for (int w = 0; w < n_win; ++w) {
+      void* q = nullptr;
+      CK(cudaMallocManaged(&q, window));
+      CK(cudaMemAdvise(q, window, cudaMemAdviseSetPreferredLocation, cpu));
+      CK(cudaMemAdvise(q, window, cudaMemAdviseSetAccessedBy, gpu));
+      madvise(q, window, MADV_HUGEPAGE);
+      if (getenv("PROBE_PREFETCH")) {
+        CK(cudaMemPrefetchAsync(q, window, cpu, 0));
+      } else {
+        memset(q, 1, window);
+      }
+      wbase.push_back((char*)q);
+    }
+    CK(cudaDeviceSynchronize());
+    dev_ptr = wbase[0];
+  } else if (!strcmp(method, "reg")) {
     void* p = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS | MAP_NORESERVE, -1, 0);
     madvise(p, bytes, MADV_HUGEPAGE);
     CK(cudaHostRegister(p, bytes, cudaHostRegisterMapped | cudaHostRegisterPortable));
@@ -127,6 +151,24 @@ int main(int argc, char** argv) {
     }
     CK(cudaHostRegister(p, bytes, cudaHostRegisterMapped | cudaHostRegisterPortable));
     CK(cudaHostGetDevicePointer(&dev_ptr, p, 0));
+  } else if (!strcmp(method, "managed")) {
+    // UVM: host-preferred managed memory the GPU maps remotely (AccessedBy)
+    CK(cudaMallocManaged(&dev_ptr, bytes));
+    cudaMemLocation cpu{};
+    cpu.type = cudaMemLocationTypeHost;
+    cpu.id = 0;
+    cudaMemLocation gpu{};
+    gpu.type = cudaMemLocationTypeDevice;
+    gpu.id = 0;
+    CK(cudaMemAdvise(dev_ptr, bytes, cudaMemAdviseSetPreferredLocation, cpu));
+    CK(cudaMemAdvise(dev_ptr, bytes, cudaMemAdviseSetAccessedBy, gpu));
+    madvise(dev_ptr, bytes, MADV_HUGEPAGE);
+    if (getenv("PROBE_PREFETCH")) {
+      CK(cudaMemPrefetchAsync(dev_ptr, bytes, cpu, 0));  // populate on the host, driver-side
+      CK(cudaDeviceSynchronize());
+    } else {
+      memset(dev_ptr, 1, bytes);  // first touch on the CPU
+    }
   } else if (!strcmp(method, "alloc")) {
     void* p = nullptr;
     CK(cudaHostAlloc(&p, bytes, cudaHostAllocMapped | cudaHostAllocPortable));
@@ -162,8 +204,20 @@ int main(int argc, char** argv) {
       if (strstr(line, "AnonHugePages") || strstr(line, "HugePages_Total") || strstr(line, "HugePages_Free")) printf("%s", line);
     if (f) fclose(f);
   }
-  fill<<<148 * 4, 256>>>((uint4*)dev_ptr, bytes / 16);
-  CK(cudaDeviceSynchronize());
+  if (wbase.empty())
+    for (int w = 0; w < n_win; ++w) wbase.push_back((char*)dev_ptr + (size_t)w * window);
+  {
+    cudaEvent_t f0, f1;
+    CK(cudaEventCreate(&f0));
+    CK(cudaEventCreate(&f1));
+    CK(cudaEventRecord(f0));
+    for (int w = 0; w < n_win; ++w) fill<<<148 * 4, 256>>>((uint4*)wbase[w], window / 16);
+    CK(cudaEventRecord(f1));
+    CK(cudaDeviceSynchronize());
+    float fms = 0;
+    CK(cudaEventElapsedTime(&fms, f0, f1));
+    printf("GPU fill of the arena: %.1f ms (%.1f GB/s)\n", fms, bytes / (fms * 1e-3) / 1e9);
+  }
 
   std::mt19937 rng(7);
   std::vector<uint32_t> hidx((size_t)n_win * kRows * kSel);
@@ -213,7 +267,7 @@ int main(int argc, char** argv) {
         sw_off = (sw_off + sw_bytes) % sw_total;
       }
       CK(cudaEventRecord(a));
-      gather<<<ctas, 256>>>((const uint4*)((char*)dev_ptr + (size_t)w * window), didx + (size_t)w * kRows * kSel, sink);
+      gather<<<ctas, 256>>>((const uint4*)wbase[w], didx + (size_t)w * kRows * kSel, sink);
       CK(cudaEventRecord(b));
       CK(cudaEventSynchronize(b));
       float ms;
@@ -224,6 +278,13 @@ int main(int argc, char** argv) {
     if (rep < 2) continue;
     printf("pattern %d arena %zu GiB %s sweep=%d ctas=%d rep %d: gather %.1f us/window (%.1f GB/s)\n", pattern, gib, method, do_sweep,
            ctas, rep, us, (double)kRows * kSel * kRowB / (us * 1e-6) / 1e9);
+  }
+  if (!strcmp(method, "managed") || !strcmp(method, "reg") || !strcmp(method, "managed_split")) {
+    // host-side check of what the GPU wrote (managed: no migration expected)
+    const uint4* hp = (const uint4*)dev_ptr;
+    size_t bad = 0;
+    for (size_t i = 0; i < window / 16; i += 1000003) bad += hp[i].x != (uint32_t)i || hp[i].y != 1;
+    printf("host check: %zu mismatches\n", bad);
   }
   return 0;
 }
