@@ -704,10 +704,10 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
         sp.force_fallback = c->cand_force_fallback;
       }
       c->timed(1, selst, [&] {
-        if (!cand) {
+        if (cand) {
+          if (!kc::select_cand_launch(sp, selst)) fail(KC_ECUDA, "candidate selection unavailable for this shape");
+        } else {
           kc::select_launch(sp, selst);
-        } else if (!kc::select_cand_launch(sp, selst)) {
-          fail(KC_ECUDA, "candidate selection unavailable for this shape");
         }
       });
       CK(cudaEventRecord(c->ev_sel[slot], selst));

@@ -376,7 +376,9 @@ __global__ void __launch_bounds__(kT, 1) select_reg_kernel(const SelectParams p)
   // unstructured rows only ~nc keys reach it. Those candidates (<= 1024, in
   // position order) get the exact treatment; anything else (ties flooding
   // the bound, nc > 1024) falls through to the full radix pass below.
-  if (nc < s && nc <= kT) {
+  bool fast = nc < s && nc <= kT;
+  uint32_t tau = 0;
+  if (fast) {
     uint32_t tmax = 0;
 #pragma unroll
     for (int i = 0; i < KPT; ++i)
@@ -385,7 +387,6 @@ __global__ void __launch_bounds__(kT, 1) select_reg_kernel(const SelectParams p)
     // (kw = ceil(nc / 32)): every warp holds >= kw maxima >= tau, so >= nc
     // keys are >= tau. Warp-local (REDUX + BALLOT), one block barrier --
     // ~2.3x more candidates than the exact nc-th maximum, far fewer barriers.
-    uint32_t tau;
     {
       const int lane = tid & 31, warp = tid >> 5;
       const int kw = (nc + 31) / 32;
@@ -404,10 +405,15 @@ __global__ void __launch_bounds__(kT, 1) select_reg_kernel(const SelectParams p)
     }
     if (G == 1) {
       // a score just below tau can still share the N-th score's p (p-tie):
-      // lower the bound by the tie window (keys are ordered logit bits)
+      // lower the bound by the tie window (keys are ordered logit bits).
+      // When p(tau) is not a normal float the ties below tau are unbounded
+      // (p underflows): take the full pass instead.
       const float ts = from_ordered(tau);
+      fast = expf(ts - S.M[0]) / S.Z[0] >= FLT_MIN;
       if (ts > -INFINITY) tau = ordered_bits(ts - 2.0f * tie_window(ts, S.M[0]));
     }
+  }
+  if (fast) {
     uint32_t ccount = 0;
 #pragma unroll
     for (int i = 0; i < KPT; ++i) ccount += (j0 + i < s && key[i] >= tau) ? 1u : 0u;
