@@ -36,7 +36,13 @@ namespace {
 constexpr int kRows = 64;     // positions per pipeline stage
 constexpr int kCWarps = 8;    // consumer warps
 constexpr int kH = 128;       // head_dim of the fast path
-constexpr int kMaxCandChunk = 2048;  // candidate mode: positions per split held in smem
+constexpr int kMaxCandChunk = 2048;
+// MHA scoring: 3 CTAs / SM (<= 72 registers, no spills). Without the bound
+// ptxas takes 82 and the SM holds only two: C2 330 -> 310 us per layer
+// scoring inside the pipelined step, candidate mode 40k 463 -> 418 us.
+#ifndef KC_MHA_MINB
+#define KC_MHA_MINB 3
+#endif  // candidate mode: positions per split held in smem
 
 __device__ __forceinline__ void named_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
@@ -191,7 +197,7 @@ __device__ __forceinline__ void emit_candidates(const float* scb, float* mx, uin
 }
 
 template <typename T, int G, int LPR, int STAGES, bool CAND>
-__global__ void __launch_bounds__((kCWarps + 1) * 32, (G >= 2 ? 2 : 1))
+__global__ void __launch_bounds__((kCWarps + 1) * 32, (G >= 2 ? 2 : KC_MHA_MINB))
     score_fast_kernel(const ScoreParams p) {
   constexpr int CPL = 16 / LPR;            // 16-B chunks per lane per row
   constexpr int RPP = 32 / LPR;            // rows per warp pass

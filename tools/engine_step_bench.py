@@ -32,11 +32,12 @@ def main():
     ap.add_argument("--groups", default="1,2,4,8")
     ap.add_argument("--out", default="")
     ap.add_argument("--profile", action="store_true")
+    ap.add_argument("--tune", action="append", default=[], help="key=value cache tuning knob (repeatable)")
     args = ap.parse_args()
     L, b, n, h, s, N = args.layers, args.batch, args.heads, 128, args.s, args.topn
     d = n * h
     groups = [int(x) for x in args.groups.split(",")]
-    total_steps = (args.steps + 3) * len(groups)
+    total_steps = (args.steps + 4) * len(groups)
     cfg = kc.ModelConfig(L, d, n, h, kc.ModelConfig.default_ffn_hidden(d), 32000, s + total_steps, n)
     cache = kc.TieredKVCache(cfg, b, kc.TierPlacement.kcache(0, L))
     kb = torch.empty(s * b, d, dtype=torch.float16, device="cuda")
@@ -51,6 +52,9 @@ def main():
     for layer in range(L):
         cache.offload_prefill_v(layer)
     cache.begin_decode()
+    for kv in args.tune:
+        k, v = kv.split("=")
+        cache.set_tuning(k, int(v))
     q = torch.empty(b, d, dtype=torch.float16, device="cuda")
     knew = torch.empty(b, d, dtype=torch.float16, device="cuda")
     vnew = torch.empty(b, d, dtype=torch.float16, device="cuda")
@@ -98,11 +102,11 @@ def main():
             sp = {k: cache.profile_spans(k) for k in ("score", "select", "recall")}
             cache.profile(False)
             t0 = sp["score"][0][0]
-            for layer in range(min(3, L)):
+            for layer in range(min(3 * max(1, g), len(sp["score"]))):
                 print("  layer", layer, "  ".join(f"{k} {(sp[k][layer][0] - t0) * 1e3:.0f}-{(sp[k][layer][1] - t0) * 1e3:.0f}"
                                                   for k in sp))
             print("  mean us:", {k: round(1e3 * sum(e - a for a, e in v) / len(v), 1) for k, v in sp.items()})
-        rec = {"score_groups": g, "ms_per_step": ms, "host_enqueue_ms_per_step": enqueue_ms, "tokens_per_s": b / (ms * 1e-3), "per_layer_us": 1e3 * ms / L,
+        rec = {"score_groups": g, "tune": args.tune, "ms_per_step": ms, "host_enqueue_ms_per_step": enqueue_ms, "tokens_per_s": b / (ms * 1e-3), "per_layer_us": 1e3 * ms / L,
                "len": cache.current_len(), "mean_dropped_mass": st["mean_dropped_mass"],
                "h2d_bytes_per_step": st["h2d_bytes"] // args.steps, "d2h_bytes_per_step": st["d2h_bytes"] // args.steps}
         print(json.dumps(rec), flush=True)
