@@ -36,13 +36,13 @@ namespace {
 constexpr int kRows = 64;     // positions per pipeline stage
 constexpr int kCWarps = 8;    // consumer warps
 constexpr int kH = 128;       // head_dim of the fast path
-constexpr int kMaxCandChunk = 2048;
+constexpr int kMaxCandChunk = 2048;  // candidate mode: positions per split held in smem
 // MHA scoring: 3 CTAs / SM (<= 72 registers, no spills). Without the bound
 // ptxas takes 82 and the SM holds only two: C2 330 -> 310 us per layer
 // scoring inside the pipelined step, candidate mode 40k 463 -> 418 us.
 #ifndef KC_MHA_MINB
 #define KC_MHA_MINB 3
-#endif  // candidate mode: positions per split held in smem
+#endif
 
 __device__ __forceinline__ void named_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
@@ -127,9 +127,11 @@ __device__ __forceinline__ void produce_k(const ScoreParams& p, uint8_t* ring, u
 }
 
 // Candidate epilogue of one split (MHA): scb[0..npos) holds the split's
-// scores. tau = the nc-th largest of the 256 consumer threads' block maxima is
-// a lower bound of the split's nc-th largest score (nc threads each hold a
-// score >= tau), so every position below tau has >= nc positions of this
+// scores. tau = the minimum over the 8 consumer warps of each warp's
+// ceil(nc/8)-th largest thread maximum is a lower bound of the split's nc-th
+// largest score (>= nc threads each hold a score >= tau; the exact nc-th
+// largest of the 256 maxima cost an all-pairs scan, +20 % instructions per
+// split), so every position below tau has >= nc positions of this
 // split strictly above it in p (p = exp(s - M)/Z is monotone in s) and can
 // never be selected -- except through a p-tie, which needs |s - tau| within a
 // few ulps: the bound keeps a window of 2^-9 (1 + |tau| + |max|) below tau.
@@ -140,7 +142,8 @@ __device__ __forceinline__ void emit_candidates(const float* scb, float* mx, uin
   constexpr int NT = kCWarps * 32;
   const int ct = threadIdx.x;  // 0..255 (consumer warps)
   const int lane = ct & 31, warp = ct >> 5;
-  float* mred = mx + NT;  // [kCWarps]
+  float* mred = mx;            // [kCWarps] per-warp bound
+  float* mtop = mx + kCWarps;  // [kCWarps] per-warp maximum
   // thread ct owns the contiguous positions [a, e) of the split
   const int ppt = (npos + NT - 1) / NT;
   const int a = min(npos, ct * ppt), e = min(npos, a + ppt);
@@ -148,27 +151,31 @@ __device__ __forceinline__ void emit_candidates(const float* scb, float* mx, uin
   if (npos > nc) {
     float m = -INFINITY;
     for (int j = a; j < e; ++j) m = fmaxf(m, scb[j]);
-    mx[ct] = m;
-    named_sync(1, NT);
-    // r = maxima strictly above m: the nc-th largest maximum is the smallest
-    // m with r < nc (no tie-break needed)
-    int r = 0;
-    float smax = -INFINITY;
-    const float4* mx4 = reinterpret_cast<const float4*>(mx);
-#pragma unroll 8
-    for (int u = 0; u < NT / 4; ++u) {
-      const float4 v = mx4[u];
-      r += (v.x > m) + (v.y > m) + (v.z > m) + (v.w > m);
-      smax = fmaxf(smax, fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w)));
+    // tau = min over warps of the warp's kw-th largest thread maximum
+    // (kw = ceil(nc / 8)): every warp holds >= kw maxima >= tau, so >= nc
+    // positions of the split score >= tau. Warp-local (REDUX + BALLOT on
+    // order-preserving bits), one barrier.
+    const int kw = (nc + kCWarps - 1) / kCWarps;
+    const uint32_t um = __float_as_uint(m);
+    uint32_t v = (um & 0x80000000u) ? ~um : (um | 0x80000000u), kth = 0, top = 0;
+    for (int r = 0; r < kw; ++r) {
+      kth = __reduce_max_sync(0xffffffffu, v);
+      top = r == 0 ? kth : top;
+      const uint32_t ball = __ballot_sync(0xffffffffu, v == kth);
+      if (lane == __ffs(ball) - 1) v = 0u;
     }
-    float t = r < nc ? m : INFINITY;
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) t = fminf(t, __shfl_xor_sync(0xffffffffu, t, o));
-    if (lane == 0) mred[warp] = t;
+    auto unord = [](uint32_t k) { return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k); };
+    if (lane == 0) {
+      mred[warp] = unord(kth);
+      mtop[warp] = unord(top);
+    }
     named_sync(1, NT);
-    float tau = mred[0];
+    float tau = mred[0], smax = mtop[0];
 #pragma unroll
-    for (int w = 1; w < kCWarps; ++w) tau = fminf(tau, mred[w]);
+    for (int w = 1; w < kCWarps; ++w) {
+      tau = fminf(tau, mred[w]);
+      smax = fmaxf(smax, mtop[w]);
+    }
     if (tau > -INFINITY) bound = tau - 0x1p-9f * (1.0f + fabsf(tau) + fabsf(smax));
   }
   // ordered compaction: count, block exclusive scan, write in position order
@@ -212,8 +219,8 @@ __global__ void __launch_bounds__((kCWarps + 1) * 32, (G >= 2 ? 2 : KC_MHA_MINB)
   float2* red = reinterpret_cast<float2*>(empty + STAGES);  // [kCWarps][G]
   // candidate mode: the split's scores, block maxima, warp counts
   float* scb = reinterpret_cast<float*>(red + kCWarps * G);  // [chunk]
-  float* mx = scb + (CAND ? p.chunk : 0);                     // [256]
-  uint32_t* wcnt = reinterpret_cast<uint32_t*>(mx + kCWarps * 32 + kCWarps);
+  float* mx = scb + (CAND ? p.chunk : 0);                     // [2 * kCWarps]
+  uint32_t* wcnt = reinterpret_cast<uint32_t*>(mx + 2 * kCWarps);
   static_assert(!CAND || G == 1, "candidate mode ranks raw scores: MHA only");
 
   const int n_items = p.rows * p.n_splits;
@@ -901,7 +908,7 @@ void launch_fast_s(const ScoreParams& p, cudaStream_t st) {
   constexpr int ROWB = kH * (int)sizeof(T);
   const size_t smem = STAGES * kRows * ROWB + 2 * STAGES * sizeof(uint64_t) +
                       kCWarps * G * sizeof(float2) +
-                      (CAND ? (size_t)kMaxCandChunk * 4 + kCWarps * 32 * 4 + 2 * kCWarps * 4 : 0);
+                      (CAND ? (size_t)kMaxCandChunk * 4 + 3 * kCWarps * 4 : 0);
   static unsigned long long configured = 0;  // one bit per device
   int dev = 0;
   cudaGetDevice(&dev);
