@@ -184,7 +184,8 @@ struct kc_cache {
   std::unique_ptr<kc::GatherPool> pool;
   cudaStream_t main_st = nullptr, side_st = nullptr, gather_st = nullptr, out_st = nullptr;
   cudaEvent_t ev_start = nullptr, ev_end = nullptr, ev_sel[kRing] = {}, ev_rec[kRing] = {},
-              ev_gath[kRing] = {}, ev_scored[kRing] = {}, ev_out[kRing] = {}, ev_cp[kRing] = {};
+              ev_gath[kRing] = {}, ev_scored[kRing] = {}, ev_out[kRing] = {}, ev_cp[kRing] = {},
+              ev_stats = nullptr;
   bool cp_pending[kRing] = {};  // ev_cp[slot] guards a device-mode copy of that slot
 
   // tuning
@@ -408,6 +409,7 @@ void destroy(kc_cache* c) {
   for (cudaEvent_t e : c->prof_pool) cudaEventDestroy(e);
   if (c->ev_start) cudaEventDestroy(c->ev_start);
   if (c->ev_end) cudaEventDestroy(c->ev_end);
+  if (c->ev_stats) cudaEventDestroy(c->ev_stats);
   if (c->main_st) cudaStreamDestroy(c->main_st);
   if (c->side_st) cudaStreamDestroy(c->side_st);
   delete c;
@@ -934,6 +936,7 @@ int kc_cache_create(const kc_config* cfg, uint64_t batch, uint64_t resident_laye
       CK(cudaStreamCreateWithFlags(&c->out_st, cudaStreamNonBlocking));
       CK(cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming));
       CK(cudaEventCreateWithFlags(&c->ev_end, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&c->ev_stats, cudaEventDisableTiming));
       for (int i = 0; i < kRing; ++i) {
         CK(cudaEventCreateWithFlags(&c->ev_sel[i], cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&c->ev_scored[i], cudaEventDisableTiming));
@@ -1049,16 +1052,25 @@ int kc_decode_step(kc_cache* c, uint64_t layer, const void* q, const void* k_new
     o.out = out;
     const void* qs[1] = {q};
     decode_topn_impl(c, 1, &layer, qs, dtype, top_n, flags & (KC_RENORMALIZE | KC_IO_DEVICE), &o, st);
-    // engine.cpp:146-156 on the device: ring slot 0 holds this call's selection
+    // engine.cpp:146-156 on the device: ring slot 0 holds this call's
+    // selection. The statistics need the selection only, so they run off the
+    // critical path on the output stream (the caller's stream waits for them,
+    // long done, together with the recall).
     const uint64_t slots = c->batch * c->n_q;
+    cudaStream_t sst = c->pipeline ? c->out_st : st;
+    if (sst != st) CK(cudaStreamWaitEvent(sst, c->ev_sel[0], 0));
     if (!c->step_dev.p) {
       c->step_dev.ensure(sizeof(kc::StepStatsDev));
-      CK(cudaMemsetAsync(c->step_dev.p, 0, sizeof(kc::StepStatsDev), st));
+      CK(cudaMemsetAsync(c->step_dev.p, 0, sizeof(kc::StepStatsDev), sst));
     }
     kc::step_stats_launch(c->idx[0].as<uint32_t>(), c->dropped[0].as<double>(), (int)c->rows, (int)c->G,
                           (int)o.nc, c->current_len(), (int)slots,
-                          static_cast<kc::StepStatsDev*>(c->step_dev.p), st);
+                          static_cast<kc::StepStatsDev*>(c->step_dev.p), sst);
     CK(cudaGetLastError());
+    if (sst != st) {
+      CK(cudaEventRecord(c->ev_stats, sst));
+      CK(cudaStreamWaitEvent(st, c->ev_stats, 0));
+    }
     c->step_host.h2d_bytes += o.h2d_bytes;
     c->step_host.selections += slots;
     if (!io_device) CK(cudaStreamSynchronize(st));

@@ -55,18 +55,16 @@ def main():
     for kv in args.tune:
         k, v = kv.split("=")
         cache.set_tuning(k, int(v))
-    q = torch.empty(b, d, dtype=torch.float16, device="cuda")
-    knew = torch.empty(b, d, dtype=torch.float16, device="cuda")
-    vnew = torch.empty(b, d, dtype=torch.float16, device="cuda")
+    # this step's q/k/v rows, as one QKV projection would write them
+    qkv = torch.empty(3, b, d, dtype=torch.float16, device="cuda")
+    q, knew, vnew = qkv[0], qkv[1], qkv[2]
     out = torch.empty(b, d, dtype=torch.float32, device="cuda")
     stream = torch.cuda.Stream()
     rows = []
 
     def step(seed):
         for layer in range(L):
-            kc.fill_uniform(q, 7 + seed * 1000 + layer, stream=stream)
-            kc.fill_uniform(knew, 8 + seed * 1000 + layer, stream=stream)
-            kc.fill_uniform(vnew, 9 + seed * 1000 + layer, stream=stream)
+            kc.fill_uniform(qkv, 7 + seed * 1000 + layer, stream=stream)
             cache.decode_step_device(layer, q, knew, vnew, out, N, stream=stream)
 
     seed = 0
