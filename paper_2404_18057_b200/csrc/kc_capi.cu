@@ -175,6 +175,7 @@ struct kc_cache {
   DevBuf cand, cand_meta, fb_flags;  // candidate-mode selection scratch
   DevBuf part_ml;                    // fused full attention: split (m, l)
   DevBuf step_dev;                   // kc_decode_step: StepStatsDev accumulator
+  DevBuf row_done;                   // fused selection: per-row split completion counters
   kc_step_stats step_host{};         // kc_decode_step: host-known counters
   DevBuf q32[kRing], idx[kRing], w[kRing], dropped[kRing], norm[kRing], out_tmp[kRing], idx_exp[kRing];
   PinnedBuf host_in, host_out;
@@ -212,6 +213,8 @@ struct kc_cache {
   int select_on_side = 0;  // pipelined: selection on the side stream too (measured: no gain)
   int full_fused = 1;      // decode_attention_full: fused K+V pass when V is in HBM
   int keep_logits = 0;     // leave dead logits in L2 instead of discarding them
+  int fuse_select = 0;     // MHA dense rows: the scoring kernel selects each row (kc_rowsel.cuh;
+                           // measured slower than the separate kernel)
   int recall_pipe = 0;    // software-pipelined recall kernel (measured: no gain, page-walk bound)
   int recall_ctas = 32;  // CTAs of the recall kernel (0: one per (batch, kv head)); 32 measured best at C2
   int gather_threads = 0;  // 0: 3/4 of the host cores
@@ -393,7 +396,7 @@ void destroy(kc_cache* c) {
   c->v_managed.clear();
   for (DevBuf* b : {&c->logits, &c->partials, &c->keys, &c->part_out, &c->stage_src, &c->stage_k,
                     &c->stage_v, &c->sel_rows, &c->sel_pos, &c->gather_out, &c->cand, &c->cand_meta,
-                    &c->fb_flags, &c->part_ml, &c->step_dev})
+                    &c->fb_flags, &c->part_ml, &c->step_dev, &c->row_done})
     b->release();
   for (int i = 0; i < kRing; ++i) {
     c->q32[i].release(); c->idx[i].release(); c->w[i].release(); c->dropped[i].release();
@@ -522,9 +525,18 @@ void maybe_flush_l2(kc_cache* c, const uint64_t* layers, uint64_t n, cudaStream_
 }
 
 void enqueue_score(kc_cache* c, uint64_t layer, const float* q32, const StepGeom& g, cudaStream_t st,
-                   int row0, int nrows, bool cand = false, int lb = 0) {
+                   int row0, int nrows, bool cand = false, int lb = 0, int slot = -1) {
   kc::ScoreParams sp{};
   sp.row0 = row0;
+  if (slot >= 0) {  // fused selection into ring slot `slot`
+    sp.row_done = c->row_done.as<uint32_t>();
+    sp.sel_idx = c->idx[slot].as<uint32_t>();
+    sp.sel_w = c->w[slot].as<float>();
+    sp.sel_dropped = c->dropped[slot].as<double>();
+    sp.sel_norm = c->norm[slot].as<float>();
+    sp.sel_nc = g.nc;
+    sp.keep_logits = c->keep_logits;
+  }
   if (cand) {
     sp.cand = c->cand_buf(lb);
     sp.cand_meta = c->cand_meta_buf(lb);
@@ -653,6 +665,15 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
     // register-resident dense selection.
     const bool cand = (c->select_cand == 1 || (c->select_cand == 0 && g.s > kc::kDenseRegMaxS)) &&
                       !c->select_global && kc::score_cand_supported(c->dtype, (int)c->h, (int)c->G, g.chunk, g.nc);
+    // Fused selection (MHA dense rows, N <= 256): the scoring CTA that
+    // completes a row's last split selects the row; no selection launch.
+    const bool fused = !cand && c->fuse_select && !c->select_global &&
+                       kc::score_fused_select_supported(c->dtype, (int)c->h, (int)c->G, g.chunk, g.nc,
+                                                        c->score_ctas_per_sm);
+    if (fused && !c->row_done.p) {
+      c->row_done.ensure(c->rows * 4);
+      CK(cudaMemsetAsync(c->row_done.p, 0, c->rows * 4, st));
+    }
     if (cand) {
       c->cand.ensure(2 * checked_mul({c->rows, (uint64_t)c->lstride, 8}));
       c->cand_meta.ensure(2 * checked_mul({c->rows, (uint64_t)c->max_splits, 8}));
@@ -663,7 +684,7 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
       const int r0 = gi * gsz;
       const int nr = std::min<int>(gsz, (int)c->rows - r0);
       if (nr <= 0) break;
-      enqueue_score(c, layer, q32, g, st, r0, nr, cand, lb);
+      enqueue_score(c, layer, q32, g, st, r0, nr, cand, lb, fused ? slot : -1);
       if (side_select) {
         CK(cudaEventRecord(c->ev_scored[slot], st));
         CK(cudaStreamWaitEvent(side, c->ev_scored[slot], 0));
@@ -705,7 +726,7 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
         sp.scale = 1.0f / std::sqrt(static_cast<float>(c->h));  // attention.hpp:15-17
         sp.force_fallback = c->cand_force_fallback;
       }
-      c->timed(1, selst, [&] {
+      if (!fused) c->timed(1, selst, [&] {
         if (cand) {
           if (!kc::select_cand_launch(sp, selst)) fail(KC_ECUDA, "candidate selection unavailable for this shape");
         } else {
@@ -1354,6 +1375,7 @@ int kc_set_tuning(kc_cache* c, const char* key, int64_t value) {
     }
     else if (k == "keep_logits") c->keep_logits = value ? 1 : 0;
     else if (k == "full_fused") c->full_fused = value ? 1 : 0;
+    else if (k == "fuse_select") c->fuse_select = value ? 1 : 0;
     else if (k == "select_on_side") c->select_on_side = value ? 1 : 0;
     else if (k == "select_cand") {
       if (value < 0 || value > 2) fail(KC_EARG, "select_cand: 0 auto, 1 on, 2 off");

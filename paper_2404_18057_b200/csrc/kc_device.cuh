@@ -90,15 +90,19 @@ __device__ __forceinline__ void ml_combine(float& m, float& l, float m2, float l
 // per-split (max, sum exp): M = max m_i, Z = sum_i l_i exp(m_i - M). Called
 // by a full warp; every kernel that needs p = exp(s - M) / Z uses this one
 // function, so selection, weights and the observer path agree bit for bit.
+// CG: read through L2 only (partials written by other CTAs of the running
+// kernel: the fused selection in kc_rowsel.cuh).
+template <bool CG = false>
 __device__ __forceinline__ void softmax_stats(const float2* part, int n_splits, int lane, float& M,
                                               float& Z) {
+  auto ld = [&](int i) { return CG ? __ldcg(part + i) : part[i]; };
   float m = -INFINITY;
-  for (int i = lane; i < n_splits; i += 32) m = fmaxf(m, part[i].x);
+  for (int i = lane; i < n_splits; i += 32) m = fmaxf(m, ld(i).x);
 #pragma unroll
   for (int o = 16; o >= 1; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
   float z = 0.0f;
   for (int i = lane; i < n_splits; i += 32) {
-    const float2 ml = part[i];
+    const float2 ml = ld(i);
     if (ml.y > 0.0f) z += ml.y * expf(ml.x - m);
   }
 #pragma unroll
@@ -189,6 +193,25 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
   uint32_t m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
   return m;
+}
+
+// ---- selection keys (kc_select.cu, kc_rowsel.cuh) ---------------------------
+// Order-preserving bits of a float; -0.0 and +0.0 compare equal, so they must
+// tie (one key).
+__device__ __forceinline__ uint32_t ordered_bits(float x) {
+  const uint32_t u = x == 0.0f ? 0u : __float_as_uint(x);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+__device__ __forceinline__ float from_ordered(uint32_t k) {
+  return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
+}
+
+// The p-tie window around a score Ts: outside it p = expf(s - M)/Z differs
+// from p(Ts) strictly, provided p(Ts) is a normal float (see
+// score_fast_kernel's candidate bound).
+__device__ __forceinline__ float tie_window(float Ts, float M) {
+  return 4e-5f * (1.0f + fabsf(Ts) + fabsf(M));
 }
 
 }  // namespace kc

@@ -27,6 +27,7 @@
 
 #include "kc_device.cuh"
 #include "kc_kernels.cuh"
+#include "kc_rowsel.cuh"
 #include "kcache_c.h"
 
 namespace kc {
@@ -203,7 +204,7 @@ __device__ __forceinline__ void emit_candidates(const float* scb, float* mx, uin
   if (ct == 0) *meta = make_uint2(tot, __float_as_uint(bound));
 }
 
-template <typename T, int G, int LPR, int STAGES, bool CAND>
+template <typename T, int G, int LPR, int STAGES, bool CAND, bool FUSE = false>
 __global__ void __launch_bounds__((kCWarps + 1) * 32, (G >= 2 ? 2 : KC_MHA_MINB))
     score_fast_kernel(const ScoreParams p) {
   constexpr int CPL = 16 / LPR;            // 16-B chunks per lane per row
@@ -360,6 +361,32 @@ __global__ void __launch_bounds__((kCWarps + 1) * 32, (G >= 2 ? 2 : KC_MHA_MINB)
       emit_candidates(scb, mx, wcnt, npos, p.cand_nc, pos0, p.cand + (size_t)row * p.lstride + pos0,
                       p.cand_meta + (size_t)row * p.max_splits + split);
     named_sync(1, kCWarps * 32);  // red / scb are reused by the next item
+    if constexpr (FUSE) {
+      static_assert(G == 1 && !CAND, "fused selection: MHA dense rows");
+      // fused selection: the CTA that completes the row's last split selects
+      // the row (kc_rowsel.cuh) in its now idle ring while the others stream
+      {
+        __shared__ uint32_t s_last;
+        // the barrier orders every thread's logits / partials before thread
+        // 0's release fence (cumulative), which orders them before the count
+        named_sync(1, kCWarps * 32);
+        if (threadIdx.x == 0) {
+          __threadfence();
+          s_last = atomicAdd(&p.row_done[row], 1u) == (uint32_t)(p.n_splits - 1);
+          if (s_last) __threadfence();  // acquire: the other splits' writes
+        }
+        named_sync(1, kCWarps * 32);
+        if (s_last) {
+          constexpr int kRingBytes = STAGES * kRows * ROWB;
+          constexpr int cap = (kRingBytes - rowsel::kSharedBytes) / 8 < 4096 ? (kRingBytes - rowsel::kSharedBytes) / 8 : 4096;
+          const rowsel::RowOut ro{p.sel_idx + (size_t)row * p.sel_nc, p.sel_w + (size_t)row * p.sel_nc,
+                                  p.sel_dropped + row, p.sel_norm + row};
+          rowsel::select_row(ring, cap, p.logits + (size_t)row * p.lstride, p.partials + (size_t)row * p.max_splits,
+                             p.n_splits, p.s, p.sel_nc, ro, p.keep_logits != 0);
+          if (threadIdx.x == 0) p.row_done[row] = 0u;  // ready for the next launch
+        }
+      }
+    }
   }
 }
 
@@ -920,6 +947,18 @@ void launch_fast_s(const ScoreParams& p, cudaStream_t st) {
   const int n_items = p.rows * p.n_splits;
   const int per_sm = p.ctas_per_sm > 0 ? p.ctas_per_sm : 1 << 20;  // 0: one CTA per item
   const int grid = (int)std::min<long long>(n_items, (long long)per_sm * num_sms());
+  if constexpr (G == 1 && !CAND) {
+    if (p.row_done) {  // fused selection (its own instantiation: the plain kernel keeps its registers)
+      static unsigned long long configured_f = 0;
+      if (!(configured_f >> (dev & 63) & 1ull)) {
+        cudaFuncSetAttribute(score_fast_kernel<T, G, LPR, STAGES, false, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        configured_f |= 1ull << (dev & 63);
+      }
+      score_fast_kernel<T, G, LPR, STAGES, false, true><<<n_items, (kCWarps + 1) * 32, smem, st>>>(p);
+      return;
+    }
+  }
   score_fast_kernel<T, G, LPR, STAGES, CAND><<<grid, (kCWarps + 1) * 32, smem, st>>>(p);
 }
 
@@ -1023,6 +1062,13 @@ bool full_fast_launch(const FullParams& p, int dtype, cudaStream_t st) {
   if (dtype == KC_F16) return try_full<__half>(p, st);
   if (dtype == KC_BF16) return try_full<__nv_bfloat16>(p, st);
   return false;
+}
+
+bool score_fused_select_supported(int dtype, int h, int G, int chunk, int nc, int ctas_per_sm) {
+  // one CTA per item (the ring is idle after it), MHA 16-bit fast path, the
+  // selection's warp-local bound (N <= 256)
+  return (dtype == KC_F16 || dtype == KC_BF16) && h == kH && G == 1 && chunk % kRows == 0 && nc >= 1 &&
+         nc <= rowsel::kMaxNc && ctas_per_sm == 0;
 }
 
 bool score_cand_supported(int dtype, int h, int G, int chunk, int nc) {

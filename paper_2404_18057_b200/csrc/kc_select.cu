@@ -172,23 +172,6 @@ __device__ __forceinline__ void radix_threshold(SelShared& S, Get&& get, int nc,
   k_eq = S.need;
 }
 
-__device__ __forceinline__ uint32_t ordered_bits(float x) {
-  // -0.0 and +0.0 compare equal, so they must tie (one key)
-  const uint32_t u = x == 0.0f ? 0u : __float_as_uint(x);
-  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
-}
-
-__device__ __forceinline__ float from_ordered(uint32_t k) {
-  return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
-}
-
-// The p-tie window around a score Ts: outside it p = expf(s - M)/Z differs
-// from p(Ts) strictly, provided p(Ts) is a normal float (see
-// score_fast_kernel's candidate bound).
-__device__ __forceinline__ float tie_window(float Ts, float M) {
-  return 4e-5f * (1.0f + fabsf(Ts) + fabsf(M));
-}
-
 // Candidate-mode fallback: recompute one MHA row's scores into the dense
 // logits row, bit-identical to score_fast_kernel<T, 1, 4, ...>: the same lane
 // roles (4 lanes per position, 16-B chunk c = ((ci ^ (pos & 1)) << 2) | sub),
