@@ -151,6 +151,21 @@ int kc_decode_step(kc_cache* cache, uint64_t layer, const void* q, const void* k
  * the cache's queued work); reset != 0 starts a new step. */
 int kc_step_stats_read(kc_cache* cache, kc_step_stats* out, int reset);
 
+/* One CUDA Graph per decode step (the reference has no GPU, so
+ * no reference counterpart): kc_step_graph_begin allocates every buffer the
+ * step may need for this top_n and starts capturing `stream` (thread-local
+ * mode); the step's KC_IO_DEVICE kc_decode_step / kc_decode_full calls on
+ * that stream are recorded instead of launched -- their host-side effects
+ * (cache lengths, ledger events, StepStats counters) happen at capture time
+ * exactly as in an eager call. kc_step_graph_launch ends the capture, updates
+ * the cache's instantiated graph in place (cudaGraphExecUpdate; a new
+ * instantiation when the step's shape changed) and launches it on `stream`.
+ * Kernel arguments change every step (the cache grows), so every step is
+ * captured once and launched once; the graph removes the per-kernel launch
+ * gaps on the device. Host-memory I/O calls are not capturable (KC_ESTATE). */
+int kc_step_graph_begin(kc_cache* cache, uint64_t top_n, void* stream);
+int kc_step_graph_launch(kc_cache* cache, void* stream);
+
 /* Full softmax rows of every (batch, q head) -- the ScoreObserver debug path
  * (attention.hpp:34-35, attention.cpp:137-139): probs [batch*n_heads][len]
  * fp32, host. Not on the hot path. */

@@ -176,6 +176,8 @@ struct kc_cache {
   DevBuf part_ml;                    // fused full attention: split (m, l)
   DevBuf step_dev;                   // kc_decode_step: StepStatsDev accumulator
   DevBuf row_done;                   // fused selection: per-row split completion counters
+  cudaGraphExec_t step_exec = nullptr;  // kc_step_graph_*: the instantiated step graph
+  cudaStream_t capture_st = nullptr;    // stream being captured (nullptr: none)
   kc_step_stats step_host{};         // kc_decode_step: host-known counters
   DevBuf q32[kRing], idx[kRing], w[kRing], dropped[kRing], norm[kRing], out_tmp[kRing], idx_exp[kRing];
   PinnedBuf host_in, host_out;
@@ -413,6 +415,7 @@ void destroy(kc_cache* c) {
   if (c->ev_start) cudaEventDestroy(c->ev_start);
   if (c->ev_end) cudaEventDestroy(c->ev_end);
   if (c->ev_stats) cudaEventDestroy(c->ev_stats);
+  if (c->step_exec) cudaGraphExecDestroy(c->step_exec);
   if (c->main_st) cudaStreamDestroy(c->main_st);
   if (c->side_st) cudaStreamDestroy(c->side_st);
   delete c;
@@ -629,7 +632,9 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
   // only: scoring(i+1) overlaps selection(i) as well as recall(i)
   const bool side_select = side != st && c->select_on_side;
   cudaStream_t selst = side_select ? side : st;
+  if (!io_device && c->capture_st) fail(KC_ESTATE, "host-memory I/O inside a step graph capture");
   maybe_flush_l2(c, layers, n, st);
+  bool out_used = false;  // c->out_st carries work of this call
   CK(cudaEventRecord(c->ev_start, st));
   if (side != st) CK(cudaStreamWaitEvent(side, c->ev_start, 0));
 
@@ -809,6 +814,7 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
     cudaStream_t cst = (dev_copies && side != st) ? c->out_st : side;
     if (cst != side) CK(cudaStreamWaitEvent(cst, c->ev_sel[slot], 0));
     c->cp_pending[slot] = cst != side;
+    out_used |= cst != side;
     const uint32_t* idx_slots = c->idx[slot].as<uint32_t>();
     if (c->G > 1 && (o.indices || !io_device)) {
       kc::expand_idx_launch(idx_slots, c->idx_exp[slot].as<uint32_t>(), (int)c->rows, (int)c->G,
@@ -825,6 +831,7 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
       // D2H straight into pinned user buffers, else into pinned staging; on
       // their own stream so the next layer's recall does not queue behind them
       cudaStream_t ost = side != st ? c->out_st : st;
+      out_used |= ost == c->out_st;
       if (ost != side) {
         CK(cudaEventRecord(c->ev_out[slot], side));
         CK(cudaStreamWaitEvent(ost, c->ev_out[slot], 0));
@@ -859,8 +866,10 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
   if (side != st) {
     CK(cudaEventRecord(c->ev_end, side));
     CK(cudaStreamWaitEvent(st, c->ev_end, 0));
-    CK(cudaEventRecord(c->ev_end, c->out_st));  // host D2H / device selection copies
-    CK(cudaStreamWaitEvent(st, c->ev_end, 0));
+    if (out_used) {  // host D2H / device selection copies
+      CK(cudaEventRecord(c->ev_end, c->out_st));
+      CK(cudaStreamWaitEvent(st, c->ev_end, 0));
+    }
   }
   if (!io_device) {
     CK(cudaStreamSynchronize(st));
@@ -1044,6 +1053,7 @@ int kc_decode_step(kc_cache* c, uint64_t layer, const void* q, const void* k_new
     const size_t esz = dtype_size(dtype);
     if (!(flags & KC_FULL) && top_n == 0) fail(KC_EARG, "decode_attention_topn: top_n must be >= 1");
     const bool io_device = flags & KC_IO_DEVICE;
+    if (!io_device && c->capture_st) fail(KC_ESTATE, "host-memory I/O inside a step graph capture");
     set_dev(c);
     cudaStream_t st = io_device ? (cudaStream_t)stream : c->main_st;
     // engine.cpp:143 -- this step's K/V row of every batch row
@@ -1098,6 +1108,84 @@ int kc_decode_step(kc_cache* c, uint64_t layer, const void* q, const void* k_new
   });
 }
 
+// Every buffer a device-mode decode step may allocate lazily, allocated now:
+// nothing may cudaMalloc while a step is being captured.
+void prepare_step_buffers(kc_cache* c, uint64_t top_n, cudaStream_t st) {
+  const uint64_t nc = std::min<uint64_t>(top_n, c->cfg.max_seq);
+  const uint64_t slots = c->batch * c->n_q;
+  for (int r = 0; r < kRing; ++r) {
+    c->idx[r].ensure(c->rows * nc * 4);
+    c->w[r].ensure(slots * nc * 4);
+    c->dropped[r].ensure(slots * 8);
+    c->norm[r].ensure(slots * 4);
+    if (c->G > 1) c->idx_exp[r].ensure(slots * nc * 4);
+    c->q32[r].ensure(slots * c->h * sizeof(float));
+  }
+  if (c->G == 1 && c->select_cand != 2) {  // candidate mode may switch on as the rows grow
+    c->cand.ensure(2 * checked_mul({c->rows, (uint64_t)c->lstride, 8}));
+    c->cand_meta.ensure(2 * checked_mul({c->rows, (uint64_t)c->max_splits, 8}));
+    c->fb_flags.ensure(c->rows * 4);
+  }
+  if (!c->row_done.p) {
+    c->row_done.ensure(c->rows * 4);
+    CK(cudaMemsetAsync(c->row_done.p, 0, c->rows * 4, st));
+  }
+  if (!c->step_dev.p) {
+    c->step_dev.ensure(sizeof(kc::StepStatsDev));
+    CK(cudaMemsetAsync(c->step_dev.p, 0, sizeof(kc::StepStatsDev), st));
+  }
+  if (c->L > 0) {  // full attention on the V-resident layers
+    c->part_out.ensure(checked_mul({slots, (uint64_t)c->max_splits, c->h, 4}));
+    c->part_ml.ensure(checked_mul({slots, (uint64_t)c->max_splits, 8}));
+  }
+  l2_scratch(c, st);
+}
+
+int kc_step_graph_begin(kc_cache* c, uint64_t top_n, void* stream) {
+  return guarded([&] {
+    if (!stream) fail(KC_EARG, "kc_step_graph_begin: needs the caller's (non-default) stream");
+    if (c->capture_st) fail(KC_ESTATE, "kc_step_graph_begin: a step capture is already open");
+    set_dev(c);
+    cudaStream_t st = (cudaStream_t)stream;
+    prepare_step_buffers(c, top_n, st);
+    // the cache's own streams must not hold work the captured step would
+    // have to order against (their events would cross the capture boundary)
+    CK(cudaStreamSynchronize(c->side_st));
+    CK(cudaStreamSynchronize(c->out_st));
+    CK(cudaStreamSynchronize(c->gather_st));
+    CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    c->capture_st = st;
+  });
+}
+
+int kc_step_graph_launch(kc_cache* c, void* stream) {
+  return guarded([&] {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (!c->capture_st || c->capture_st != st) fail(KC_ESTATE, "kc_step_graph_launch: no capture open on this stream");
+    set_dev(c);
+    c->capture_st = nullptr;
+    cudaGraph_t graph = nullptr;
+    CK(cudaStreamEndCapture(st, &graph));
+    // kernel arguments (cache length, split counts, grids) change every step:
+    // update the instantiated graph in place, re-instantiate on a topology change
+    bool ok = false;
+    if (c->step_exec) {
+      cudaGraphExecUpdateResultInfo info{};
+      ok = cudaGraphExecUpdate(c->step_exec, graph, &info) == cudaSuccess;
+      if (!ok) {
+        cudaGetLastError();
+        cudaGraphExecDestroy(c->step_exec);
+        c->step_exec = nullptr;
+      }
+    }
+    cudaError_t e = cudaSuccess;
+    if (!ok) e = cudaGraphInstantiate(&c->step_exec, graph, 0);
+    if (e == cudaSuccess) e = cudaGraphLaunch(c->step_exec, st);
+    cudaGraphDestroy(graph);
+    CK(e);
+  });
+}
+
 int kc_step_stats_read(kc_cache* c, kc_step_stats* out, int reset) {
   return guarded([&] {
     if (!out) fail(KC_EARG, "kc_step_stats_read: null argument");
@@ -1137,6 +1225,7 @@ int kc_decode_full(kc_cache* c, uint64_t layer, const void* q, int q_dtype, uint
     set_dev(c);
     const bool io_device = flags & KC_IO_DEVICE;
     cudaStream_t st = io_device ? (cudaStream_t)stream : c->main_st;
+    if (!io_device && c->capture_st) fail(KC_ESTATE, "host-memory I/O inside a step graph capture");
     const StepGeom g = geom(c, 1, 1);  // fused full kernel: MHA split sizing
     maybe_flush_l2(c, &layer, 1, st);
     const float* q32 = stage_q(c, 0, q, q_dtype, io_device, st);

@@ -93,6 +93,8 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         "kc_decode_full": (i32, [vp, u64, vp, i32, u32, vp, vp]),
         "kc_decode_step": (i32, [vp, u64, vp, vp, vp, i32, u64, u32, vp, vp]),
         "kc_step_stats_read": (i32, [vp, C.POINTER(_StepStats), i32]),
+        "kc_step_graph_begin": (i32, [vp, u64, vp]),
+        "kc_step_graph_launch": (i32, [vp, vp]),
         "kc_score_probs": (i32, [vp, u64, vp, i32, vp]),
         "kc_gather_v": (i32, [vp, u64, vp, vp, vp, p64]),
         "kc_read_row": (i32, [vp, u64, u64, u64, i32, vp]),
@@ -518,6 +520,16 @@ class TieredKVCache:
         st = stream.cuda_stream if stream is not None else torch.cuda.current_stream().cuda_stream
         _check(self._lib.kc_decode_step(self._h, layer, q.data_ptr(), k_new.data_ptr(), v_new.data_ptr(), dt,
                                         top_n, flags, out.data_ptr(), st))
+
+    def step_graph_begin(self, top_n: int, stream) -> None:
+        """Start capturing one decode step on `stream` (a torch.cuda.Stream):
+        the decode_step_device / decode_full_device calls that follow are
+        recorded, and step_graph_launch replays them as one CUDA Graph."""
+        _check(self._lib.kc_step_graph_begin(self._h, top_n, stream.cuda_stream))
+
+    def step_graph_launch(self, stream) -> None:
+        """End the capture and launch the step's graph on `stream`."""
+        _check(self._lib.kc_step_graph_launch(self._h, stream.cuda_stream))
 
     def step_stats(self, reset: bool = True) -> dict:
         """StepStats (engine.hpp:37-45) accumulated by decode_step since the last reset."""

@@ -95,3 +95,60 @@ def test_decode_step_errors(kc):
     with pytest.raises(kc.ShapeError):
         cache.decode_step(0, q, row[:, :h], row, 4)
     cache.close()
+
+
+@pytest.mark.parametrize("n,n_kv,dtype", [(4, 4, "f16"), (8, 2, "bf16")], ids=["mha-f16", "gqa-bf16"])
+def test_step_graph_equals_eager(kc, n, n_kv, dtype):
+    """One CUDA Graph per decode step (kc_step_graph_begin / _launch): the
+    captured-then-launched step writes the same outputs, bit for bit, and the
+    same StepStats, ledger bytes and cache rows as the eager calls."""
+    import torch
+    b, h, s0, N, L, steps = 2, 128, 500, 64, 3, 3
+    tdt = {"f16": torch.float16, "bf16": torch.bfloat16}[dtype]
+    runs = []
+    for graph in (False, True):
+        cache, ks, vs = build_cache(kc, b, n, n_kv, h, s0, dtype, resident=1, n_layers=L, max_seq=s0 + steps + 1)
+        stream = torch.cuda.Stream()
+        cache.step_stats(reset=True)
+        outs, stats = [], []
+        for step in range(steps):
+            ins = [[torch.from_numpy(synth_matrix(900 + 10 * step + l + 100 * j, b, (n if j == 0 else n_kv) * h,
+                                                  dtype=dtype)).to(tdt).cuda() for j in range(3)] for l in range(L)]
+            out = [torch.full((b, n * h), float("nan"), dtype=torch.float32, device="cuda") for _ in range(L)]
+            torch.cuda.synchronize()
+            if graph:
+                cache.step_graph_begin(N, stream)
+            for l in range(L):
+                cache.decode_step_device(l, ins[l][0], ins[l][1], ins[l][2], out[l], N, full=l < 1, stream=stream)
+            if graph:
+                cache.step_graph_launch(stream)
+            stream.synchronize()
+            outs.append([o.cpu().numpy() for o in out])
+            stats.append(cache.step_stats(reset=True))
+        rows = [cache.v_row(l, s0 + steps - 1, bb) for l in range(L) for bb in range(b)]
+        runs.append((outs, stats, cache.d2h_bytes_total(), cache.h2d_bytes_total(), rows))
+        cache.close()
+    (eo, es, ed, eh, er), (go, gs, gd, gh, gr) = runs
+    for step in range(steps):
+        for l in range(L):
+            assert not np.isnan(go[step][l]).any()
+            np.testing.assert_array_equal(go[step][l], eo[step][l])
+        assert gs[step] == es[step]
+    assert (gd, gh) == (ed, eh)
+    for a, c in zip(gr, er):
+        np.testing.assert_array_equal(a, c)
+
+
+def test_step_graph_rejects_host_io(kc):
+    import torch
+    b, n, h, s0 = 1, 2, 128, 100
+    cache, ks, vs = build_cache(kc, b, n, n, h, s0, "f16", n_layers=1, max_seq=s0 + 2)
+    stream = torch.cuda.Stream()
+    cache.step_graph_begin(8, stream)
+    with pytest.raises(kc.StateError):
+        cache.decode_step(0, synth_matrix(1, b, n * h), synth_matrix(2, b, n * h), synth_matrix(3, b, n * h), 8)
+    with pytest.raises(kc.StateError):
+        cache.step_graph_begin(8, stream)  # one capture at a time
+    cache.step_graph_launch(stream)  # ends the (empty) capture
+    stream.synchronize()
+    cache.close()

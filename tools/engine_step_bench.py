@@ -33,11 +33,12 @@ def main():
     ap.add_argument("--out", default="")
     ap.add_argument("--profile", action="store_true")
     ap.add_argument("--tune", action="append", default=[], help="key=value cache tuning knob (repeatable)")
+    ap.add_argument("--graph", default="0", help="comma list of 0/1: eager launches / one CUDA Graph per step")
     args = ap.parse_args()
     L, b, n, h, s, N = args.layers, args.batch, args.heads, 128, args.s, args.topn
     d = n * h
     groups = [int(x) for x in args.groups.split(",")]
-    total_steps = (args.steps + 4) * len(groups)
+    total_steps = (args.steps + 4) * len(groups) * len(args.graph.split(","))
     cfg = kc.ModelConfig(L, d, n, h, kc.ModelConfig.default_ffn_hidden(d), 32000, s + total_steps, n)
     cache = kc.TieredKVCache(cfg, b, kc.TierPlacement.kcache(0, L))
     kb = torch.empty(s * b, d, dtype=torch.float16, device="cuda")
@@ -62,13 +63,20 @@ def main():
     stream = torch.cuda.Stream()
     rows = []
 
+    use_graph = [False]
+
     def step(seed):
+        if use_graph[0]:
+            cache.step_graph_begin(N, stream)
         for layer in range(L):
             kc.fill_uniform(qkv, 7 + seed * 1000 + layer, stream=stream)
             cache.decode_step_device(layer, q, knew, vnew, out, N, stream=stream)
+        if use_graph[0]:
+            cache.step_graph_launch(stream)
 
     seed = 0
-    for g in groups:
+    for g, gr in [(g, gr) for gr in args.graph.split(",") for g in groups]:
+        use_graph[0] = gr == "1"
         cache.set_tuning("score_groups", g)
         for _ in range(2):
             step(seed)
@@ -92,7 +100,7 @@ def main():
         enqueue_ms = (_t.perf_counter() - c0) * 1e3
         torch.cuda.synchronize()
         cache.step_stats(reset=True)
-        if args.profile:
+        if args.profile and not use_graph[0]:
             cache.profile(True)
             step(seed)
             seed += 1
@@ -105,7 +113,7 @@ def main():
                 print("  layer", layer, "  ".join(f"{k} {(sp[k][layer][0] - t0) * 1e3:.0f}-{(sp[k][layer][1] - t0) * 1e3:.0f}"
                                                   for k in sp))
             print("  mean us:", {k: round(1e3 * sum(e - a for a, e in v) / len(v), 1) for k, v in sp.items()})
-        rec = {"score_groups": g, "tune": args.tune, "ms_per_step": ms, "host_enqueue_ms_per_step": enqueue_ms, "tokens_per_s": b / (ms * 1e-3), "per_layer_us": 1e3 * ms / L,
+        rec = {"score_groups": g, "graph": use_graph[0], "tune": args.tune, "ms_per_step": ms, "host_enqueue_ms_per_step": enqueue_ms, "tokens_per_s": b / (ms * 1e-3), "per_layer_us": 1e3 * ms / L,
                "len": cache.current_len(), "mean_dropped_mass": st["mean_dropped_mass"],
                "h2d_bytes_per_step": st["h2d_bytes"] // args.steps, "d2h_bytes_per_step": st["d2h_bytes"] // args.steps}
         print(json.dumps(rec), flush=True)
