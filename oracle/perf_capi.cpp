@@ -7,7 +7,8 @@
 // measured B200 profile (profiles/b200_profile.json, written by
 // tools/b200_profile.py in the reference's load_profile format) through the
 // reference's own load_profile and checks decode_transfer_check /
-// project_run against the measured C5 crossover. No reference source is
+// project_run against the measured C5 crossover and prefill_overlap_check
+// against the measured prefill V offload. No reference source is
 // copied into this repository.
 #include <cstring>
 #include <exception>
@@ -48,6 +49,24 @@ int ref_perf_transfer_check(const char* profile, unsigned long long s, unsigned 
     out[0] = c.beneficial ? 1.0 : 0.0;
     out[1] = c.ratio;
     out[2] = c.threshold;
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
+// prefill_overlap_check (perf_model.hpp:87-89, perf_model.cpp:147-162, the
+// paper's Eq. 1-2): out = {holds, compute_time, transfer_time, lhs, rhs}
+int ref_perf_prefill_check(const char* profile, unsigned long long s, unsigned long long d, unsigned long long b,
+                           unsigned long long bytes, double* out) {
+  try {
+    const OverlapCheck c = prefill_overlap_check(s, d, b, bytes, resolve_profile(profile));
+    out[0] = c.holds ? 1.0 : 0.0;
+    out[1] = c.compute_time;
+    out[2] = c.transfer_time;
+    out[3] = c.lhs;
+    out[4] = c.rhs;
     return 0;
   } catch (const std::exception& e) {
     g_err = e.what();

@@ -70,3 +70,28 @@ def test_projected_attention_time_bounds_the_measured_layer(perf):
         # copy-measured bw_gpu by ~10 %; the recall never beats the DMA rate
         assert t >= 0.85 * max(t_k, t_v), r
         assert t <= 2.5 * (t_k + t_v), r
+
+
+def test_prefill_offload_hides_behind_prefill_compute(perf, tmp_path):
+    """the paper's Eq. 1-2 (prefill_overlap_check,
+    perf_model.cpp:147-162) on B200 numbers -- the measured prefill V offload
+    rate (tools/prefill_offload_bench.py: the append kernel's mapped stores
+    into the host arena) as bw_d2h. At C2 (s = 32k, d = 4096, b = 8, fp16) the
+    modelled prefill compute of a layer must exceed its V offload, and the
+    model's transfer time must equal the measured offload time."""
+    meas = json.load(open(os.path.join(ROOT, "profiles", "r01_prefill_offload.json")))
+    prof = dict(json.load(open(PROFILE)))
+    prof["name"] = "b200-prefill-offload"
+    prof["bw_d2h"] = meas["offload_gbs"] * 1e9
+    path = tmp_path / "b200_offload.json"
+    path.write_text(json.dumps(prof))
+    perf.ref_perf_prefill_check.argtypes = [C.c_char_p] + [C.c_ulonglong] * 4 + [C.POINTER(C.c_double)]
+    out = (C.c_double * 5)()
+    s, d, b = 32768, 4096, 8
+    assert perf.ref_perf_prefill_check(str(path).encode(), s, d, b, 2, out) == 0, perf.ref_perf_last_error()
+    holds, compute_t, transfer_t, lhs, rhs = list(out)
+    assert holds == 1.0 and compute_t > transfer_t
+    assert lhs == (22 * d + 4 * s) / 2 and abs(rhs - prof["flops"] / prof["bw_d2h"]) <= 1e-6 * rhs
+    assert meas["v_bytes_per_layer"] == 2 * b * s * d
+    assert abs(transfer_t - meas["offload_extra_ms_per_layer"] * 1e-3) <= 0.01 * transfer_t
+    assert lhs / rhs > 2.0  # the offload hides with margin on the B200
