@@ -181,6 +181,9 @@ struct kc_cache {
   kc_step_stats step_host{};         // kc_decode_step: host-known counters
   DevBuf q32[kRing], idx[kRing], w[kRing], dropped[kRing], norm[kRing], out_tmp[kRing], idx_exp[kRing];
   PinnedBuf host_in, host_out;
+  DevBuf q_all;  // host-mode multi-layer calls: every layer's q, staged up front
+  cudaStream_t in_st = nullptr;  // host-mode q uploads (off the scoring stream)
+  cudaEvent_t ev_q0 = nullptr, ev_qall = nullptr;
   // DMA recall: pinned copy of the selection, pinned compacted rows, HBM copy
   PinnedBuf idx_host[kRing], stage_host[kRing];
   DevBuf stage_dev[kRing];
@@ -388,6 +391,10 @@ void destroy(kc_cache* c) {
   }
   if (c->gather_st) cudaStreamDestroy(c->gather_st);
   if (c->out_st) cudaStreamDestroy(c->out_st);
+  if (c->in_st) cudaStreamDestroy(c->in_st);
+  if (c->ev_q0) cudaEventDestroy(c->ev_q0);
+  if (c->ev_qall) cudaEventDestroy(c->ev_qall);
+  c->q_all.release();
   if (c->k_arena) cudaFree(c->k_arena);
   if (c->v_dev) cudaFree(c->v_dev);
   if (c->v_host) {
@@ -601,6 +608,38 @@ const float* stage_q(kc_cache* c, int slot, const void* q, int q_dtype, bool io_
   return c->q32[slot].as<float>();
 }
 
+// Host-mode multi-layer call with pinned q: upload (and convert) every
+// layer's q up front on in_st, so no H2D + conversion sits between one
+// layer's selection and the next layer's scoring on the main stream. The main
+// stream waits for layer 0's q now and for the rest before layer 1 (long
+// done by then). nullptr: some q is pageable, stage per layer instead.
+const float* stage_q_host_all(kc_cache* c, uint64_t n, const void* const* q, int q_dtype, cudaStream_t st) {
+  if (n < 2) return nullptr;
+  for (uint64_t i = 0; i < n; ++i)
+    if (!host_pinned(q[i])) return nullptr;
+  const uint64_t nq = c->batch * c->n_q * c->h;
+  const size_t bytes = nq * dtype_size(q_dtype);
+  c->q_all.ensure(checked_mul({n, nq, 4}));
+  if (q_dtype != KC_F32) c->stage_src.ensure(bytes * n);
+  // the previous call's readers of q_all / stage_src ran on st
+  CK(cudaEventRecord(c->ev_q0, st));
+  CK(cudaStreamWaitEvent(c->in_st, c->ev_q0, 0));
+  float* all = c->q_all.as<float>();
+  for (uint64_t i = 0; i < n; ++i) {
+    if (q_dtype == KC_F32) {
+      CK(cudaMemcpyAsync(all + i * nq, q[i], bytes, cudaMemcpyHostToDevice, c->in_st));
+    } else {
+      void* dst = (char*)c->stage_src.p + i * bytes;
+      CK(cudaMemcpyAsync(dst, q[i], bytes, cudaMemcpyHostToDevice, c->in_st));
+      kc::to_f32_launch(dst, q_dtype, all + i * nq, (int64_t)nq, c->in_st);
+    }
+    if (i == 0) CK(cudaEventRecord(c->ev_q0, c->in_st));
+  }
+  CK(cudaEventRecord(c->ev_qall, c->in_st));
+  CK(cudaStreamWaitEvent(st, c->ev_q0, 0));
+  return all;
+}
+
 void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const void* const* q,
                       int q_dtype, uint64_t top_n, uint32_t flags, kc_topn_out* outs,
                       cudaStream_t user_st) {
@@ -635,6 +674,7 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
   if (!io_device && c->capture_st) fail(KC_ESTATE, "host-memory I/O inside a step graph capture");
   maybe_flush_l2(c, layers, n, st);
   bool out_used = false;  // c->out_st carries work of this call
+  const float* q_all = io_device ? nullptr : stage_q_host_all(c, n, q, q_dtype, st);
   CK(cudaEventRecord(c->ev_start, st));
   if (side != st) CK(cudaStreamWaitEvent(side, c->ev_start, 0));
 
@@ -645,7 +685,9 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
     // selection of layer i-2 (which also released q32[slot]) has finished
     const int lb = side_select ? (int)(i & 1) : 0;
     if (side_select && i >= 2) CK(cudaStreamWaitEvent(st, c->ev_sel[(i - 2) % kRing], 0));
-    const float* q32 = stage_q(c, slot, q[i], q_dtype, io_device, st, i, n);
+    if (q_all && i == 1) CK(cudaStreamWaitEvent(st, c->ev_qall, 0));
+    const float* q32 = q_all ? q_all + i * (c->batch * c->n_q * c->h)
+                             : stage_q(c, slot, q[i], q_dtype, io_device, st, i, n);
     kc_topn_out& o = outs[i];
     // Offloaded layer in DMA mode: compact the selected rows on the host (pool
     // threads, stream-ordered via cudaLaunchHostFunc on gather_st), then one DMA.
@@ -964,6 +1006,9 @@ int kc_cache_create(const kc_config* cfg, uint64_t batch, uint64_t resident_laye
       CK(cudaStreamCreateWithPriority(&c->side_st, cudaStreamNonBlocking, hi));
       CK(cudaStreamCreateWithPriority(&c->gather_st, cudaStreamNonBlocking, hi));
       CK(cudaStreamCreateWithFlags(&c->out_st, cudaStreamNonBlocking));
+      CK(cudaStreamCreateWithFlags(&c->in_st, cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&c->ev_q0, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&c->ev_qall, cudaEventDisableTiming));
       CK(cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming));
       CK(cudaEventCreateWithFlags(&c->ev_end, cudaEventDisableTiming));
       CK(cudaEventCreateWithFlags(&c->ev_stats, cudaEventDisableTiming));
