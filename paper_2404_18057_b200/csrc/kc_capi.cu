@@ -858,36 +858,42 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
     c->cp_pending[slot] = cst != side;
     out_used |= cst != side;
     const uint32_t* idx_slots = c->idx[slot].as<uint32_t>();
-    if (c->G > 1 && (o.indices || !io_device)) {
-      kc::expand_idx_launch(idx_slots, c->idx_exp[slot].as<uint32_t>(), (int)c->rows, (int)c->G,
-                            g.nc, io_device ? cst : side);
-      idx_slots = c->idx_exp[slot].as<uint32_t>();
-    }
     if (io_device) {
+      if (c->G > 1 && o.indices) {
+        kc::expand_idx_launch(idx_slots, c->idx_exp[slot].as<uint32_t>(), (int)c->rows, (int)c->G, g.nc, cst);
+        idx_slots = c->idx_exp[slot].as<uint32_t>();
+      }
       if (o.indices) CK(cudaMemcpyAsync(o.indices, idx_slots, o_idx, cudaMemcpyDeviceToDevice, cst));
       if (o.weights) CK(cudaMemcpyAsync(o.weights, c->w[slot].p, o_w, cudaMemcpyDeviceToDevice, cst));
       if (o.dropped_mass)
         CK(cudaMemcpyAsync(o.dropped_mass, c->dropped[slot].p, o_dr, cudaMemcpyDeviceToDevice, cst));
       if (cst != side) CK(cudaEventRecord(c->ev_cp[slot], cst));
     } else {
-      // D2H straight into pinned user buffers, else into pinned staging; on
-      // their own stream so the next layer's recall does not queue behind them
+      // D2H straight into pinned user buffers, else into pinned staging, on
+      // their own stream: the selection outputs as soon as the selection is
+      // done (GQA index expansion there too, not on the recall stream), the
+      // attention output once the recall is
       cudaStream_t ost = side != st ? c->out_st : st;
       out_used |= ost == c->out_st;
-      if (ost != side) {
-        CK(cudaEventRecord(c->ev_out[slot], side));
-        CK(cudaStreamWaitEvent(ost, c->ev_out[slot], 0));
-      }
+      if (ost != st) CK(cudaStreamWaitEvent(ost, c->ev_sel[slot], 0));
       char* hb = (char*)c->host_out.p + i * per_layer;
       auto d2h = [&](void* user, size_t off, const void* src, size_t bytes) {
         if (!user) return;
         void* dst = host_pinned(user) ? user : (void*)(hb + off);
         CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ost));
       };
-      d2h(o.out, 0, c->out_tmp[slot].p, o_out);
+      if (c->G > 1 && o.indices) {
+        kc::expand_idx_launch(idx_slots, c->idx_exp[slot].as<uint32_t>(), (int)c->rows, (int)c->G, g.nc, ost);
+        idx_slots = c->idx_exp[slot].as<uint32_t>();
+      }
       d2h(o.indices, o_out, idx_slots, o_idx);
       d2h(o.weights, o_out + o_idx, c->w[slot].p, o_w);
       d2h(o.dropped_mass, o_out + o_idx + o_w, c->dropped[slot].p, o_dr);
+      if (ost != side) {
+        CK(cudaEventRecord(c->ev_out[slot], side));
+        CK(cudaStreamWaitEvent(ost, c->ev_out[slot], 0));
+      }
+      d2h(o.out, 0, c->out_tmp[slot].p, o_out);
       // the ring slot is free once its outputs have left the device (the main
       // stream waits on ev_rec before reusing it)
       if (ost != side) CK(cudaEventRecord(c->ev_rec[slot], ost));
