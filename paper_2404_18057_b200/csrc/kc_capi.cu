@@ -220,7 +220,8 @@ struct kc_cache {
   int keep_logits = 0;     // leave dead logits in L2 instead of discarding them
   int fuse_select = 0;     // MHA dense rows: the scoring kernel selects each row (kc_rowsel.cuh;
                            // measured slower than the separate kernel)
-  int recall_pipe = 0;    // software-pipelined recall kernel (measured: no gain, page-walk bound)
+  int recall_pipe = -1;   // software-pipelined recall kernel: -1 auto = GQA only (r01, managed
+                          // arena: C3 8.35 -> 7.9 ms per step; MHA C2 no gain)
   int recall_ctas = 32;  // CTAs of the recall kernel (0: one per (batch, kv head)); 32 measured best at C2
   int gather_threads = 0;  // 0: 3/4 of the host cores
 
@@ -815,7 +816,7 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
       }
       rp.staged = 0;
       rp.grid = c->recall_ctas;
-      rp.pipelined = c->recall_pipe;
+      rp.pipelined = c->recall_pipe < 0 ? (c->G > 1 ? 1 : 0) : c->recall_pipe;
       rp.idx = c->idx[slot].as<uint32_t>();
       rp.w = c->w[slot].as<float>();
       rp.norm = c->norm[slot].as<float>();
@@ -1503,7 +1504,7 @@ int kc_set_tuning(kc_cache* c, const char* key, int64_t value) {
     else if (k == "score_stages") c->score_stages = (int)value;
     else if (k == "score_ctas_per_sm") c->score_ctas_per_sm = (int)value;
     else if (k == "recall_ctas") c->recall_ctas = (int)value;
-    else if (k == "recall_pipe") c->recall_pipe = value ? 1 : 0;
+    else if (k == "recall_pipe") c->recall_pipe = value < 0 ? -1 : (value ? 1 : 0);
     else if (k == "side_priority") {
       // 1: the recall stream at the device's highest priority (default), 0: normal
       set_dev(c);

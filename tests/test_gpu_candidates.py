@@ -17,7 +17,7 @@ from tests.test_gpu_parity import build_cache, compare_all
 pytestmark = pytest.mark.gpu
 
 DEFAULTS = {"select_cand": 0, "cand_force_fallback": 0, "score_groups": 0, "recall_mode": 0, "score_chunk": 0,
-            "recall_pipe": 0, "score_mma": 1, "recall_ctas": 32, "select_on_side": 0, "tlb_ahead": -1, "fuse_select": 0}
+            "recall_pipe": -1, "score_mma": 1, "recall_ctas": 32, "select_on_side": 0, "tlb_ahead": -1, "fuse_select": 0}
 
 
 def _run(kc, cache, q, N, renorm=False, **tune):
@@ -118,11 +118,11 @@ def test_underflow_ties_take_lowest_positions(kc, oracle):
 
 @pytest.mark.parametrize("tune", [dict(score_groups=2), dict(score_groups=5), dict(recall_mode=2),
                                   dict(recall_mode=3), dict(select_cand=1), dict(select_cand=1, score_groups=3),
-                                  dict(recall_pipe=1), dict(recall_pipe=1, recall_ctas=0), dict(select_on_side=1),
+                                  dict(recall_pipe=1), dict(recall_pipe=1, recall_ctas=0), dict(recall_pipe=0), dict(select_on_side=1),
                                   dict(tlb_ahead=0), dict(score_chunk=4096), dict(fuse_select=1),
                                   dict(fuse_select=1, score_groups=2)],
                          ids=["groups2", "groups5", "dma", "hybrid", "cand", "cand-groups3", "recall-pipe",
-                              "recall-pipe-per-row", "side-select", "no-tlb-warm", "chunk4096", "fused-select",
+                              "recall-pipe-per-row", "recall-plain", "side-select", "no-tlb-warm", "chunk4096", "fused-select",
                                   "fused-select-groups2"])
 @pytest.mark.parametrize("n_kv", [8, 2], ids=["mha", "gqa4"])
 def test_pipeline_variants_bitwise(kc, tune, n_kv):
