@@ -403,12 +403,16 @@ def run_ours(args, cfg):
         "config": {"workload": cfg["workload"], "config": args.config, "layers": L, "batch_per_gpu": b,
                    "global_batch": b * world, "n_heads": n, "n_kv_heads": n_kv, "head_dim": h, "s": s, "top_n": N,
                    "parallelism": f"partition by request batch x{world}, no data-path collective",
-                   "l2": "inputs larger than L2 (64 GiB K per GPU)", "pipeline": "recall(l) overlaps scoring(l+1)",
+                   "l2": f"inputs larger than L2 ({L * k_bytes_layer / 2**30:.0f} GiB K per GPU)",
+                   "pipeline": "recall(l) overlaps scoring(l+1)",
                    "v_arena_numa_node": numa},
         "per_gpu_tokens_per_s": value / world,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": traffic, "peak_kind": peak_kind,
-                     "kernel": "score_fast_kernel (q.K^T, TMA bulk-staged K)",
+                     "kernel": ("score_fast_kernel (q.K^T, TMA bulk-staged K)" if n_kv == n else
+                                "score_mma_kernel (GQA q.K^T on the tensor cores, TMA bulk-staged K)"),
+                     "peak_note": "a read-only K stream against the measured read+write copy rate: frac can "
+                                  "exceed 1 (ncu: 86 % of the HW DRAM peak, profiles/)",
                      "algorithmic_bytes_per_launch": k_bytes_layer, "avg_launch_ms": score_avg_ms},
         "step_roofline": {"k_bytes_per_step": L * k_bytes_layer, "vsel_bytes_per_step": L * v_bytes_layer,
                           "hbm_gbs": hbm_peak, "h2d_gbs_measured": h2d_bw,
