@@ -32,7 +32,7 @@ sys.path.insert(0, ROOT)
 
 CONFIGS = {
     "c2": dict(workload="LLaMA2-7B-shape KCache decode attention: 32 layers, batch 8, 32k context, N=128, "
-                        "fp16 K in HBM / fp16 V in pinned host memory",
+                        "fp16 K in HBM / fp16 V in host memory (read zero-copy over PCIe)",
                n_layers=32, batch=8, n_heads=32, n_kv=32, h=128, s=32768, top_n=128),
     "c3": dict(workload="LLaMA3-8B-shape GQA (32 q / 8 kv heads) KCache decode attention: 32 layers, batch 32, "
                         "16k context, N=128",
@@ -254,6 +254,7 @@ def run_ours(args, cfg):
     numa = gpu_numa_node(local_rank)
     t0 = time.time()
     cache = kc.TieredKVCache(mcfg, b, kc.TierPlacement.kcache(0, L, 2, "f16"), device=local_rank, numa_node=numa)
+    v_arena = cache.v_arena_kind()
     for kv in args.tune:
         key, val = kv.split("=")
         cache.set_tuning(key, int(val))
@@ -405,7 +406,9 @@ def run_ours(args, cfg):
                    "parallelism": f"partition by request batch x{world}, no data-path collective",
                    "l2": f"inputs larger than L2 ({L * k_bytes_layer / 2**30:.0f} GiB K per GPU)",
                    "pipeline": "recall(l) overlaps scoring(l+1)",
-                   "v_arena_numa_node": numa},
+                   "v_arena_numa_node": numa,
+                   "v_arena": v_arena + " (UVM managed, host-resident: large GPU pages, no per-row page walks; "
+                              "pinned beyond the driver's managed-memory cap; KCACHE_V_ARENA=pinned forces pinned)"},
         "per_gpu_tokens_per_s": value / world,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": traffic, "peak_kind": peak_kind,
