@@ -218,6 +218,7 @@ struct kc_cache {
   int select_on_side = 0;  // pipelined: selection on the side stream too (measured: no gain)
   int full_fused = 1;      // decode_attention_full: fused K+V pass when V is in HBM
   int keep_logits = 0;     // leave dead logits in L2 instead of discarding them
+  int pdl = 0;             // scoring launched behind the preceding selection (PDL; measured neutral, r01)
   int fuse_select = 0;     // MHA dense rows: the scoring kernel selects each row (kc_rowsel.cuh;
                            // measured slower than the separate kernel)
   int recall_pipe = -1;   // software-pipelined recall kernel: -1 auto = GQA only (r01, managed
@@ -536,9 +537,10 @@ void maybe_flush_l2(kc_cache* c, const uint64_t* layers, uint64_t n, cudaStream_
 }
 
 void enqueue_score(kc_cache* c, uint64_t layer, const float* q32, const StepGeom& g, cudaStream_t st,
-                   int row0, int nrows, bool cand = false, int lb = 0, int slot = -1) {
+                   int row0, int nrows, bool cand = false, int lb = 0, int slot = -1, bool pdl = false) {
   kc::ScoreParams sp{};
   sp.row0 = row0;
+  sp.pdl = pdl ? 1 : 0;
   if (slot >= 0) {  // fused selection into ring slot `slot`
     sp.row_done = c->row_done.as<uint32_t>();
     sp.sel_idx = c->idx[slot].as<uint32_t>();
@@ -614,20 +616,24 @@ const float* stage_q(kc_cache* c, int slot, const void* q, int q_dtype, bool io_
 // layer's selection and the next layer's scoring on the main stream. The main
 // stream waits for layer 0's q now and for the rest before layer 1 (long
 // done by then). nullptr: some q is pageable, stage per layer instead.
-const float* stage_q_host_all(kc_cache* c, uint64_t n, const void* const* q, int q_dtype, cudaStream_t st) {
-  if (n < 2) return nullptr;
-  for (uint64_t i = 0; i < n; ++i)
-    if (!host_pinned(q[i])) return nullptr;
+const float* stage_q_all(kc_cache* c, uint64_t n, const void* const* q, int q_dtype, bool io_device,
+                         cudaStream_t st) {
+  if (n < 2 || (io_device && q_dtype == KC_F32)) return nullptr;
+  if (!io_device)
+    for (uint64_t i = 0; i < n; ++i)
+      if (!host_pinned(q[i])) return nullptr;
   const uint64_t nq = c->batch * c->n_q * c->h;
   const size_t bytes = nq * dtype_size(q_dtype);
   c->q_all.ensure(checked_mul({n, nq, 4}));
-  if (q_dtype != KC_F32) c->stage_src.ensure(bytes * n);
+  if (q_dtype != KC_F32 && !io_device) c->stage_src.ensure(bytes * n);
   // the previous call's readers of q_all / stage_src ran on st
   CK(cudaEventRecord(c->ev_q0, st));
   CK(cudaStreamWaitEvent(c->in_st, c->ev_q0, 0));
   float* all = c->q_all.as<float>();
   for (uint64_t i = 0; i < n; ++i) {
-    if (q_dtype == KC_F32) {
+    if (io_device) {  // device q of a 16-bit dtype: convert only
+      kc::to_f32_launch(q[i], q_dtype, all + i * nq, (int64_t)nq, c->in_st);
+    } else if (q_dtype == KC_F32) {
       CK(cudaMemcpyAsync(all + i * nq, q[i], bytes, cudaMemcpyHostToDevice, c->in_st));
     } else {
       void* dst = (char*)c->stage_src.p + i * bytes;
@@ -675,7 +681,14 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
   if (!io_device && c->capture_st) fail(KC_ESTATE, "host-memory I/O inside a step graph capture");
   maybe_flush_l2(c, layers, n, st);
   bool out_used = false;  // c->out_st carries work of this call
-  const float* q_all = io_device ? nullptr : stage_q_host_all(c, n, q, q_dtype, st);
+  const float* q_all = c->capture_st ? nullptr : stage_q_all(c, n, q, q_dtype, io_device, st);
+  // Programmatic dependent launch: the scoring of layer i (group g) may start
+  // behind the selection before it when nothing launches q in between (q
+  // direct or staged up front) and that selection reads the other scoring
+  // buffer (lb alternates per layer); scoring i waits for selection i-2 (the
+  // last reader of its buffer) by event.
+  const bool q_direct = q_all || (io_device && q_dtype == KC_F32);
+  const bool pdl_ok = c->pdl && side != st && !side_select && q_direct;
   CK(cudaEventRecord(c->ev_start, st));
   if (side != st) CK(cudaStreamWaitEvent(side, c->ev_start, 0));
 
@@ -684,8 +697,8 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
     const uint64_t layer = layers[i];
     // selection on the side stream: scoring buffer i % 2, free once the
     // selection of layer i-2 (which also released q32[slot]) has finished
-    const int lb = side_select ? (int)(i & 1) : 0;
-    if (side_select && i >= 2) CK(cudaStreamWaitEvent(st, c->ev_sel[(i - 2) % kRing], 0));
+    const int lb = (side_select || pdl_ok) ? (int)(i & 1) : 0;
+    if ((side_select || pdl_ok) && i >= 2) CK(cudaStreamWaitEvent(st, c->ev_sel[(i - 2) % kRing], 0));
     if (q_all && i == 1) CK(cudaStreamWaitEvent(st, c->ev_qall, 0));
     const float* q32 = q_all ? q_all + i * (c->batch * c->n_q * c->h)
                              : stage_q(c, slot, q[i], q_dtype, io_device, st, i, n);
@@ -732,7 +745,7 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
       const int r0 = gi * gsz;
       const int nr = std::min<int>(gsz, (int)c->rows - r0);
       if (nr <= 0) break;
-      enqueue_score(c, layer, q32, g, st, r0, nr, cand, lb, fused ? slot : -1);
+      enqueue_score(c, layer, q32, g, st, r0, nr, cand, lb, fused ? slot : -1, pdl_ok && (i > 0 || gi > 0));
       if (side_select) {
         CK(cudaEventRecord(c->ev_scored[slot], st));
         CK(cudaStreamWaitEvent(side, c->ev_scored[slot], 0));
@@ -740,6 +753,11 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
         CK(cudaStreamWaitEvent(st, c->ev_rec[slot], 0));
         if (c->cp_pending[slot]) CK(cudaStreamWaitEvent(st, c->ev_cp[slot], 0));
       }
+      // the scoring above may have started behind the previous selection
+      // (PDL), which orders nothing after it: make this selection wait for
+      // the previous one explicitly (they share scratch: keys, fb_flags)
+      if (pdl_ok && (i > 0 || gi > 0))
+        CK(cudaStreamWaitEvent(st, c->ev_sel[gi > 0 ? slot : (int)((i - 1) % kRing)], 0));
 
       kc::SelectParams sp{};
       sp.logits = c->logits_buf(lb);
@@ -1517,6 +1535,7 @@ int kc_set_tuning(kc_cache* c, const char* key, int64_t value) {
     else if (k == "keep_logits") c->keep_logits = value ? 1 : 0;
     else if (k == "full_fused") c->full_fused = value ? 1 : 0;
     else if (k == "fuse_select") c->fuse_select = value ? 1 : 0;
+    else if (k == "pdl") c->pdl = value ? 1 : 0;
     else if (k == "select_on_side") c->select_on_side = value ? 1 : 0;
     else if (k == "select_cand") {
       if (value < 0 || value > 2) fail(KC_EARG, "select_cand: 0 auto, 1 on, 2 off");

@@ -52,6 +52,7 @@ struct ScoreParams {
   float* sel_norm;      // [rows]
   int sel_nc;
   int keep_logits;      // 1: leave the dead logits in L2
+  int pdl;              // programmatic dependent launch behind the preceding selection
 };
 // Read `bytes` of a scratch buffer larger than L2: evicts (and so writes back)
 // every dirty L2 line, after which all stored K is clean in DRAM.

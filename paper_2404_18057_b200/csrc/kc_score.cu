@@ -930,6 +930,24 @@ int num_sms() {
   return n[dev & 63] > 0 ? n[dev & 63] : 148;
 }
 
+// Scoring launch; with p.pdl the kernel may start while the preceding kernel
+// in the stream (a selection: allow_dependent_launch) is still running -- the
+// caller guarantees it reads nothing that kernel writes.
+template <typename K>
+void launch_score(K kern, int grid, int block, size_t smem, cudaStream_t st, const ScoreParams& p) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3((unsigned)block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = p.pdl ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, kern, p);
+}
+
 template <typename T, int G, int LPR, int STAGES, bool CAND>
 void launch_fast_s(const ScoreParams& p, cudaStream_t st) {
   constexpr int ROWB = kH * (int)sizeof(T);
@@ -955,11 +973,11 @@ void launch_fast_s(const ScoreParams& p, cudaStream_t st) {
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         configured_f |= 1ull << (dev & 63);
       }
-      score_fast_kernel<T, G, LPR, STAGES, false, true><<<n_items, (kCWarps + 1) * 32, smem, st>>>(p);
+      launch_score(score_fast_kernel<T, G, LPR, STAGES, false, true>, n_items, (kCWarps + 1) * 32, smem, st, p);
       return;
     }
   }
-  score_fast_kernel<T, G, LPR, STAGES, CAND><<<grid, (kCWarps + 1) * 32, smem, st>>>(p);
+  launch_score(score_fast_kernel<T, G, LPR, STAGES, CAND>, grid, (kCWarps + 1) * 32, smem, st, p);
 }
 
 template <typename T, int G, int LPR, bool CAND>
@@ -988,7 +1006,7 @@ void launch_mma_s(const ScoreParams& p, cudaStream_t st) {
   const int n_items = p.rows * p.n_splits;
   const int per_sm = p.ctas_per_sm > 0 ? p.ctas_per_sm : 1 << 20;
   const int grid = (int)std::min<long long>(n_items, (long long)per_sm * num_sms());
-  score_mma_kernel<T, STAGES, NCW><<<grid, (NCW + 1) * 32, smem, st>>>(p);
+  launch_score(score_mma_kernel<T, STAGES, NCW>, grid, (NCW + 1) * 32, smem, st, p);
 }
 
 template <typename T>
