@@ -611,11 +611,12 @@ const float* stage_q(kc_cache* c, int slot, const void* q, int q_dtype, bool io_
   return c->q32[slot].as<float>();
 }
 
-// Host-mode multi-layer call with pinned q: upload (and convert) every
-// layer's q up front on in_st, so no H2D + conversion sits between one
+// Multi-layer call: upload (host q, pinned) and/or convert (16-bit q) every
+// layer's q up front on in_st, so no H2D or conversion sits between one
 // layer's selection and the next layer's scoring on the main stream. The main
 // stream waits for layer 0's q now and for the rest before layer 1 (long
-// done by then). nullptr: some q is pageable, stage per layer instead.
+// done by then). nullptr: nothing to stage (device fp32 q) or some host q is
+// pageable (staged per layer instead).
 const float* stage_q_all(kc_cache* c, uint64_t n, const void* const* q, int q_dtype, bool io_device,
                          cudaStream_t st) {
   if (n < 2 || (io_device && q_dtype == KC_F32)) return nullptr;
