@@ -63,6 +63,8 @@ CASES = [
     (1, 1, 1, 1, 4, 2, "f32"),         # h = 1
     (1, 4, 4, 128, 1, 4, "f16"),       # single position
     (2, 4, 4, 64, 129, 1, "bf16"),     # N = 1, generic h
+    (1, 4, 4, 128, 5000, 2000, "f16"),  # N > 1024: the full radix pass, 2000 survivors
+    (1, 4, 2, 128, 3000, 3000, "bf16"),  # N = s (GQA): everything selected
 ]
 
 
