@@ -384,13 +384,15 @@ def run_ours(args, cfg):
     score_avg_ms = score_ms / max(score_n, 1)
     achieved = k_bytes_layer / (score_avg_ms * 1e-3) / 1e9
     traffic = None
-    try:
-        with open(os.path.join(ROOT, "profiles", "ncu_score_summary.json")) as f:
-            prof = json.load(f)
+    for name in ("ncu_score_summary_%s.json" % args.config, "ncu_score_summary.json"):
+        try:
+            with open(os.path.join(ROOT, "profiles", name)) as f:
+                prof = json.load(f)
+        except (OSError, ValueError):
+            continue
         if prof.get("config") == args.config:
             traffic = prof.get("dram_bytes_per_launch")
-    except Exception:
-        pass
+            break
     t_k = L * k_bytes_layer / (hbm_peak * 1e9)
     t_v = L * v_bytes_layer / (h2d_bw * 1e9)
     value = world * b / (ms * 1e-3)
