@@ -240,12 +240,14 @@ __device__ __forceinline__ void load_stats(SelShared& S, const SelectParams& p, 
 // dropped mass and renormaliser of every q head of the group from the weights
 // just written (block-wide reductions; the weights are visible after the
 // caller's __syncthreads).
-__device__ void finish_group(SelShared& S, const SelectParams& p, int b, int kvh) {
+// wsm: the same weights staged in shared memory ([G][nc], saves the global
+// round trip), or null.
+__device__ void finish_group(SelShared& S, const SelectParams& p, int b, int kvh, const float* wsm = nullptr) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n_q = p.n_kv * p.G;
   for (int g = 0; g < p.G; ++g) {
     const size_t slot = (size_t)b * n_q + kvh * p.G + g;
-    const float* wg = p.w + slot * p.nc;
+    const float* wg = wsm ? wsm + (size_t)g * p.nc : p.w + slot * p.nc;
     double md = 0.0;
     float fs = 0.0f;
     for (int r = tid; r < p.nc; r += kT) {
@@ -291,7 +293,7 @@ __device__ __forceinline__ void drop_rows(const float* base, int64_t stride, int
 }
 
 template <int KPT>
-__global__ void __launch_bounds__(kT, 1) select_reg_kernel(const SelectParams p) {
+__device__ __forceinline__ void select_reg_body(const SelectParams& p) {
   __shared__ SelShared S;
   allow_dependent_launch();
   const int row = p.row0 + blockIdx.x;
@@ -305,9 +307,9 @@ __global__ void __launch_bounds__(kT, 1) select_reg_kernel(const SelectParams p)
   uint32_t* idx = p.idx + (size_t)row * p.nc;
   const int s = p.s, nc = p.nc;
   const int j0 = tid * KPT;
-  load_stats(S, p, b, kvh);
 
-  // keys: MHA -> ordered logit bits; GQA -> bits of sum_g p_g
+  // keys: MHA -> ordered logit bits (loaded before the stats' barrier: the
+  // two global round trips overlap); GQA -> bits of sum_g p_g (needs M, Z)
   uint32_t key[KPT];
   if (G == 1) {
     if (j0 + KPT <= s) {
@@ -323,7 +325,9 @@ __global__ void __launch_bounds__(kT, 1) select_reg_kernel(const SelectParams p)
 #pragma unroll
       for (int i = 0; i < KPT; ++i) key[i] = j0 + i < s ? ordered_bits(lbase[j0 + i]) : 0u;
     }
-  } else {
+  }
+  load_stats(S, p, b, kvh);
+  if (G != 1) {
 #pragma unroll
     for (int i = 0; i < KPT; ++i) key[i] = 0u;
     // GQA ranking key sum_g p_g: the fast exp and a reciprocal (ranking only;
@@ -454,15 +458,23 @@ __global__ void __launch_bounds__(kT, 1) select_reg_kernel(const SelectParams p)
       const uint32_t ebase = block_excl_scan(eq, S.wa);
       const bool sel = gt || (eq && ebase < keq);
       const uint32_t o = block_excl_scan(sel ? 1u : 0u, S.wb);
+      // the weights also go to shared memory (the histogram space is free
+      // now) so finish_group reduces them without a global round trip
+      float* wsm = G * nc <= kBins ? reinterpret_cast<float*>(S.hist) : nullptr;
       if (sel) {
         idx[o] = cp;
-        for (int g = 0; g < G; ++g)
-          p.w[((size_t)b * n_q + kvh * G + g) * nc + o] =
-              expf(lbase[(size_t)g * p.lstride + cp] - S.M[g]) / S.Z[g];
+        for (int g = 0; g < G; ++g) {
+          // MHA: the candidate's logit is from_ordered(ck) (-0 -> +0 changes
+          // nothing in expf(s - M)); GQA reloads each head's logit
+          const float sg = G == 1 ? from_ordered(ck) : lbase[(size_t)g * p.lstride + cp];
+          const float wv = expf(sg - S.M[g]) / S.Z[g];
+          p.w[((size_t)b * n_q + kvh * G + g) * nc + o] = wv;
+          if (wsm) wsm[(size_t)g * nc + o] = wv;
+        }
       }
       __syncthreads();
       if (!p.keep_logits) drop_rows(lbase, p.lstride, G, s);
-      finish_group(S, p, b, kvh);
+      finish_group(S, p, b, kvh, wsm);
       return;
     }
   }
@@ -536,6 +548,11 @@ __global__ void __launch_bounds__(kT, 1) select_reg_kernel(const SelectParams p)
   __syncthreads();
   if (!p.keep_logits) drop_rows(lbase, p.lstride, G, s);
   finish_group(S, p, b, kvh);
+}
+
+template <int KPT>
+__global__ void __launch_bounds__(kT, 1) select_reg_kernel(const SelectParams p) {
+  select_reg_body<KPT>(p);
 }
 
 // Any length: keys in a global scratch row (L2-resident), same rule.
