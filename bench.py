@@ -344,12 +344,15 @@ def run_ours(args, cfg):
                "weights": torch.empty(slots, nc, dtype=torch.float32, pin_memory=True).numpy(),
                "dropped": torch.empty(slots, dtype=torch.float64, pin_memory=True).numpy()} for _ in range(L)]
     e2e_steps = 0 if args.no_e2e else args.steps
+    # the decode loop's host buffers are fixed: bind them once (ctypes
+    # argument arrays), every step is one kc_decode_topn_layers call
+    e2e_call = cache.prepare_topn_layers_host(layers, qh_np, N, outs_h)
     for _ in range(args.warmup if e2e_steps else 0):
-        cache.decode_topn_layers_host(layers, qh_np, N, outs_h)
+        e2e_call()
     barrier()
     te0 = time.perf_counter()
     for _ in range(e2e_steps):
-        cache.decode_topn_layers_host(layers, qh_np, N, outs_h)
+        e2e_call()
     te1 = time.perf_counter()
     barrier()
     e2e_ms_local = (te1 - te0) * 1e3 / max(e2e_steps, 1)
@@ -359,7 +362,7 @@ def run_ours(args, cfg):
     barrier()
     h2d_local = h2d_bandwidth(torch)
     e2e_check = float(np.abs(outs_h[0]["out"]).sum())
-    del outs_h, qh, qh_np
+    del e2e_call, outs_h, qh, qh_np
 
     from paper_2404_18057_b200.sharding import max_over_ranks
     ms, e2e_ms, neg_h2d = max_over_ranks([ms_local, e2e_ms_local, -h2d_local], device=dev)
@@ -438,7 +441,7 @@ def run_ours(args, cfg):
         "h2d_ledger_bytes_per_layer": h2d_per_layer,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": L * b * d * 4,
                 "d2h_bytes_per_step": L * (b * d * 4 + slots * nc * 8 + slots * 8), "ms_per_step": e2e_ms,
-                "path": "kc_decode_topn_layers with pinned host q / outputs (TieredKVCache.decode_topn_layers_host)"},
+                "path": "kc_decode_topn_layers with pinned host q / outputs (TieredKVCache.prepare_topn_layers_host: buffers bound once, one C-ABI call per step)"},
         "kernel_isolated_ms_per_launch": {k: iso[k][0] / max(iso[k][1], 1) for k in iso},
         "serial_step_ms": serial_ms,
         "gpu_launches": launches_per_layer * L * args.steps,

@@ -673,6 +673,14 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
   const size_t o_out = slots * c->h * 4, o_idx = slots * nc * 4, o_w = slots * nc * 4, o_dr = slots * 8;
   const size_t per_layer = o_out + o_idx + o_w + o_dr;
   if (!io_device) c->host_out.ensure(per_layer * n);
+  // host mode: whether each user output buffer is pinned (D2H straight into
+  // it) -- asked once per buffer while enqueueing, reused after the sync
+  std::vector<signed char> pinned(io_device ? 0 : n * 4, -1);
+  auto user_pinned = [&](uint64_t i, int k, const void* user) {
+    signed char& f = pinned[i * 4 + k];
+    if (f < 0) f = host_pinned(user) ? 1 : 0;
+    return f != 0;
+  };
 
   cudaStream_t side = c->pipeline ? c->side_st : st;
   // the selection runs on the side stream too, so the main stream is scoring
@@ -897,23 +905,23 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
       out_used |= ost == c->out_st;
       if (ost != st) CK(cudaStreamWaitEvent(ost, c->ev_sel[slot], 0));
       char* hb = (char*)c->host_out.p + i * per_layer;
-      auto d2h = [&](void* user, size_t off, const void* src, size_t bytes) {
+      auto d2h = [&](int k, void* user, size_t off, const void* src, size_t bytes) {
         if (!user) return;
-        void* dst = host_pinned(user) ? user : (void*)(hb + off);
+        void* dst = user_pinned(i, k, user) ? user : (void*)(hb + off);
         CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ost));
       };
       if (c->G > 1 && o.indices) {
         kc::expand_idx_launch(idx_slots, c->idx_exp[slot].as<uint32_t>(), (int)c->rows, (int)c->G, g.nc, ost);
         idx_slots = c->idx_exp[slot].as<uint32_t>();
       }
-      d2h(o.indices, o_out, idx_slots, o_idx);
-      d2h(o.weights, o_out + o_idx, c->w[slot].p, o_w);
-      d2h(o.dropped_mass, o_out + o_idx + o_w, c->dropped[slot].p, o_dr);
+      d2h(1, o.indices, o_out, idx_slots, o_idx);
+      d2h(2, o.weights, o_out + o_idx, c->w[slot].p, o_w);
+      d2h(3, o.dropped_mass, o_out + o_idx + o_w, c->dropped[slot].p, o_dr);
       if (ost != side) {
         CK(cudaEventRecord(c->ev_out[slot], side));
         CK(cudaStreamWaitEvent(ost, c->ev_out[slot], 0));
       }
-      d2h(o.out, 0, c->out_tmp[slot].p, o_out);
+      d2h(0, o.out, 0, c->out_tmp[slot].p, o_out);
       // the ring slot is free once its outputs have left the device (the main
       // stream waits on ev_rec before reusing it)
       if (ost != side) CK(cudaEventRecord(c->ev_rec[slot], ost));
@@ -944,13 +952,13 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
     for (uint64_t i = 0; i < n; ++i) {
       const char* hb = (const char*)c->host_out.p + i * per_layer;
       kc_topn_out& o = outs[i];
-      auto copy = [&](void* user, size_t off, size_t bytes) {
-        if (user && !host_pinned(user)) std::memcpy(user, hb + off, bytes);
+      auto copy = [&](int k, void* user, size_t off, size_t bytes) {
+        if (user && !user_pinned(i, k, user)) std::memcpy(user, hb + off, bytes);
       };
-      copy(o.out, 0, o_out);
-      copy(o.indices, o_out, o_idx);
-      copy(o.weights, o_out + o_idx, o_w);
-      copy(o.dropped_mass, o_out + o_idx + o_w, o_dr);
+      copy(0, o.out, 0, o_out);
+      copy(1, o.indices, o_out, o_idx);
+      copy(2, o.weights, o_out + o_idx, o_w);
+      copy(3, o.dropped_mass, o_out + o_idx + o_w, o_dr);
     }
   }
 }

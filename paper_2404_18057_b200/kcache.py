@@ -544,19 +544,42 @@ class TieredKVCache:
                                 outs: Sequence[dict], renormalize=False) -> list:
         """Same with host numpy buffers (H2D of q and D2H of every output inside
         the call, which returns finished): the end-to-end path."""
+        return self.prepare_topn_layers_host(layers, qs, top_n, outs, renormalize)()
+
+    def prepare_topn_layers_host(self, layers: Sequence[int], qs: Sequence[np.ndarray], top_n: int,
+                                 outs: Sequence[dict], renormalize=False) -> "TopnLayersHostCall":
+        """decode_topn_layers_host bound to fixed host buffers: the argument
+        arrays are built once, every call() is one kc_decode_topn_layers
+        (a decode loop that refills the same pinned q / output buffers each
+        step pays no per-step marshalling)."""
+        return TopnLayersHostCall(self, layers, qs, top_n, outs, renormalize)
+
+
+class TopnLayersHostCall:
+    """One kc_decode_topn_layers call over fixed host buffers (the ctypes
+    argument arrays are built here once); keeps the buffers alive."""
+
+    def __init__(self, cache: "TieredKVCache", layers, qs, top_n: int, outs, renormalize=False):
         n = len(layers)
-        arr_l = (C.c_uint64 * n)(*layers)
-        arr_q = (C.c_void_p * n)(*[q.ctypes.data for q in qs])
-        arr_o = (_TopnOut * n)()
+        self._cache, self._qs, self._outs = cache, list(qs), list(outs)
+        self._n = n
+        self._arr_l = (C.c_uint64 * n)(*layers)
+        self._arr_q = (C.c_void_p * n)(*[q.ctypes.data for q in qs])
+        self._arr_o = (_TopnOut * n)()
         for i, o in enumerate(outs):
-            arr_o[i].out = o["out"].ctypes.data
-            arr_o[i].indices = o["indices"].ctypes.data if "indices" in o else None
-            arr_o[i].weights = o["weights"].ctypes.data if "weights" in o else None
-            arr_o[i].dropped_mass = o["dropped"].ctypes.data if "dropped" in o else None
-        dt = {np.dtype(np.float32): KC_F32, np.dtype(np.float16): KC_F16}[qs[0].dtype]
-        flags = KC_RENORMALIZE if renormalize else 0
-        _check(self._lib.kc_decode_topn_layers(self._h, n, arr_l, arr_q, dt, top_n, flags, arr_o, None))
-        return [(arr_o[i].nc, arr_o[i].h2d_bytes) for i in range(n)]
+            self._arr_o[i].out = o["out"].ctypes.data
+            self._arr_o[i].indices = o["indices"].ctypes.data if "indices" in o else None
+            self._arr_o[i].weights = o["weights"].ctypes.data if "weights" in o else None
+            self._arr_o[i].dropped_mass = o["dropped"].ctypes.data if "dropped" in o else None
+        self._dt = {np.dtype(np.float32): KC_F32, np.dtype(np.float16): KC_F16}[qs[0].dtype]
+        self._top_n = top_n
+        self._flags = KC_RENORMALIZE if renormalize else 0
+
+    def __call__(self) -> list:
+        c = self._cache
+        _check(c._lib.kc_decode_topn_layers(c._h, self._n, self._arr_l, self._arr_q, self._dt, self._top_n,
+                                            self._flags, self._arr_o, None))
+        return [(self._arr_o[i].nc, self._arr_o[i].h2d_bytes) for i in range(self._n)]
 
 
 # ---------------------------------------------------------------------------

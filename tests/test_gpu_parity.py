@@ -131,6 +131,36 @@ def test_pipelined_layers_equal_single_calls(kc):
         assert info[l] == (nc, 2 * b * n_kv * nc * h)
 
 
+def test_prepared_host_call_pinned_and_pageable(kc):
+    """The bench's end-to-end call: buffers bound once (prepare_topn_layers_host),
+    called repeatedly; pinned outputs take the direct D2H, a pageable one the
+    staging copy -- bit-identical to single-layer calls every time."""
+    import torch
+    b, n, n_kv, h, s, N, L = 2, 8, 4, 128, 600, 32, 3
+    cache, ks, vs = build_cache(kc, b, n, n_kv, h, s, "f16", n_layers=L)
+    qs = [torch.from_numpy(synth_matrix(20 + l, b, n * h)).pin_memory().numpy() for l in range(L)]
+    singles = [kc.decode_attention_topn(qs[l], cache, l, N, False) for l in range(L)]
+    nc = min(N, s)
+
+    def pinned(shape, dt):
+        return torch.zeros(shape, dtype=dt).pin_memory().numpy()
+    outs = [{"out": pinned((b, n * h), torch.float32), "indices": pinned((b * n, nc), torch.int32).view(np.uint32),
+             "weights": np.zeros((b * n, nc), np.float32), "dropped": pinned(b * n, torch.float64)}
+            for _ in range(L)]
+    call = cache.prepare_topn_layers_host(list(range(L)), qs, N, outs)
+    for _ in range(3):
+        for o in outs:
+            for a in o.values():
+                a.fill(0)
+        info = call()
+        for l in range(L):
+            np.testing.assert_array_equal(outs[l]["out"], singles[l].out)
+            np.testing.assert_array_equal(outs[l]["indices"], singles[l].selection.indices)
+            np.testing.assert_array_equal(outs[l]["weights"], singles[l].selection.weights)
+            np.testing.assert_array_equal(outs[l]["dropped"], singles[l].selection.dropped_mass)
+            assert info[l] == (nc, 2 * b * n_kv * nc * h)
+
+
 @pytest.mark.parametrize("recall_mode", [0, 1])
 def test_repeated_decode_and_decode_appends(kc, oracle, recall_mode):
     """Decode is idempotent across calls (the scoring kernel drops consumed,
