@@ -32,6 +32,7 @@ def main():
     ap.add_argument("--run-layers", default="", help="comma list: decode only these layers (default all)")
     ap.add_argument("--profile", action="store_true", help="also print per-kernel event times (perturbs overlap)")
     ap.add_argument("--per-step", action="store_true", help="print every step's time")
+    ap.add_argument("--graph", action="store_true", help="capture every step into the cache's step graph")
     args = ap.parse_args()
     L, b, n, n_kv, h, s, N = args.layers, args.batch, args.heads, args.kv, 128, args.s, args.topn
     d = n * h
@@ -67,13 +68,19 @@ def main():
     for combo in itertools.product(*vals) if vals else [()]:
         for k, v in zip(keys, combo):
             cache.set_tuning(k, v)
-        for _ in range(3):
+        def step():
+            if args.graph:
+                cache.step_graph_begin(N, stream)
             cache.decode_topn_layers_device(run, qs, N, outs, stream=stream)
+            if args.graph:
+                cache.step_graph_launch(stream)
+        for _ in range(3):
+            step()
         torch.cuda.synchronize()
         evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
         evs[0].record(stream)
         for i in range(args.steps):
-            cache.decode_topn_layers_device(run, qs, N, outs, stream=stream)
+            step()
             evs[i + 1].record(stream)
         torch.cuda.synchronize()
         ms = evs[0].elapsed_time(evs[-1]) / args.steps
