@@ -23,6 +23,8 @@
 
 #include <memory>
 
+#include <cuda.h>  // green-context types; entry points via cudaGetDriverEntryPoint (no libcuda link)
+
 #include "kc_gather.hpp"
 #include "kc_kernels.cuh"
 #include "kcache_c.h"
@@ -136,6 +138,19 @@ bool host_pinned(const void* p) {
   return a.type == cudaMemoryTypeHost;
 }
 
+// driver entry points of the green-context API, resolved through the runtime
+// (the library does not link libcuda)
+template <typename F>
+F driver_fn(const char* name) {
+  void* p = nullptr;
+  cudaDriverEntryPointQueryResult q{};
+  if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return reinterpret_cast<F>(p);
+}
+
 }  // namespace
 
 struct kc_cache {
@@ -225,6 +240,14 @@ struct kc_cache {
                           // arena: C3 8.35 -> 7.9 ms per step; MHA C2 no gain)
   int recall_ctas = 32;  // CTAs of the recall kernel (0: one per (batch, kv head)); 32 measured best at C2
   int gather_threads = 0;  // 0: 3/4 of the host cores
+  // SM partition (green contexts): the pipelined call scores on score_sms SMs
+  // and runs the selection and the recall on the rest, so the selection of
+  // layer i leaves the critical path (0 = off)
+  int score_sms = 0;
+  int green_sms = 0;                      // partition the streams below were built for
+  CUgreenCtx green[2] = {};               // [0] scoring SMs, [1] the rest
+  cudaStream_t gst_score = nullptr, gst_sel = nullptr, gst_rec = nullptr;
+  cudaEvent_t ev_gfork = nullptr, ev_gjoin = nullptr;
 
   // per-kernel CUDA-event timing (kc_profile): [kind] -> (start, stop) pairs
   bool prof_on = false;
@@ -297,6 +320,7 @@ struct kc_cache {
 };
 
 namespace {
+void release_green(kc_cache* c);  // green-context SM partition (below)
 
 template <typename F>
 int guarded(F&& f) {
@@ -425,6 +449,9 @@ void destroy(kc_cache* c) {
   if (c->ev_end) cudaEventDestroy(c->ev_end);
   if (c->ev_stats) cudaEventDestroy(c->ev_stats);
   if (c->step_exec) cudaGraphExecDestroy(c->step_exec);
+  release_green(c);
+  if (c->ev_gfork) cudaEventDestroy(c->ev_gfork);
+  if (c->ev_gjoin) cudaEventDestroy(c->ev_gjoin);
   if (c->main_st) cudaStreamDestroy(c->main_st);
   if (c->side_st) cudaStreamDestroy(c->side_st);
   delete c;
@@ -648,6 +675,76 @@ const float* stage_q_all(kc_cache* c, uint64_t n, const void* const* q, int q_dt
   return all;
 }
 
+void release_green(kc_cache* c) {
+  using DestroyFn = CUresult (*)(CUgreenCtx);
+  for (cudaStream_t* s : {&c->gst_score, &c->gst_sel, &c->gst_rec})
+    if (*s) {
+      cudaStreamSynchronize(*s);
+      cudaStreamDestroy(*s);
+      *s = nullptr;
+    }
+  static DestroyFn destroy = driver_fn<DestroyFn>("cuGreenCtxDestroy");
+  for (CUgreenCtx& g : c->green)
+    if (g) {
+      if (destroy) destroy(g);
+      g = nullptr;
+    }
+  c->green_sms = 0;
+}
+
+// Green contexts for the SM partition: c->score_sms SMs (rounded up to the
+// driver's split granularity) for the scoring, the remaining SMs for the
+// selection and the (high-priority) recall. Kernels launched on a green
+// context's stream run only on its SMs; events order work across them.
+void ensure_green(kc_cache* c) {
+  if (c->green_sms == c->score_sms && c->gst_score) return;
+  release_green(c);
+  using DevGetFn = CUresult (*)(CUdevice*, int);
+  using ResFn = CUresult (*)(CUdevice, CUdevResource*, CUdevResourceType);
+  using SplitFn = CUresult (*)(CUdevResource*, unsigned int*, const CUdevResource*, CUdevResource*, unsigned int,
+                               unsigned int);
+  using DescFn = CUresult (*)(CUdevResourceDesc*, CUdevResource*, unsigned int);
+  using CreateFn = CUresult (*)(CUgreenCtx*, CUdevResourceDesc, CUdevice, unsigned int);
+  using StreamFn = CUresult (*)(CUstream*, CUgreenCtx, unsigned int, int);
+  static DevGetFn dev_get = driver_fn<DevGetFn>("cuDeviceGet");
+  static ResFn get_res = driver_fn<ResFn>("cuDeviceGetDevResource");
+  static SplitFn split = driver_fn<SplitFn>("cuDevSmResourceSplitByCount");
+  static DescFn gen = driver_fn<DescFn>("cuDevResourceGenerateDesc");
+  static CreateFn create = driver_fn<CreateFn>("cuGreenCtxCreate");
+  static StreamFn mk_stream = driver_fn<StreamFn>("cuGreenCtxStreamCreate");
+  if (!dev_get || !get_res || !split || !gen || !create || !mk_stream)
+    fail(KC_ECUDA, "score_sms: the driver has no green-context API");
+  auto ok = [](CUresult r, const char* what) {
+    if (r != CUDA_SUCCESS) fail(KC_ECUDA, std::string("score_sms: ") + what + " failed (" + std::to_string((int)r) + ")");
+  };
+  CUdevice dev{};
+  ok(dev_get(&dev, c->device), "cuDeviceGet");
+  CUdevResource all{};
+  ok(get_res(dev, &all, CU_DEV_RESOURCE_TYPE_SM), "cuDeviceGetDevResource");
+  if ((unsigned)c->score_sms >= all.sm.smCount) fail(KC_EARG, "score_sms must leave SMs for the selection and recall");
+  CUdevResource grp{}, rest{};
+  unsigned int nb = 1;
+  ok(split(&grp, &nb, &all, &rest, 0, (unsigned)c->score_sms), "cuDevSmResourceSplitByCount");
+  if (nb != 1 || rest.sm.smCount == 0) fail(KC_EARG, "score_sms: no SMs left for the selection and recall");
+  CUdevResourceDesc da{}, db{};
+  ok(gen(&da, &grp, 1), "cuDevResourceGenerateDesc");
+  ok(gen(&db, &rest, 1), "cuDevResourceGenerateDesc");
+  ok(create(&c->green[0], da, dev, CU_GREEN_CTX_DEFAULT_STREAM), "cuGreenCtxCreate");
+  ok(create(&c->green[1], db, dev, CU_GREEN_CTX_DEFAULT_STREAM), "cuGreenCtxCreate");
+  int lo = 0, hi = 0;
+  CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  CUstream s0{}, s1{}, s2{};
+  ok(mk_stream(&s0, c->green[0], CU_STREAM_NON_BLOCKING, 0), "cuGreenCtxStreamCreate");
+  ok(mk_stream(&s1, c->green[1], CU_STREAM_NON_BLOCKING, 0), "cuGreenCtxStreamCreate");
+  ok(mk_stream(&s2, c->green[1], CU_STREAM_NON_BLOCKING, hi), "cuGreenCtxStreamCreate");
+  c->gst_score = (cudaStream_t)s0;
+  c->gst_sel = (cudaStream_t)s1;
+  c->gst_rec = (cudaStream_t)s2;
+  if (!c->ev_gfork) CK(cudaEventCreateWithFlags(&c->ev_gfork, cudaEventDisableTiming));
+  if (!c->ev_gjoin) CK(cudaEventCreateWithFlags(&c->ev_gjoin, cudaEventDisableTiming));
+  c->green_sms = c->score_sms;
+}
+
 void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const void* const* q,
                       int q_dtype, uint64_t top_n, uint32_t flags, kc_topn_out* outs,
                       cudaStream_t user_st) {
@@ -682,15 +779,26 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
     return f != 0;
   };
 
-  cudaStream_t side = c->pipeline ? c->side_st : st;
-  // the selection runs on the side stream too, so the main stream is scoring
-  // only: scoring(i+1) overlaps selection(i) as well as recall(i)
-  const bool side_select = side != st && c->select_on_side;
-  cudaStream_t selst = side_select ? side : st;
   if (!io_device && c->capture_st) fail(KC_ESTATE, "host-memory I/O inside a step graph capture");
   maybe_flush_l2(c, layers, n, st);
   bool out_used = false;  // c->out_st carries work of this call
   const float* q_all = c->capture_st ? nullptr : stage_q_all(c, n, q, q_dtype, io_device, st);
+  // SM partition: fork onto the green-context streams (scoring / selection /
+  // recall), joined back into the caller's stream at the end
+  const bool green = c->score_sms > 0 && c->pipeline && !c->capture_st;
+  const cudaStream_t call_st = st;
+  if (green) {
+    ensure_green(c);
+    CK(cudaEventRecord(c->ev_gfork, call_st));
+    for (cudaStream_t s : {c->gst_score, c->gst_sel, c->gst_rec}) CK(cudaStreamWaitEvent(s, c->ev_gfork, 0));
+    st = c->gst_score;
+  }
+  cudaStream_t side = c->pipeline ? (green ? c->gst_rec : c->side_st) : st;
+  // the selection runs on the side stream too (or its own green stream), so
+  // the main stream is scoring only: scoring(i+1) overlaps selection(i) as
+  // well as recall(i)
+  const bool side_select = side != st && (c->select_on_side || green);
+  cudaStream_t selst = side_select ? (green ? c->gst_sel : side) : st;
   // Programmatic dependent launch: the scoring of layer i (group g) may start
   // behind the selection before it when nothing launches q in between (q
   // direct or staged up front) and that selection reads the other scoring
@@ -757,7 +865,13 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
       enqueue_score(c, layer, q32, g, st, r0, nr, cand, lb, fused ? slot : -1, pdl_ok && (i > 0 || gi > 0));
       if (side_select) {
         CK(cudaEventRecord(c->ev_scored[slot], st));
-        CK(cudaStreamWaitEvent(side, c->ev_scored[slot], 0));
+        CK(cudaStreamWaitEvent(selst, c->ev_scored[slot], 0));
+        // the selection overwrites ring slot `slot`: its recall (layer i-3)
+        // and device copies must be done (same stream when selst == side)
+        if (selst != side && gi == 0 && i >= (uint64_t)kRing) {
+          CK(cudaStreamWaitEvent(selst, c->ev_rec[slot], 0));
+          if (c->cp_pending[slot]) CK(cudaStreamWaitEvent(selst, c->ev_cp[slot], 0));
+        }
       } else if (gi == 0 && i >= (uint64_t)kRing && side != st) {
         CK(cudaStreamWaitEvent(st, c->ev_rec[slot], 0));
         if (c->cp_pending[slot]) CK(cudaStreamWaitEvent(st, c->ev_cp[slot], 0));
@@ -946,6 +1060,11 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
       CK(cudaEventRecord(c->ev_end, c->out_st));
       CK(cudaStreamWaitEvent(st, c->ev_end, 0));
     }
+  }
+  if (green) {  // join the partition back into the caller's stream
+    CK(cudaEventRecord(c->ev_gjoin, st));
+    CK(cudaStreamWaitEvent(call_st, c->ev_gjoin, 0));
+    st = call_st;
   }
   if (!io_device) {
     CK(cudaStreamSynchronize(st));
@@ -1546,6 +1665,10 @@ int kc_set_tuning(kc_cache* c, const char* key, int64_t value) {
     else if (k == "fuse_select") c->fuse_select = value ? 1 : 0;
     else if (k == "pdl") c->pdl = value ? 1 : 0;
     else if (k == "select_on_side") c->select_on_side = value ? 1 : 0;
+    else if (k == "score_sms") {
+      if (value < 0) fail(KC_EARG, "score_sms must be >= 0 (0 = no SM partition)");
+      c->score_sms = (int)value;
+    }
     else if (k == "select_cand") {
       if (value < 0 || value > 2) fail(KC_EARG, "select_cand: 0 auto, 1 on, 2 off");
       c->select_cand = (int)value;

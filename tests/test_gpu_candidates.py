@@ -17,7 +17,7 @@ from tests.test_gpu_parity import build_cache, compare_all
 pytestmark = pytest.mark.gpu
 
 DEFAULTS = {"select_cand": 0, "cand_force_fallback": 0, "score_groups": 0, "recall_mode": 0, "score_chunk": 0,
-            "recall_pipe": -1, "score_mma": 1, "recall_ctas": 32, "select_on_side": 0, "tlb_ahead": -1, "fuse_select": 0, "pdl": 0}
+            "recall_pipe": -1, "score_mma": 1, "recall_ctas": 32, "select_on_side": 0, "tlb_ahead": -1, "fuse_select": 0, "pdl": 0, "score_sms": 0}
 
 
 def _run(kc, cache, q, N, renorm=False, **tune):
@@ -120,10 +120,11 @@ def test_underflow_ties_take_lowest_positions(kc, oracle):
                                   dict(recall_mode=3), dict(select_cand=1), dict(select_cand=1, score_groups=3),
                                   dict(recall_pipe=1), dict(recall_pipe=1, recall_ctas=0), dict(recall_pipe=0), dict(select_on_side=1),
                                   dict(tlb_ahead=0), dict(score_chunk=4096), dict(fuse_select=1),
-                                  dict(fuse_select=1, score_groups=2), dict(pdl=1), dict(pdl=1, score_groups=2)],
+                                  dict(fuse_select=1, score_groups=2), dict(pdl=1), dict(pdl=1, score_groups=2),
+                                  dict(score_sms=120), dict(score_sms=64, score_groups=2)],
                          ids=["groups2", "groups5", "dma", "hybrid", "cand", "cand-groups3", "recall-pipe",
                               "recall-pipe-per-row", "recall-plain", "side-select", "no-tlb-warm", "chunk4096", "fused-select",
-                                  "fused-select-groups2", "pdl", "pdl-groups2"])
+                                  "fused-select-groups2", "pdl", "pdl-groups2", "sm-partition", "sm-partition-groups2"])
 @pytest.mark.parametrize("n_kv", [8, 2], ids=["mha", "gqa4"])
 def test_pipeline_variants_bitwise(kc, tune, n_kv):
     """Row groups, host-gather DMA recall, the hybrid recall and candidate
