@@ -244,6 +244,7 @@ struct kc_cache {
   // and runs the selection and the recall on the rest, so the selection of
   // layer i leaves the critical path (0 = off)
   int score_sms = 0;
+  int green_flags = 0;  // cuDevSmResourceSplitByCount useFlags (1: ignore SM co-scheduling, finer groups)
   int green_sms = 0;                      // partition the streams below were built for
   CUgreenCtx green[2] = {};               // [0] scoring SMs, [1] the rest
   cudaStream_t gst_score = nullptr, gst_sel = nullptr, gst_rec = nullptr;
@@ -724,8 +725,10 @@ void ensure_green(kc_cache* c) {
   if ((unsigned)c->score_sms >= all.sm.smCount) fail(KC_EARG, "score_sms must leave SMs for the selection and recall");
   CUdevResource grp{}, rest{};
   unsigned int nb = 1;
-  ok(split(&grp, &nb, &all, &rest, 0, (unsigned)c->score_sms), "cuDevSmResourceSplitByCount");
+  ok(split(&grp, &nb, &all, &rest, (unsigned)c->green_flags, (unsigned)c->score_sms), "cuDevSmResourceSplitByCount");
   if (nb != 1 || rest.sm.smCount == 0) fail(KC_EARG, "score_sms: no SMs left for the selection and recall");
+  if (getenv("KCACHE_VERBOSE"))
+    fprintf(stderr, "kcache: SM partition %u scoring / %u selection+recall\n", grp.sm.smCount, rest.sm.smCount);
   CUdevResourceDesc da{}, db{};
   ok(gen(&da, &grp, 1), "cuDevResourceGenerateDesc");
   ok(gen(&db, &rest, 1), "cuDevResourceGenerateDesc");
@@ -1665,6 +1668,10 @@ int kc_set_tuning(kc_cache* c, const char* key, int64_t value) {
     else if (k == "fuse_select") c->fuse_select = value ? 1 : 0;
     else if (k == "pdl") c->pdl = value ? 1 : 0;
     else if (k == "select_on_side") c->select_on_side = value ? 1 : 0;
+    else if (k == "green_flags") {
+      c->green_flags = (int)value;
+      c->green_sms = -1;  // rebuild the partition
+    }
     else if (k == "score_sms") {
       if (value < 0) fail(KC_EARG, "score_sms must be >= 0 (0 = no SM partition)");
       c->score_sms = (int)value;
