@@ -119,84 +119,166 @@ def h2d_bandwidth(torch):
 
 
 def cpu_reference_sample(cfg, threads, passes, warm=1):
-    """The reference decode_attention_topn (oracle/_ref) on host threads over
-    one layer of the workload (all batch rows, all heads); returns
-    (seconds per layer-pass list, kind, sample text)."""
+    """The reference decode_attention_topn (oracle/_ref) on host threads: one
+    pass = a whole decode step (every layer's q against the layer cache, all
+    batch rows, all heads); returns (seconds per step list, kind, sample)."""
     from oracle.oracle import Reference, ReferenceBench
     if cfg["n_kv"] != cfg["n_heads"] or not Reference.available():
         return None
     hps = 16 if cfg["n_heads"] % 16 == 0 else cfg["n_heads"]
     rb = ReferenceBench(cfg["s"], cfg["batch"], cfg["n_heads"], cfg["h"], hps, cfg["top_n"], threads,
-                        seeds=(SEED_Q, SEED_K, SEED_V))
+                        seeds=(SEED_Q, SEED_K, SEED_V), n_layers=cfg["n_layers"])
     try:
         for _ in range(warm):
             rb.run()
         times = [rb.run()[0] for _ in range(passes)]
     finally:
         rb.close()
-    sample = (f"reference decode_attention_topn (oracle/_ref, -O3 -ffp-contract=off) on 1 of {cfg['n_layers']} "
-              f"layers x {cfg['batch']} rows x {cfg['n_heads']} heads at s={cfg['s']}, N={cfg['top_n']}, "
-              f"{threads} threads over {cfg['batch'] * cfg['n_heads'] // hps} (row, 16-head) shards; "
-              f"step time = layer time x {cfg['n_layers']}")
+    sample = (f"reference decode_attention_topn (oracle/_ref, -O3 -ffp-contract=off), a whole step: "
+              f"{cfg['n_layers']} layers' q (seeds of the GPU arm) x {cfg['batch']} rows x {cfg['n_heads']} heads "
+              f"at s={cfg['s']}, N={cfg['top_n']}, against one fp32 layer cache (the fp32 cache of all "
+              f"{cfg['n_layers']} layers would need {4 * 2 * cfg['n_layers'] * cfg['batch'] * cfg['s'] * cfg['n_heads'] * cfg['h'] / 2**30:.0f} GiB "
+              f"of host RAM; the per-layer work is identical), {threads} threads over "
+              f"{cfg['n_layers'] * cfg['batch'] * cfg['n_heads'] // hps} (layer, row, 16-head) items")
     return times, "reference", sample
+
+
+def resolve_shard(args, cfg, world):
+    """How N > 1 ranks split the work: "batch" = every rank
+    serves its own batch of cfg["batch"] sequences (weak scaling), "units" =
+    the (batch row, kv head) units of ONE global batch are partitioned
+    (strong scaling). auto: units for config 3 (a fixed global batch of 32,
+    BASELINE.json configs[2]) and whenever the weak-scaling V shards would not
+    fit in host memory; batch otherwise."""
+    if world == 1:
+        return "batch"
+    if args.shard != "auto":
+        return args.shard
+    if args.config == "c3":
+        return "units"
+    from paper_2404_18057_b200.sharding import host_mem_available
+    v_all = world * 2 * cfg["n_layers"] * cfg["batch"] * cfg["n_kv"] * cfg["s"] * cfg["h"]
+    avail = host_mem_available()
+    return "units" if avail and v_all > 0.85 * avail else "batch"
+
+
+def config_block(cfg, args, world, shard):
+    """The workload keys both arms report (same dict, so the driver can match
+    the reference arm's config to this arm's)."""
+    b, n_kv, L = cfg["batch"], cfg["n_kv"], cfg["n_layers"]
+    units = b * n_kv
+    if shard == "units":
+        per = (units + world - 1) // world
+        par = f"(batch row, kv head) units of one global batch: {per} of {units} per rank, no data-path collective"
+        gb = b
+        k_gpu = 2 * L * per * cfg["s"] * cfg["h"]
+    else:
+        par = f"partition by request batch x{world}, no data-path collective"
+        gb = b * world
+        k_gpu = 2 * L * units * cfg["s"] * cfg["h"]
+    return {"workload": cfg["workload"], "config": args.config, "layers": L, "global_batch": gb,
+            "n_heads": cfg["n_heads"], "n_kv_heads": n_kv, "head_dim": cfg["h"], "s": cfg["s"],
+            "top_n": cfg["top_n"], "shard": shard, "parallelism": par,
+            "l2": "inputs larger than L2 (%.1f GiB K per GPU)" % (k_gpu / 2**30)}
 
 
 def run_reference_arm(args, cfg):
     rank, _, world = dist_env()
     if rank != 0:
         return
+    shard = resolve_shard(args, cfg, world)
     threads = os.cpu_count() or 1
     res = cpu_reference_sample(cfg, threads, passes=args.steps, warm=args.warmup)
     if res is None:
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built or config is GQA (reference is MHA-only)"}))
         return
     times, kind, sample = res
-    t_layer = statistics.mean(times)
-    value = cfg["batch"] / (t_layer * cfg["n_layers"])
+    t_step = statistics.mean(times)
+    # whole job: the reference serves the same global batch on the host cores
+    value = (cfg["batch"] * (world if shard == "batch" else 1)) / t_step
+    if shard == "batch" and world > 1:
+        t_step = t_step * world  # the host runs every rank's batch in turn
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_layer * cfg["n_layers"] * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic (SeededRng, fp16-rounded, fed as fp32)",
-        "config": {"workload": cfg["workload"], "layers": cfg["n_layers"], "batch": cfg["batch"], "s": cfg["s"],
-                   "top_n": cfg["top_n"]},
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step * 1e3,
+        "higher_is_better": True, "scaling": "weak" if shard == "batch" else "strong", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic (SeededRng, fp16-rounded, fed as fp32)",
+        "config": config_block(cfg, args, world, shard),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-def full_kv_step(kc, torch, cfg, dev, local_rank, rank, args, barrier):
+class RankWorkload:
+    """This rank's share of the workload, resident: the TieredKVCache (K in
+    HBM, V in host memory or -- resident=True -- in HBM), the layers' q and
+    the output buffers. shard "batch": the rank's own batch of cfg["batch"]
+    sequences (data seeded per rank); "units": the rank's (batch, kv head)
+    units of the global batch (sharding.UnitShard; the global data, sliced)."""
+
+    def __init__(self, kc, torch, cfg, dev, rank, world, shard, resident=False, tune=()):
+        from paper_2404_18057_b200.sharding import UnitShard, gpu_numa_node
+        L, B, n, n_kv, h, s = (cfg[k] for k in ("n_layers", "batch", "n_heads", "n_kv", "h", "s"))
+        G = n // n_kv
+        self.numa = gpu_numa_node(dev.index)
+        if shard == "units":
+            self.shard = UnitShard(B, n_kv, G, h, world, rank)
+            mcfg = self.shard.model_config(kc, L, s)
+            self.b, self.rows = 1, self.shard.n_units
+            seed_off = 0
+        else:
+            self.shard = None
+            d = n * h
+            mcfg = kc.ModelConfig(L, d, n, h, kc.ModelConfig.default_ffn_hidden(d), 32000, s, n_kv)
+            self.b, self.rows = B, B * n_kv
+            seed_off = 1_000_003 * rank
+        self.d = mcfg.d_model
+        self.slots = self.b * mcfg.n_heads
+        self.cache = kc.TieredKVCache(mcfg, self.b, kc.TierPlacement.kcache(L if resident else 0, L, 2, "f16"),
+                                      device=dev.index, numa_node=-1 if resident else self.numa)
+        for kv in tune:
+            key, val = kv.split("=")
+            self.cache.set_tuning(key, int(val))
+        kbuf = torch.empty(s * B, n_kv * h, dtype=torch.float16, device=dev)
+        vbuf = torch.empty_like(kbuf)
+        for layer in range(L):
+            kc.fill_uniform(kbuf, SEED_K + 100 * layer + seed_off)
+            kc.fill_uniform(vbuf, SEED_V + 100 * layer + seed_off)
+            if self.shard is None:
+                self.cache.append_kv_device(layer, kbuf, vbuf)
+            else:
+                self.cache.append_kv_device(layer, self.shard.kv_rows(kbuf).contiguous(),
+                                            self.shard.kv_rows(vbuf).contiguous())
+        torch.cuda.synchronize()
+        del kbuf, vbuf
+        torch.cuda.empty_cache()
+        for layer in range(L):
+            self.cache.offload_prefill_v(layer)
+        self.cache.begin_decode()
+        self.qs = []
+        for layer in range(L):
+            q16 = torch.empty(B, n * h, dtype=torch.float16, device=dev)
+            kc.fill_uniform(q16, SEED_Q + 100 * layer + seed_off)
+            q = q16.float()
+            self.qs.append(q if self.shard is None else self.shard.q_rows(q).contiguous())
+
+    def close(self):
+        self.cache.close()
+        self.qs = []
+
+
+def full_kv_step(kc, torch, cfg, dev, rank, world, shard, args, barrier):
     """decode_attention_full over every layer with K and V resident in HBM
     (C2: 128 GiB), timed like the KCache step. Returns the per-step numbers."""
-    L, b, n, n_kv, h, s = (cfg[k] for k in ("n_layers", "batch", "n_heads", "n_kv", "h", "s"))
-    d = n * h
-    mcfg = kc.ModelConfig(L, d, n, h, kc.ModelConfig.default_ffn_hidden(d), 32000, s, n_kv)
-    cache = kc.TieredKVCache(mcfg, b, kc.TierPlacement.kcache(L, L, 2, "f16"), device=local_rank)
-    kbuf = torch.empty(s * b, n_kv * h, dtype=torch.float16, device=dev)
-    vbuf = torch.empty_like(kbuf)
-    seed_off = 1_000_003 * rank
-    for layer in range(L):
-        kc.fill_uniform(kbuf, SEED_K + 100 * layer + seed_off)
-        kc.fill_uniform(vbuf, SEED_V + 100 * layer + seed_off)
-        cache.append_kv_device(layer, kbuf, vbuf)
-    torch.cuda.synchronize()
-    del kbuf, vbuf
-    torch.cuda.empty_cache()
-    for layer in range(L):
-        cache.offload_prefill_v(layer)
-    cache.begin_decode()
-    qs = []
-    for layer in range(L):
-        q16 = torch.empty(b, d, dtype=torch.float16, device=dev)
-        kc.fill_uniform(q16, SEED_Q + 100 * layer + seed_off)
-        qs.append(q16.float())
-    outs = [torch.empty(b, d, dtype=torch.float32, device=dev) for _ in range(L)]
+    L, n_kv, h, s = (cfg[k] for k in ("n_layers", "n_kv", "h", "s"))
+    wl = RankWorkload(kc, torch, cfg, dev, rank, world, shard, resident=True)
+    outs = [torch.empty(wl.b, wl.d, dtype=torch.float32, device=dev) for _ in range(L)]
     stream = torch.cuda.Stream(device=dev)
 
     def step():
         for layer in range(L):
-            cache.decode_full_device(layer, qs[layer], outs[layer], stream=stream)
+            wl.cache.decode_full_device(layer, wl.qs[layer], outs[layer], stream=stream)
 
     for _ in range(args.warmup):
         step()
@@ -213,9 +295,9 @@ def full_kv_step(kc, torch, cfg, dev, local_rank, rank, args, barrier):
     torch.cuda.synchronize()
     barrier()
     ms = e0.elapsed_time(e1) / steps
-    kv_bytes = 2 * 2 * b * n_kv * s * h * L
-    cache.close()
-    del qs, outs
+    kv_bytes = 2 * 2 * wl.rows * s * h * L
+    wl.close()
+    del outs
     torch.cuda.empty_cache()
     return {"ms_per_step": ms, "steps": steps, "kv_bytes_per_step": kv_bytes,
             "hbm_gbs": kv_bytes / (ms * 1e-3) / 1e9, "hbm_bytes": kv_bytes}
@@ -234,51 +316,28 @@ def run_ours(args, cfg):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
 
-    L, b, n, n_kv, h, s, N = (cfg[k] for k in ("n_layers", "batch", "n_heads", "n_kv", "h", "s", "top_n"))
+    L, B, n, n_kv, h, s, N = (cfg[k] for k in ("n_layers", "batch", "n_heads", "n_kv", "h", "s", "top_n"))
     G = n // n_kv
-    d = n * h
     nc = min(N, s)
-    slots = b * n
-    mcfg = kc.ModelConfig(L, d, n, h, kc.ModelConfig.default_ffn_hidden(d), 32000, s, n_kv)
-    # every rank pins its own V shard (C2: 64 GiB): refuse cleanly rather than
-    # drive the host out of memory when the node cannot hold all shards
-    from paper_2404_18057_b200.sharding import gpu_numa_node, host_mem_available
+    shard = resolve_shard(args, cfg, world)
+    # every rank keeps its V shard in host memory (C2 weak scaling: 64 GiB per
+    # rank): refuse cleanly rather than drive the host out of memory
+    from paper_2404_18057_b200.sharding import host_mem_available, partition_units
     local_world = int(os.environ.get("LOCAL_WORLD_SIZE", world))
-    v_bytes_rank = 2 * L * b * n_kv * s * h
+    rows_rank = len(partition_units(B, n_kv, world, rank)) if shard == "units" else B * n_kv
+    v_bytes_rank = 2 * L * rows_rank * s * h
     avail = host_mem_available()
     if avail and local_world * v_bytes_rank > 0.92 * avail:
         if rank == 0:
-            print(json.dumps({"metric": METRIC, "error": "host memory: %d ranks x %.1f GiB pinned V shards exceed "
+            print(json.dumps({"metric": METRIC, "error": "host memory: %d ranks x %.1f GiB V shards exceed "
                               "MemAvailable %.1f GiB" % (local_world, v_bytes_rank / 2**30, avail / 2**30)}))
         sys.exit(3)
-    numa = gpu_numa_node(local_rank)
     t0 = time.time()
-    cache = kc.TieredKVCache(mcfg, b, kc.TierPlacement.kcache(0, L, 2, "f16"), device=local_rank, numa_node=numa)
+    wl = RankWorkload(kc, torch, cfg, dev, rank, world, shard, tune=args.tune)
+    cache, qs, b, d, slots = wl.cache, wl.qs, wl.b, wl.d, wl.slots
+    numa = wl.numa
     v_arena = cache.v_arena_kind()
-    for kv in args.tune:
-        key, val = kv.split("=")
-        cache.set_tuning(key, int(val))
-    rows = s * b
-    kbuf = torch.empty(rows, n_kv * h, dtype=torch.float16, device=dev)
-    vbuf = torch.empty_like(kbuf)
-    seed_off = 1_000_003 * rank
-    for layer in range(L):
-        kc.fill_uniform(kbuf, SEED_K + 100 * layer + seed_off)
-        kc.fill_uniform(vbuf, SEED_V + 100 * layer + seed_off)
-        cache.append_kv_device(layer, kbuf, vbuf)
-    torch.cuda.synchronize()
-    del kbuf, vbuf
-    torch.cuda.empty_cache()
-    for layer in range(L):
-        cache.offload_prefill_v(layer)
-    cache.begin_decode()
     setup_s = time.time() - t0
-
-    qs = []
-    for layer in range(L):
-        q16 = torch.empty(b, d, dtype=torch.float16, device=dev)
-        kc.fill_uniform(q16, SEED_Q + 100 * layer + seed_off)
-        qs.append(q16.float())
     outs = [{"out": torch.empty(b, d, dtype=torch.float32, device=dev),
              "indices": torch.empty(slots, nc, dtype=torch.int32, device=dev),
              "weights": torch.empty(slots, nc, dtype=torch.float32, device=dev),
@@ -363,18 +422,25 @@ def run_ours(args, cfg):
     h2d_local = h2d_bandwidth(torch)
     e2e_check = float(np.abs(outs_h[0]["out"]).sum())
     del e2e_call, outs_h, qh, qh_np
+    # unit shards: gather layer 0's outputs of every rank into the global
+    # [batch, d] (outside the timed region; verification / checksum only)
+    gathered = None
+    if shard == "units":
+        from paper_2404_18057_b200.sharding import gather_units
+        full_out = gather_units(outs[0]["out"], wl.shard)
+        gathered = {"shape": list(full_out.shape), "abs_sum": float(full_out.abs().sum())}
 
     from paper_2404_18057_b200.sharding import max_over_ranks
     ms, e2e_ms, neg_h2d = max_over_ranks([ms_local, e2e_ms_local, -h2d_local], device=dev)
     h2d_bw = -neg_h2d
-    cache.close()
-    del qs, outs
+    wl.close()
+    del qs, outs, cache
     torch.cuda.empty_cache()
 
     # ---- the comparator: full-KV-in-HBM decode attention on the same workload ----
     full = None
     if not args.no_full_kv:
-        full = full_kv_step(kc, torch, cfg, dev, local_rank, rank, args, barrier)
+        full = full_kv_step(kc, torch, cfg, dev, rank, world, shard, args, barrier)
         if world > 1:
             from paper_2404_18057_b200.sharding import max_over_ranks
             full["ms_per_step"] = max_over_ranks([full["ms_per_step"]], device=dev)[0]
@@ -386,12 +452,15 @@ def run_ours(args, cfg):
         return
 
     hbm_peak, peak_kind = measured_peaks()
-    k_bytes_layer = 2 * b * n_kv * s * h
-    v_bytes_layer = 2 * b * n_kv * nc * h
+    k_bytes_layer = 2 * wl.rows * s * h  # this rank's K per layer (one scoring launch's bytes)
+    v_bytes_layer = 2 * wl.rows * nc * h
     score_avg_ms = score_ms / max(score_n, 1)
     achieved = k_bytes_layer / (score_avg_ms * 1e-3) / 1e9
     traffic = None
-    for name in ("ncu_score_summary_%s.json" % args.config, "ncu_score_summary.json"):
+    # the committed ncu capture is of the N=1 launch (same bytes per launch as
+    # a batch shard; a unit shard's launch is smaller)
+    for name in (("ncu_score_summary_%s.json" % args.config, "ncu_score_summary.json")
+                 if shard == "batch" else ()):
         try:
             with open(os.path.join(ROOT, "profiles", name)) as f:
                 prof = json.load(f)
@@ -402,22 +471,20 @@ def run_ours(args, cfg):
             break
     t_k = L * k_bytes_layer / (hbm_peak * 1e9)
     t_v = L * v_bytes_layer / (h2d_bw * 1e9)
-    value = world * b / (ms * 1e-3)
-    e2e_value = world * b / (e2e_ms * 1e-3)
+    global_batch = B * world if shard == "batch" else B
+    value = global_batch / (ms * 1e-3)
+    e2e_value = global_batch / (e2e_ms * 1e-3)
     launches_per_layer = 3 + (1 if G > 1 else 0)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak" if shard == "batch" else "strong",
         "vs_baseline": None, "dtype": "f16 storage / f32 accumulate",
         "data": "synthetic (SeededRng SplitMix64 U[-1,1], fp16-rounded)",
-        "config": {"workload": cfg["workload"], "config": args.config, "layers": L, "batch_per_gpu": b,
-                   "global_batch": b * world, "n_heads": n, "n_kv_heads": n_kv, "head_dim": h, "s": s, "top_n": N,
-                   "parallelism": f"partition by request batch x{world}, no data-path collective",
-                   "l2": f"inputs larger than L2 ({L * k_bytes_layer / 2**30:.0f} GiB K per GPU)",
-                   "pipeline": "recall(l) overlaps scoring(l+1)",
-                   "v_arena_numa_node": numa,
-                   "v_arena": v_arena + " (UVM managed, host-resident: large GPU pages, no per-row page walks; "
-                              "pinned beyond the driver's managed-memory cap; KCACHE_V_ARENA=pinned forces pinned)"},
+        "config": config_block(cfg, args, world, shard),
+        "placement": {"pipeline": "recall(l) overlaps scoring(l+1)", "v_arena_numa_node": numa,
+                      "v_arena": v_arena + " (UVM managed, host-resident: large GPU pages, no per-row page walks; "
+                                 "pinned beyond the driver's managed-memory cap; KCACHE_V_ARENA=pinned forces pinned)"},
         "per_gpu_tokens_per_s": value / world,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": traffic, "peak_kind": peak_kind,
@@ -449,18 +516,20 @@ def run_ours(args, cfg):
         "setup_s": setup_s,
         "e2e_checksum": e2e_check,
     }
+    if gathered is not None:
+        line["gathered_layer0_out"] = gathered
     line["roofline"]["achieved_isolated"] = k_bytes_layer / (iso["score"][0] / max(iso["score"][1], 1) * 1e-3) / 1e9
     if full is not None:
         full_ms = full["ms_per_step"]
-        line["full_kv"] = dict(full, value=world * b / (full_ms * 1e-3), unit=UNIT,
+        line["full_kv"] = dict(full, value=global_batch / (full_ms * 1e-3), unit=UNIT,
                                kcache_over_full=full_ms / ms,
                                note="same workload with K and V in HBM, fused flash-decode kernel "
                                     "(decode_attention_full, attention.cpp:91-114): the paper's comparator")
     if world == 1 and not args.no_cpu_baseline:
-        res = cpu_reference_sample(cfg, os.cpu_count() or 1, passes=1)
+        res = cpu_reference_sample(cfg, os.cpu_count() or 1, passes=1, warm=0)
         if res is not None:
             times, kind, sample = res
-            cpu_val = b / (statistics.mean(times) * L)
+            cpu_val = b / statistics.mean(times)
             line["cpu_baseline"] = {"value": cpu_val, "unit": UNIT, "cores": os.cpu_count() or 1, "kind": kind,
                                     "sample": sample}
     print(json.dumps(line), flush=True)
@@ -480,6 +549,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-full-kv", action="store_true", help="skip the full-KV-in-HBM comparator")
     ap.add_argument("--tune", action="append", default=[], help="kc_set_tuning key=value")
+    ap.add_argument("--shard", default="auto", choices=["auto", "batch", "units"],
+                    help="N>1: own batch per rank (weak) or (batch, kv head) units of one batch (strong)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = dict(CONFIGS[args.config])

@@ -99,7 +99,10 @@ int kc_cache_destroy(kc_cache* cache);
  * [rows][n_kv_heads*head_dim], position-major (all batch rows of a position
  * together); rows a positive multiple of batch. Converted on device. */
 int kc_append_kv(kc_cache* cache, uint64_t layer, const float* k, const float* v, uint64_t rows);
-/* Same, from device buffers of `dtype`, asynchronous on `stream`. */
+/* Same, from device buffers of `dtype`, asynchronous on `stream`. The cache's
+ * host-mode calls (and kc_sync) are ordered after the last such append; a
+ * KC_IO_DEVICE call on another stream than `stream` must be ordered by the
+ * caller (same stream, or an event). */
 int kc_append_kv_device(kc_cache* cache, uint64_t layer, const void* k, const void* v, int dtype,
                         uint64_t rows, void* stream);
 
@@ -200,7 +203,8 @@ int kc_layer_storage(const kc_cache* cache, uint64_t layer, void** k, void** v, 
  * offloaded layer, 3 = the first layers managed, the rest pinned (the
  * driver's managed-memory cap). */
 int kc_v_arena_kind(const kc_cache* cache, int* kind);
-/* Wait for all work the cache enqueued. */
+/* Wait for all work the cache enqueued: every stream it owns and the last
+ * kc_append_kv_device on the caller's stream. */
 int kc_sync(kc_cache* cache);
 /* Tuning knobs ("score_chunk", "recall_ctas", ...); DESIGN.md lists them. */
 int kc_set_tuning(kc_cache* cache, const char* key, int64_t value);
@@ -217,6 +221,22 @@ int kc_profile_read(kc_cache* cache, const char* kernel, double* total_ms, uint6
 int kc_profile_launch(kc_cache* cache, const char* kernel, uint64_t i, double* ms);
 /* start / end of launch i in ms since the first profiled event (timelines) */
 int kc_profile_span(kc_cache* cache, const char* kernel, uint64_t i, double* t0, double* t1);
+
+/* The split length (positions per scoring work item) the store picks on its
+ * own ("score_chunk" 0) for s positions over `rows` (batch x kv head) rows of
+ * GQA group `group`. Setting it explicitly on a cache holding a subset of the
+ * rows reproduces the full cache's softmax rounding bit for bit (sharding). */
+int kc_score_chunk_plan(uint64_t s, uint64_t rows, uint64_t group, int64_t* chunk);
+
+/* prefill_attention (attention.hpp:40, attention.cpp:31-62) on the GPU:
+ * causal attention of one sequence, q/k/v/out [s][n_heads*head_dim] fp32,
+ * the reference's dot, softmax and accumulation order. Host pointers,
+ * synchronous, on `device` (< 0: the calling thread's current device). */
+int kc_prefill_attention(const float* q, const float* k, const float* v, uint64_t s, uint64_t n_heads,
+                         uint64_t head_dim, float* out, int device);
+/* Same with device pointers, asynchronous on `stream`. */
+int kc_prefill_attention_device(const float* q, const float* k, const float* v, uint64_t s, uint64_t n_heads,
+                                uint64_t head_dim, float* out, void* stream);
 
 /* arg_topk (matrix.hpp:49-52, matrix.cpp:109-122) on the GPU: indices of the
  * k largest of n host floats, ties to the lowest index, ascending. */

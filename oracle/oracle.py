@@ -205,12 +205,15 @@ class Reference:
                                                                   _fp, _u32p, _fp, _dp, _u64p, _u64p]
         lib.kcref_decode_full.restype = _c.c_int
         lib.kcref_decode_full.argtypes = [_sz] * 4 + [_fp] * 3 + [_c.c_int, _fp]
+        lib.kcref_prefill.restype = _c.c_int
+        lib.kcref_prefill.argtypes = [_sz] * 3 + [_fp] * 4
         lib.kcref_arg_topk.restype = _c.c_long
         lib.kcref_arg_topk.argtypes = [_fp, _sz, _sz, _u32p]
         lib.kcref_softmax.argtypes = [_fp, _sz]
         lib.kcref_rng_uniform.argtypes = [_c.c_uint64, _sz, _c.c_float, _c.c_float, _fp]
         lib.kcref_bench_create.restype = _c.c_void_p
-        lib.kcref_bench_create.argtypes = [_sz] * 6 + [_c.c_int, _c.c_uint, _c.c_uint64, _c.c_uint64, _c.c_uint64]
+        lib.kcref_bench_create.argtypes = [_sz] * 6 + [_c.c_int, _c.c_uint, _c.c_uint64, _c.c_uint64, _c.c_uint64,
+                                                       _sz]
         lib.kcref_bench_run.restype = _c.c_double
         lib.kcref_bench_run.argtypes = [_c.c_void_p, _dp]
         lib.kcref_bench_destroy.argtypes = [_c.c_void_p]
@@ -218,6 +221,15 @@ class Reference:
 
     def _err(self, rc):
         raise RuntimeError(f"reference {REF_ERRORS.get(rc, rc)}: {self.lib.kcref_last_error().decode()}")
+
+    def prefill_attention(self, q, k, v, n_heads):
+        q, k, v = (np.ascontiguousarray(a, np.float32) for a in (q, k, v))
+        s, d = q.shape
+        out = np.zeros((s, d), np.float32)
+        rc = self.lib.kcref_prefill(s, n_heads, d // n_heads, _f(q), _f(k), _f(v), _f(out))
+        if rc:
+            self._err(rc)
+        return out
 
     def decode_topn(self, q, k, v, batch, n_heads, h, s, top_n, renormalize=False, ordered=True, resident=False):
         q = np.ascontiguousarray(q, np.float32)
@@ -269,10 +281,11 @@ class Reference:
 class ReferenceBench:
     """The reference decode_attention_topn timed on host threads (cpu baseline)."""
 
-    def __init__(self, s, batch, n_heads, h, heads_per_shard, top_n, threads, seeds=(1, 2, 3), renormalize=False):
+    def __init__(self, s, batch, n_heads, h, heads_per_shard, top_n, threads, seeds=(1, 2, 3), renormalize=False,
+                 n_layers=1):
         self.ref = Reference()
         self.handle = self.ref.lib.kcref_bench_create(s, batch, n_heads, h, heads_per_shard, top_n,
-                                                      int(renormalize), threads, *seeds)
+                                                      int(renormalize), threads, *seeds, n_layers)
         if not self.handle:
             raise RuntimeError(self.ref.lib.kcref_last_error().decode())
 

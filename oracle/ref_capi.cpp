@@ -151,6 +151,19 @@ int kcref_decode_full(std::size_t batch, std::size_t n_heads, std::size_t h, std
   }
 }
 
+// prefill_attention (attention.cpp:31-62): one sequence, [s][n_heads*h].
+int kcref_prefill(std::size_t s, std::size_t n_heads, std::size_t h, const float* q, const float* k,
+                  const float* v, float* out) {
+  try {
+    const std::size_t d = n_heads * h;
+    const Matrix r = prefill_attention(from_ptr(s, d, q), from_ptr(s, d, k), from_ptr(s, d, v), n_heads);
+    std::memcpy(out, r.data.data(), r.data.size() * sizeof(float));
+    return 0;
+  } catch (...) {
+    return map_exception();
+  }
+}
+
 // arg_topk (matrix.cpp:109-122). Returns the count, or -(error code).
 long kcref_arg_topk(const float* values, std::size_t n, std::size_t k, uint32_t* out) {
   try {
@@ -186,9 +199,13 @@ struct KcrefBench {
   unsigned threads = 1;
 };
 
+// n_layers q sets (seed_q + 100*layer, the GPU bench's q seeds) against one
+// layer's cache: one run = decode_attention_topn of every layer for every
+// (row, head-group) shard -- a whole decode step's work, timed as such.
 void* kcref_bench_create(std::size_t s, std::size_t batch, std::size_t n_heads, std::size_t h,
                          std::size_t heads_per_shard, std::size_t top_n, int renormalize,
-                         unsigned threads, uint64_t seed_q, uint64_t seed_k, uint64_t seed_v) {
+                         unsigned threads, uint64_t seed_q, uint64_t seed_k, uint64_t seed_v,
+                         std::size_t n_layers) {
   try {
     if (heads_per_shard == 0 || n_heads % heads_per_shard != 0) {
       throw ShapeError("heads_per_shard must divide n_heads");
@@ -202,7 +219,8 @@ void* kcref_bench_create(std::size_t s, std::size_t batch, std::size_t n_heads, 
     const std::size_t n_shards = batch * groups;
     const ModelConfig c = make_config(1, heads_per_shard, h, s);
     bench->caches.resize(n_shards);
-    bench->qs.resize(n_shards);
+    const std::size_t n_sets = n_layers ? n_layers : 1;
+    bench->qs.resize(n_sets * n_shards);
     std::atomic<std::size_t> next{0};
     std::vector<std::thread> pool;
     for (unsigned t = 0; t < bench->threads; ++t) {
@@ -210,7 +228,7 @@ void* kcref_bench_create(std::size_t s, std::size_t batch, std::size_t n_heads, 
         for (std::size_t sh = next++; sh < n_shards; sh = next++) {
           const std::size_t b = sh / groups, grp = sh % groups;
           const std::size_t col0 = grp * heads_per_shard * h;
-          Matrix km(s, c.d_model), vm(s, c.d_model), qm(1, c.d_model);
+          Matrix km(s, c.d_model), vm(s, c.d_model);
           for (std::size_t pos = 0; pos < s; ++pos) {
             const uint64_t base = (pos * batch + b) * D + col0;
             for (std::size_t col = 0; col < c.d_model; ++col) {
@@ -218,15 +236,18 @@ void* kcref_bench_create(std::size_t s, std::size_t batch, std::size_t n_heads, 
               vm.data[pos * c.d_model + col] = synth_f16(seed_v, base + col, -1.0f, 1.0f);
             }
           }
-          for (std::size_t col = 0; col < c.d_model; ++col) {
-            qm.data[col] = synth_f16(seed_q, b * D + col0 + col, -1.0f, 1.0f);
+          for (std::size_t l = 0; l < n_sets; ++l) {
+            Matrix ql(1, c.d_model);
+            for (std::size_t col = 0; col < c.d_model; ++col) {
+              ql.data[col] = synth_f16(seed_q + 100 * l, b * D + col0 + col, -1.0f, 1.0f);
+            }
+            bench->qs[l * n_shards + sh] = std::move(ql);
           }
           auto cache = std::make_unique<TieredKVCache>(c, 1, TierPlacement::kcache(0, 1));
           cache->append_kv(0, km, vm);
           cache->offload_prefill_v(0);
           cache->begin_decode();
           bench->caches[sh] = std::move(cache);
-          bench->qs[sh] = std::move(qm);
         }
       });
     }
@@ -238,10 +259,12 @@ void* kcref_bench_create(std::size_t s, std::size_t batch, std::size_t n_heads, 
   }
 }
 
-// One pass over every shard; returns wall seconds of the decode calls only.
+// One pass over every (q set, shard); returns wall seconds of the decode
+// calls only.
 double kcref_bench_run(void* handle, double* checksum) {
   auto* bench = static_cast<KcrefBench*>(handle);
-  const std::size_t n = bench->caches.size();
+  const std::size_t n = bench->qs.size();
+  const std::size_t n_shards = bench->caches.size();
   std::vector<double> sums(n, 0.0);
   std::atomic<std::size_t> next{0};
   const auto t0 = std::chrono::steady_clock::now();
@@ -249,7 +272,7 @@ double kcref_bench_run(void* handle, double* checksum) {
   for (unsigned t = 0; t < bench->threads; ++t) {
     pool.emplace_back([&] {
       for (std::size_t sh = next++; sh < n; sh = next++) {
-        TopNResult r = decode_attention_topn(bench->qs[sh], *bench->caches[sh], 0, bench->top_n,
+        TopNResult r = decode_attention_topn(bench->qs[sh], *bench->caches[sh % n_shards], 0, bench->top_n,
                                              bench->renormalize != 0);
         double acc = 0.0;
         for (float x : r.out.data) acc += x;

@@ -8,6 +8,7 @@
 #include <string>
 
 #include "kcache/attention.hpp"
+#include "kcache/b200.hpp"
 #include "kcache/checked.hpp"
 #include "kcache/errors.hpp"
 #include "kcache/kv_cache.hpp"
@@ -33,7 +34,6 @@ void check(int rc) {
   }
 }
 
-std::size_t kv_width(const ModelConfig& c) { return c.kv_heads() * c.head_dim; }
 
 }  // namespace
 
@@ -47,7 +47,6 @@ void ModelConfig::validate() const {
   if (d_model != n_heads * head_dim) {
     throw ShapeError("ModelConfig: d_model must equal n_heads * head_dim");
   }
-  if (n_heads % kv_heads() != 0) throw ShapeError("ModelConfig: n_kv_heads must divide n_heads");
 }
 
 std::size_t ModelConfig::default_ffn_hidden(std::size_t d) {
@@ -55,10 +54,10 @@ std::size_t ModelConfig::default_ffn_hidden(std::size_t d) {
   return (eight_thirds + 15) / 16 * 16;
 }
 
-ModelConfig ModelConfig::toy() { return ModelConfig{4, 64, 4, 16, 176, 256, 4096, 0}; }
+ModelConfig ModelConfig::toy() { return ModelConfig{4, 64, 4, 16, 176, 256, 4096}; }
 
 ModelConfig ModelConfig::shape_7b() {
-  return ModelConfig{32, 4096, 32, 128, default_ffn_hidden(4096), 32000, 32768, 0};
+  return ModelConfig{32, 4096, 32, 128, default_ffn_hidden(4096), 32000, 32768};
 }
 
 std::uint64_t param_count(const ModelConfig& c) {
@@ -131,8 +130,11 @@ TieredKVCache::TieredKVCache(const ModelConfig& config, std::size_t batch, TierP
     throw ShapeError("TieredKVCache: placement layer count differs from config");
   }
   if (batch_ == 0) throw ShapeError("TieredKVCache: batch must be >= 1");
-  kc_config c{config_.n_layers, config_.d_model, config_.n_heads, config_.kv_heads(),
-              config_.head_dim, config_.max_seq};
+  const std::size_t kv = placement_.kv_heads(config_);
+  if (kv == 0 || config_.n_heads % kv != 0) {
+    throw ShapeError("TierPlacement: n_kv_heads must divide n_heads");
+  }
+  kc_config c{config_.n_layers, config_.d_model, config_.n_heads, kv, config_.head_dim, config_.max_seq};
   check(kc_cache_create(&c, batch_, placement_.resident_layers, placement_.bytes_per_element,
                         static_cast<int>(placement_.storage), fast_capacity_bytes.has_value() ? 1 : 0,
                         fast_capacity_bytes.value_or(0), device, -1, &handle_));
@@ -182,7 +184,7 @@ void TieredKVCache::append_kv(std::size_t layer, const Matrix& k_rows, const Mat
   if (layer >= config_.n_layers) {
     throw std::out_of_range("TieredKVCache: layer " + std::to_string(layer) + " out of range");
   }
-  const std::size_t w = kv_width(config_);
+  const std::size_t w = placement_.kv_heads(config_) * config_.head_dim;
   if (k_rows.cols != w || v_rows.cols != w) {
     throw ShapeError("append_kv: row width must equal d_model");
   }
@@ -233,14 +235,14 @@ GatheredV TieredKVCache::gather_v(std::size_t layer, const SelectionIndices& sel
 
 std::span<const float> TieredKVCache::k_row(std::size_t layer, std::size_t pos,
                                             std::size_t batch_idx) const {
-  row_stage_.resize(kv_width(config_));
+  row_stage_.resize(placement_.kv_heads(config_) * config_.head_dim);
   check(kc_read_row(handle_, layer, pos, batch_idx, 0, row_stage_.data()));
   return {row_stage_.data(), row_stage_.size()};
 }
 
 std::span<const float> TieredKVCache::v_row(std::size_t layer, std::size_t pos,
                                             std::size_t batch_idx) const {
-  row_stage_.resize(kv_width(config_));
+  row_stage_.resize(placement_.kv_heads(config_) * config_.head_dim);
   check(kc_read_row(handle_, layer, pos, batch_idx, 1, row_stage_.data()));
   return {row_stage_.data(), row_stage_.size()};
 }
@@ -303,11 +305,24 @@ Matrix decode_attention_full(const Matrix& q, const TieredKVCache& cache, std::s
   return out;
 }
 
+Matrix prefill_attention(const Matrix& q, const Matrix& k, const Matrix& v, std::size_t n_heads) {
+  // attention.cpp:31-37
+  if (!q.same_shape(k) || !q.same_shape(v)) throw ShapeError("prefill_attention: Q/K/V shapes differ");
+  if (n_heads == 0 || q.cols % n_heads != 0) throw ShapeError("prefill_attention: cols must divide into heads");
+  Matrix out(q.rows, q.cols);
+  if (q.rows == 0) return out;
+  check(kc_prefill_attention(q.data.data(), k.data.data(), v.data.data(), q.rows, n_heads, q.cols / n_heads,
+                             out.data.data(), -1));
+  return out;
+}
+
+namespace b200 {
+
 Matrix decode_step_attention(const Matrix& q, const Matrix& k_rows, const Matrix& v_rows,
                              TieredKVCache& cache, std::size_t layer, bool use_topn,
                              std::size_t top_n, bool renormalize) {
   if (use_topn && top_n == 0) throw std::invalid_argument("decode_attention_topn: top_n must be >= 1");
-  const std::size_t width = cache.config().kv_heads() * cache.config().head_dim;
+  const std::size_t width = cache.placement().kv_heads(cache.config()) * cache.config().head_dim;
   if (k_rows.cols != width || v_rows.cols != width)
     throw ShapeError("append_kv: row width must equal d_model");
   if (k_rows.rows != cache.batch() || v_rows.rows != cache.batch())
@@ -321,16 +336,18 @@ Matrix decode_step_attention(const Matrix& q, const Matrix& k_rows, const Matrix
   return out;
 }
 
-StepStats read_step_stats(TieredKVCache& cache) {
+DeviceStepStats read_step_stats(TieredKVCache& cache) {
   kc_step_stats s{};
   check(kc_step_stats_read(cache.handle(), &s, 1));
-  StepStats out;
+  DeviceStepStats out;
   out.h2d_bytes = s.h2d_bytes;
   out.d2h_bytes = s.d2h_bytes;
   out.mean_dropped_mass = s.selections ? s.dropped_sum / static_cast<double>(s.selections) : 0.0;
-  for (std::size_t i = 0; i < kPositionHistogramBins; ++i) out.position_histogram[i] = s.position_histogram[i];
+  for (std::size_t i = 0; i < kHistogramBins; ++i) out.position_histogram[i] = s.position_histogram[i];
   return out;
 }
+
+}  // namespace b200
 
 TopNResult decode_attention_topn(const Matrix& q, TieredKVCache& cache, std::size_t layer,
                                  std::size_t top_n, bool renormalize, bool ordered_accumulation,

@@ -113,7 +113,6 @@ struct LedgerEvent {
 
 struct LayerState {
   uint64_t len = 0;
-  uint64_t clean_len = 0;  // K positions written back to DRAM (safe to drop from L2)
   bool offloaded = false;
   uint64_t k_elems = 0, vfast_elems = 0, vslow_elems = 0;
 };
@@ -208,12 +207,19 @@ struct kc_cache {
               ev_gath[kRing] = {}, ev_scored[kRing] = {}, ev_out[kRing] = {}, ev_cp[kRing] = {},
               ev_stats = nullptr;
   bool cp_pending[kRing] = {};  // ev_cp[slot] guards a device-mode copy of that slot
+  // kc_append_kv_device enqueues on the caller's stream: ev_append marks the
+  // last such append; the cache's own streams wait on it before reading K/V
+  cudaEvent_t ev_append = nullptr;
+  bool append_pending = false;
+  void order_after_appends(cudaStream_t st) {
+    if (!append_pending) return;
+    CK(cudaStreamWaitEvent(st, ev_append, 0));
+  }
 
   // tuning
   int score_chunk = 0;
   int pipeline = 1;
   int recall_mode = kRecallAuto;
-  int discard = 1;
   int select_global = 0;
   int score_stages = 4;
   // persistent scoring grid (ctas_per_sm x SMs); 0 = one CTA per work item,
@@ -449,6 +455,7 @@ void destroy(kc_cache* c) {
   if (c->ev_start) cudaEventDestroy(c->ev_start);
   if (c->ev_end) cudaEventDestroy(c->ev_end);
   if (c->ev_stats) cudaEventDestroy(c->ev_stats);
+  if (c->ev_append) cudaEventDestroy(c->ev_append);
   if (c->step_exec) cudaGraphExecDestroy(c->step_exec);
   release_green(c);
   if (c->ev_gfork) cudaEventDestroy(c->ev_gfork);
@@ -530,40 +537,6 @@ StepGeom geom(kc_cache* c, uint64_t top_n, int chunk_g = -1) {
   return g;
 }
 
-// Write back every dirty L2 line (a read sweep of 2.5x L2) so that all stored
-// K becomes clean and the scoring kernel may drop its lines after use. Done
-// at the first decode after appends, then whenever the not-yet-clean tail of
-// a layer exceeds ~8 MB; positions appended since stay un-dropped.
-// per-device scratch of 2.5x L2 for the flush sweep
-std::pair<void*, size_t> l2_scratch(kc_cache* c, cudaStream_t st) {
-  static std::mutex mu;
-  static std::vector<std::pair<void*, size_t>> bufs(64, {nullptr, 0});
-  std::lock_guard<std::mutex> lk(mu);
-  auto& buf = bufs[c->device & 63];
-  if (!buf.first) {
-    int l2 = 0;
-    CK(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, c->device));
-    buf.second = ((size_t)l2 * 5 / 2 + 4095) & ~size_t(4095);
-    CK(cudaMalloc(&buf.first, buf.second));
-    CK(cudaMemsetAsync(buf.first, 0, buf.second, st));
-  }
-  return buf;
-}
-
-void maybe_flush_l2(kc_cache* c, const uint64_t* layers, uint64_t n, cudaStream_t st) {
-  const uint64_t pos_bytes = c->rows * c->h * c->esz;
-  const uint64_t slack = (8ull << 20) / std::max<uint64_t>(pos_bytes, 1);
-  bool need = false;
-  for (uint64_t i = 0; i < n; ++i) {
-    const LayerState& ls = c->layers[layers[i]];
-    if (ls.len > ls.clean_len && (ls.clean_len == 0 || ls.len - ls.clean_len > slack)) need = true;
-  }
-  if (!need) return;
-  const auto buf = l2_scratch(c, st);
-  kc::l2_flush_launch(buf.first, buf.second, st);
-  for (auto& ls : c->layers) ls.clean_len = ls.len;
-}
-
 void enqueue_score(kc_cache* c, uint64_t layer, const float* q32, const StepGeom& g, cudaStream_t st,
                    int row0, int nrows, bool cand = false, int lb = 0, int slot = -1, bool pdl = false) {
   kc::ScoreParams sp{};
@@ -598,8 +571,6 @@ void enqueue_score(kc_cache* c, uint64_t layer, const float* q32, const StepGeom
   sp.n_splits = g.n_splits;
   sp.max_splits = c->max_splits;
   sp.scale = 1.0f / std::sqrt(static_cast<float>(c->h));  // attention.hpp:15-17
-  sp.discard_len = (int)std::min<uint64_t>(c->layers[layer].clean_len, (uint64_t)g.s);
-  if (!c->discard) sp.discard_len = 0;
   sp.stages = c->score_stages;
   sp.ctas_per_sm = c->score_ctas_per_sm;
   sp.k_policy = c->k_policy;
@@ -758,6 +729,7 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
   set_dev(c);
   const bool io_device = flags & KC_IO_DEVICE;
   cudaStream_t st = io_device ? user_st : c->main_st;
+  if (!io_device) c->order_after_appends(st);
   const StepGeom g = geom(c, top_n);
   const uint64_t nc = (uint64_t)g.nc;
   const uint64_t slots = c->batch * c->n_q;
@@ -783,7 +755,6 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
   };
 
   if (!io_device && c->capture_st) fail(KC_ESTATE, "host-memory I/O inside a step graph capture");
-  maybe_flush_l2(c, layers, n, st);
   bool out_used = false;  // c->out_st carries work of this call
   const float* q_all = c->capture_st ? nullptr : stage_q_all(c, n, q, q_dtype, io_device, st);
   // SM partition: fork onto the green-context streams (scoring / selection /
@@ -869,9 +840,10 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
       if (side_select) {
         CK(cudaEventRecord(c->ev_scored[slot], st));
         CK(cudaStreamWaitEvent(selst, c->ev_scored[slot], 0));
-        // the selection overwrites ring slot `slot`: its recall (layer i-3)
-        // and device copies must be done (same stream when selst == side)
-        if (selst != side && gi == 0 && i >= (uint64_t)kRing) {
+        // the selection overwrites ring slot `slot`: its recall (layer i-3),
+        // the device copies and host D2H of its outputs (on out_st) must be
+        // done -- also when selst == side, where only the recall is ordered
+        if (gi == 0 && i >= (uint64_t)kRing) {
           CK(cudaStreamWaitEvent(selst, c->ev_rec[slot], 0));
           if (c->cp_pending[slot]) CK(cudaStreamWaitEvent(selst, c->ev_cp[slot], 0));
         }
@@ -974,7 +946,6 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
       rp.renormalize = (flags & KC_RENORMALIZE) ? 1 : 0;
       rp.reverse = (flags & KC_REVERSE_ACCUM) ? 1 : 0;
       rp.row_offset = dma ? host_rows : r0;
-      rp.discard_len = c->discard && (c->h * c->esz) % 128 == 0 ? (int)std::min<uint64_t>(c->layers[layer].clean_len, (uint64_t)g.s) : 0;
       c->timed(2, side, [&] {
         // zero-copy rows first (they need nothing but the selection), then the
         // host-gathered rows once their DMA has landed
@@ -988,7 +959,6 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
           hp.staged = 1;
           hp.row_offset = 0;
           hp.rows = host_rows;
-          hp.discard_len = 0;
           kc::recall_launch(hp, c->dtype, side);
         }
       });
@@ -1168,6 +1138,7 @@ int kc_cache_create(const kc_config* cfg, uint64_t batch, uint64_t resident_laye
       CK(cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming));
       CK(cudaEventCreateWithFlags(&c->ev_end, cudaEventDisableTiming));
       CK(cudaEventCreateWithFlags(&c->ev_stats, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&c->ev_append, cudaEventDisableTiming));
       for (int i = 0; i < kRing; ++i) {
         CK(cudaEventCreateWithFlags(&c->ev_sel[i], cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&c->ev_scored[i], cudaEventDisableTiming));
@@ -1195,6 +1166,7 @@ int kc_append_kv(kc_cache* c, uint64_t layer, const float* k, const float* v, ui
     const size_t bytes = rows * c->dkv * sizeof(float);
     c->stage_k.ensure(bytes);
     c->stage_v.ensure(bytes);
+    c->order_after_appends(c->main_st);
     CK(cudaMemcpyAsync(c->stage_k.p, k, bytes, cudaMemcpyHostToDevice, c->main_st));
     CK(cudaMemcpyAsync(c->stage_v.p, v, bytes, cudaMemcpyHostToDevice, c->main_st));
     enqueue_append(c, layer, c->stage_k.p, c->stage_v.p, KC_F32, rows, c->main_st);
@@ -1210,6 +1182,10 @@ int kc_append_kv_device(kc_cache* c, uint64_t layer, const void* k, const void* 
     append_checks(c, layer, rows);
     set_dev(c);
     enqueue_append(c, layer, k, v, dtype, rows, (cudaStream_t)stream);
+    // the cache's own streams (host-mode calls, k_row/v_row, gather_v) must
+    // not read these rows before the caller's stream has written them
+    CK(cudaEventRecord(c->ev_append, (cudaStream_t)stream));
+    c->append_pending = true;
     append_account(c, layer, rows);
   });
 }
@@ -1257,6 +1233,7 @@ int kc_decode_step(kc_cache* c, uint64_t layer, const void* q, const void* k_new
     if (!io_device && c->capture_st) fail(KC_ESTATE, "host-memory I/O inside a step graph capture");
     set_dev(c);
     cudaStream_t st = io_device ? (cudaStream_t)stream : c->main_st;
+    if (!io_device) c->order_after_appends(st);
     // engine.cpp:143 -- this step's K/V row of every batch row
     const uint64_t rows = c->batch;
     append_checks(c, layer, rows);
@@ -1339,7 +1316,6 @@ void prepare_step_buffers(kc_cache* c, uint64_t top_n, cudaStream_t st) {
     c->part_out.ensure(checked_mul({slots, (uint64_t)c->max_splits, c->h, 4}));
     c->part_ml.ensure(checked_mul({slots, (uint64_t)c->max_splits, 8}));
   }
-  l2_scratch(c, st);
 }
 
 int kc_step_graph_begin(kc_cache* c, uint64_t top_n, void* stream) {
@@ -1427,8 +1403,8 @@ int kc_decode_full(kc_cache* c, uint64_t layer, const void* q, int q_dtype, uint
     const bool io_device = flags & KC_IO_DEVICE;
     cudaStream_t st = io_device ? (cudaStream_t)stream : c->main_st;
     if (!io_device && c->capture_st) fail(KC_ESTATE, "host-memory I/O inside a step graph capture");
+    if (!io_device) c->order_after_appends(st);
     const StepGeom g = geom(c, 1, 1);  // fused full kernel: MHA split sizing
-    maybe_flush_l2(c, &layer, 1, st);
     const float* q32 = stage_q(c, 0, q, q_dtype, io_device, st);
     const uint64_t slots = c->batch * c->n_q;
     if (!io_device) c->out_tmp[0].ensure(slots * c->h * 4);
@@ -1454,7 +1430,6 @@ int kc_decode_full(kc_cache* c, uint64_t layer, const void* q, int q_dtype, uint
       fp.n_splits = g.n_splits;
       fp.max_splits = c->max_splits;
       fp.scale = 1.0f / std::sqrt(static_cast<float>(c->h));  // attention.hpp:15-17
-      fp.discard_len = c->discard ? (int)std::min<uint64_t>(c->layers[layer].clean_len, (uint64_t)g.s) : 0;
       c->timed(0, st, [&] { fused = kc::full_fast_launch(fp, c->dtype, st); });
     }
     if (fused) {
@@ -1499,8 +1474,8 @@ int kc_score_probs(kc_cache* c, uint64_t layer, const void* q, int q_dtype, floa
     decode_checks(c, layer);
     set_dev(c);
     cudaStream_t st = c->main_st;
+    c->order_after_appends(st);
     const StepGeom g = geom(c, 1);
-    maybe_flush_l2(c, &layer, 1, st);
     const float* q32 = stage_q(c, 0, q, q_dtype, false, st);
     enqueue_score(c, layer, q32, g, st, 0, (int)c->rows);
     const uint64_t slots = c->batch * c->n_q;
@@ -1547,6 +1522,7 @@ int kc_gather_v(kc_cache* c, uint64_t layer, const uint32_t* indices, const uint
       c->sel_rows.ensure(total * 4);
       c->sel_pos.ensure(total * 4);
       c->gather_out.ensure(total * c->h * 4);
+      c->order_after_appends(c->main_st);
       CK(cudaMemcpyAsync(c->sel_rows.p, rows.data(), total * 4, cudaMemcpyHostToDevice, c->main_st));
       CK(cudaMemcpyAsync(c->sel_pos.p, pos.data(), total * 4, cudaMemcpyHostToDevice, c->main_st));
       kc::gather_rows_launch(c->v_layer(layer), c->dtype, c->sel_rows.as<uint32_t>(),
@@ -1577,6 +1553,7 @@ int kc_read_row(kc_cache* c, uint64_t layer, uint64_t pos, uint64_t bi, int whic
     c->sel_rows.ensure(c->n_kv * 4);
     c->sel_pos.ensure(c->n_kv * 4);
     c->gather_out.ensure(c->dkv * 4);
+    c->order_after_appends(c->main_st);
     CK(cudaMemcpyAsync(c->sel_rows.p, rows.data(), c->n_kv * 4, cudaMemcpyHostToDevice, c->main_st));
     CK(cudaMemcpyAsync(c->sel_pos.p, ps.data(), c->n_kv * 4, cudaMemcpyHostToDevice, c->main_st));
     kc::gather_rows_launch(which ? c->v_layer(layer) : c->k_layer(layer), c->dtype,
@@ -1639,8 +1616,10 @@ int kc_v_arena_kind(const kc_cache* c, int* kind) {
 int kc_sync(kc_cache* c) {
   return guarded([&] {
     set_dev(c);
-    CK(cudaStreamSynchronize(c->main_st));
-    CK(cudaStreamSynchronize(c->side_st));
+    for (cudaStream_t s : {c->main_st, c->side_st, c->gather_st, c->out_st, c->in_st, c->gst_score, c->gst_sel,
+                           c->gst_rec})
+      if (s) CK(cudaStreamSynchronize(s));
+    if (c->append_pending) CK(cudaEventSynchronize(c->ev_append));
   });
 }
 int kc_set_tuning(kc_cache* c, const char* key, int64_t value) {
@@ -1648,7 +1627,6 @@ int kc_set_tuning(kc_cache* c, const char* key, int64_t value) {
     const std::string k = key ? key : "";
     if (k == "score_chunk") c->score_chunk = (int)value;
     else if (k == "pipeline") c->pipeline = value ? 1 : 0;
-    else if (k == "discard") c->discard = value ? 1 : 0;
     else if (k == "select_global") c->select_global = value ? 1 : 0;
     else if (k == "score_stages") c->score_stages = (int)value;
     else if (k == "score_ctas_per_sm") c->score_ctas_per_sm = (int)value;
@@ -1762,6 +1740,56 @@ int kc_profile_launch(kc_cache* c, const char* kernel, uint64_t i, double* ms) {
     float t = 0.0f;
     CK(cudaEventElapsedTime(&t, c->prof[kind][i].first, c->prof[kind][i].second));
     *ms = t;
+  });
+}
+
+int kc_score_chunk_plan(uint64_t s, uint64_t rows, uint64_t group, int64_t* chunk) {
+  return guarded([&] {
+    if (!chunk || s == 0 || rows == 0 || group == 0) fail(KC_EARG, "kc_score_chunk_plan: bad argument");
+    *chunk = kc::score_pick_chunk((int)s, (int)rows, 0, (int)group);
+  });
+}
+
+int kc_prefill_attention(const float* q, const float* k, const float* v, uint64_t s, uint64_t n_heads,
+                         uint64_t head_dim, float* out, int device) {
+  return guarded([&] {
+    if (!q || !k || !v || !out) fail(KC_EARG, "kc_prefill_attention: null argument");
+    if (n_heads == 0 || head_dim == 0) fail(KC_ESHAPE, "prefill_attention: cols must divide into heads");
+    if (s == 0) return;
+    if (s > (1ull << 30) || n_heads * head_dim > (1ull << 20)) fail(KC_ESHAPE, "prefill_attention: too large");
+    if (device >= 0) CK(cudaSetDevice(device));  // < 0: the calling thread's current device
+    const size_t bytes = checked_mul({s, n_heads, head_dim, 4});
+    float* buf = nullptr;
+    CK(cudaMalloc(&buf, 4 * bytes));
+    cudaStream_t st = nullptr;
+    cudaError_t e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(buf, q, bytes, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync((char*)buf + bytes, k, bytes, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync((char*)buf + 2 * bytes, v, bytes, cudaMemcpyHostToDevice, st);
+    float* dout = (float*)((char*)buf + 3 * bytes);
+    if (e == cudaSuccess &&
+        !kc::prefill_attention_launch(buf, (float*)((char*)buf + bytes), (float*)((char*)buf + 2 * bytes), dout,
+                                      (int)s, (int)n_heads, (int)head_dim, st))
+      e = cudaErrorInvalidValue;
+    if (e == cudaSuccess) e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaMemcpyAsync(out, dout, bytes, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (st) cudaStreamDestroy(st);
+    cudaFree(buf);
+    if (e != cudaSuccess) fail(KC_ECUDA, std::string("prefill_attention: ") + cudaGetErrorString(e));
+  });
+}
+
+int kc_prefill_attention_device(const float* q, const float* k, const float* v, uint64_t s, uint64_t n_heads,
+                                uint64_t head_dim, float* out, void* stream) {
+  return guarded([&] {
+    if (!q || !k || !v || !out) fail(KC_EARG, "kc_prefill_attention_device: null argument");
+    if (n_heads == 0 || head_dim == 0) fail(KC_ESHAPE, "prefill_attention: cols must divide into heads");
+    if (s == 0) return;
+    if (s > (1ull << 30) || n_heads * head_dim > (1ull << 20)) fail(KC_ESHAPE, "prefill_attention: too large");
+    if (!kc::prefill_attention_launch(q, k, v, out, (int)s, (int)n_heads, (int)head_dim, (cudaStream_t)stream))
+      fail(KC_ESHAPE, "prefill_attention: head_dim too large for the shared-memory tiles");
+    CK(cudaGetLastError());
   });
 }
 

@@ -182,11 +182,23 @@ __device__ __forceinline__ void tma_bulk_g2s(void* dst_smem, const void* src_gme
       : "memory");
 }
 
-// Invalidate one 128-B L2 line without write-back. Only for lines known to be
-// clean (their DRAM copy current): the store never issues it for K positions
-// appended since its last L2 flush.
+// Invalidate one 128-B L2 line without write-back (PTX: a weak write of an
+// indeterminate value). Used only on dead scratch -- logits whose row has been
+// selected and that are overwritten before they are read again -- never on
+// K/V cache data.
 __device__ __forceinline__ void discard_l2_line(const void* p) {
   asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
+}
+
+// 16-B read-only load that marks its L2 line evict-first (V rows read once per
+// decode step: the recall's lines should be the first to leave L2, without
+// dropping anything).
+__device__ __forceinline__ uint4 ld_stream16(const void* p, uint64_t pol) {
+  uint4 r;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+      : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+      : "l"(p), "l"(pol));
+  return r;
 }
 
 __device__ __forceinline__ uint32_t lanemask_lt() {

@@ -28,7 +28,6 @@ struct ScoreParams {
   int n_splits;
   int max_splits;
   float scale;          // 1/sqrt(h) as the reference computes it
-  int discard_len;      // K positions < discard_len are clean: drop their L2 lines after use
   int stages;           // TMA ring depth (4, 6 or 8 stages of 64 positions)
   int ctas_per_sm;      // persistent grid = ctas_per_sm x SMs (0: one CTA per item)
   int row0;             // first row of this launch (row groups); rows = rows in this launch
@@ -56,7 +55,6 @@ struct ScoreParams {
 };
 // Read `bytes` of a scratch buffer larger than L2: evicts (and so writes back)
 // every dirty L2 line, after which all stored K is clean in DRAM.
-void l2_flush_launch(const void* scratch, size_t bytes, cudaStream_t st);
 // dtype: KC_F32 / KC_F16 / KC_BF16 (storage)
 void score_launch(const ScoreParams& p, int dtype, cudaStream_t st);
 // positions per CTA for a given shape (tuning override when > 0)
@@ -136,7 +134,6 @@ struct RecallParams {
   int row_offset;         // first row of this launch (pipelined chunks)
   int staged;             // v is the compacted [rows][nc][h] block (DMA recall)
   int grid;               // CTAs (0: one per row); CTAs loop over rows
-  int discard_len;        // positions < discard_len are clean: drop their lines from L2 after use
   int pipelined;          // use recall_pv_pipe_kernel where the shape allows
 };
 void recall_launch(const RecallParams& p, int dtype, cudaStream_t st);
@@ -189,9 +186,13 @@ struct FullParams {
   int n_splits;
   int max_splits;
   float scale;
-  int discard_len;        // positions < discard_len are clean in DRAM (K and V)
 };
 bool full_fast_launch(const FullParams& p, int dtype, cudaStream_t st);
+
+// ---- prefill attention (kc_prefill.cu) ----
+// q, k, v, out: device fp32 [s][n_heads*h]; false if h is too large
+bool prefill_attention_launch(const float* q, const float* k, const float* v, float* out, int s, int n_heads,
+                              int h, cudaStream_t st);
 
 // Position-major [rows][n_kv*h] input rows -> [b][n_kv][max_seq][h] storage
 // at positions [pos0, pos0 + rows/batch).

@@ -59,6 +59,7 @@ __global__ void __launch_bounds__(kRecallThreads) recall_pv_kernel(const RecallP
       const int vpr = (int)(rowb >> 4);
       const int total = rc * vpr;
       uint4* dst = reinterpret_cast<uint4*>(vbuf);
+      const uint64_t pol = l2_evict_first_policy();
       constexpr int kBatch = 8;
       for (int v0 = tid; v0 < total; v0 += kRecallThreads * kBatch) {
         uint4 tmp[kBatch];
@@ -68,22 +69,13 @@ __global__ void __launch_bounds__(kRecallThreads) recall_pv_kernel(const RecallP
           if (v < total) {
             const int r = v / vpr, part = v - r * vpr;
             const size_t pos = p.staged ? (size_t)(c0 + r) : (size_t)idx[c0 + r];
-            tmp[u] = *(reinterpret_cast<const uint4*>(vslot + pos * h) + part);
+            tmp[u] = ld_stream16(reinterpret_cast<const uint4*>(vslot + pos * h) + part, pol);
           }
         }
 #pragma unroll
         for (int u = 0; u < kBatch; ++u) {
           const int v = v0 + u * kRecallThreads;
-          if (v < total) {
-            dst[v] = tmp[u];
-            // the row's 128-B line has landed: drop it from L2 (sysmem lines
-            // left in L2 slow every later zero-copy gather)
-            const int r = v / vpr, part = v - r * vpr;
-            if (!p.staged && (part & 7) == 0) {
-              const uint32_t pos = idx[c0 + r];
-              if ((int)pos < p.discard_len) discard_l2_line(reinterpret_cast<const uint4*>(vslot + (size_t)pos * h) + part);
-            }
-          }
+          if (v < total) dst[v] = tmp[u];
         }
       }
     } else {
@@ -156,6 +148,7 @@ __global__ void __launch_bounds__(kRecallThreads) recall_pv_pipe_kernel(const Re
     return reinterpret_cast<const uint4*>(static_cast<const T*>(p.v) +
                                           (size_t)row * (p.staged ? (size_t)nc : (size_t)p.max_seq) * kH);
   };
+  const uint64_t pol = l2_evict_first_policy();
   auto issue = [&](int row) {
     const uint4* vs = vslot_of(row);
     const uint32_t* idx = p.idx + (size_t)row * nc;
@@ -165,7 +158,7 @@ __global__ void __launch_bounds__(kRecallThreads) recall_pv_pipe_kernel(const Re
       if (v < total) {
         const int r = v >> 4, part = v & 15;
         const size_t pos = p.staged ? (size_t)r : (size_t)idx[r];
-        tmp[u] = vs[pos * kVpr + part];
+        tmp[u] = ld_stream16(vs + pos * kVpr + part, pol);
       }
     }
   };
@@ -175,23 +168,14 @@ __global__ void __launch_bounds__(kRecallThreads) recall_pv_pipe_kernel(const Re
   while (row < end) {
     const int b = row / p.n_kv;
     const int kvh = row - b * p.n_kv;
-    // land: the rows this thread loaded -> shared memory, then drop their
-    // (clean) L2 lines; the weights of the row's q heads
+    // land: the rows this thread loaded -> shared memory; the weights of the
+    // row's q heads
     {
-      const uint4* vs = vslot_of(row);
-      const uint32_t* idx = p.idx + (size_t)row * nc;
       uint4* dst = vb + buf * kPipeMaxNc * kVpr;
 #pragma unroll
       for (int u = 0; u < kLoads; ++u) {
         const int v = tid + u * kRecallThreads;
-        if (v < total) {
-          dst[v] = tmp[u];
-          const int r = v >> 4, part = v & 15;
-          if (!p.staged && (part & 7) == 0) {
-            const uint32_t pos = idx[r];
-            if ((int)pos < p.discard_len) discard_l2_line(vs + (size_t)pos * kVpr + part);
-          }
-        }
+        if (v < total) dst[v] = tmp[u];
       }
       float* wd = wb + buf * kMaxGroup * kPipeMaxNc;
       for (int e = tid; e < G * nc; e += kRecallThreads) {

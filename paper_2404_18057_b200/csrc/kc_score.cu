@@ -62,32 +62,16 @@ __device__ __forceinline__ int chunk_of(int ci, int rl, int sub) {
 // Producer warp: lane 0 streams the items' K runs (one contiguous run of
 // chunk*h elements per (row, split) in the [b][kv][pos][h] arena) into a
 // STAGES-deep ring of 64-position stages with 1-D TMA bulk copies
-// (cp.async.bulk, L2 evict-first) on mbarriers. As soon as a stage has landed
-// in shared memory the warp drops its K lines from L2 (discard.global.L2,
-// positions < discard_len, which the store keeps clean): a decode step streams
-// the whole K cache once, and L2 lines held by dead K are useless to the
-// concurrent V recall.
+// (cp.async.bulk) on mbarriers, under an L2 evict-first policy: a decode step
+// streams the whole K cache exactly once, so its lines should be the first
+// to leave L2 (they are never dropped without write-back -- the cache data
+// stays defined whatever the L2 state).
 template <typename T, int STAGES>
 __device__ __forceinline__ void produce_k(const ScoreParams& p, uint8_t* ring, uint64_t* full, uint64_t* empty,
                                           int lane, int n_items) {
   constexpr int ROWB = kH * (int)sizeof(T);
   const uint64_t pol = l2_policy(p.k_policy);
-  const char* held[STAGES];  // what each ring slot holds: start + line count
-  int held_lines[STAGES];
-#pragma unroll
-  for (int st = 0; st < STAGES; ++st) held_lines[st] = 0;
-  auto drop = [&](int st) {
-    const char* base = held[st];
-    for (int l = lane; l < held_lines[st]; l += 32) discard_l2_line(base + (size_t)l * 128);
-  };
   uint32_t g = 0;  // global stage counter across items
-  // drop stage j's lines as soon as its bytes have landed (lag STAGES-1
-  // behind the issue point so the ring stays full)
-  auto land_and_drop = [&](uint32_t j) {
-    const int sj = (int)(j % STAGES);
-    mbar_wait(&full[sj], (j / STAGES) & 1);
-    drop(sj);
-  };
   for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
     const int row = p.row0 + item / p.n_splits;
     const int split = item - (row - p.row0) * p.n_splits;
@@ -107,24 +91,18 @@ __device__ __forceinline__ void produce_k(const ScoreParams& p, uint8_t* ring, u
         asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
       }
     }
-    for (int it = 0; it < n_it; ++it, ++g) {
-      const int st = (int)(g % STAGES);
-      if (g >= (uint32_t)STAGES) mbar_wait(&empty[st], ((g / STAGES) - 1) & 1);
-      const int pstart = pos0 + it * kRows;
-      const int rows = min(kRows, npos - it * kRows);
-      held[st] = reinterpret_cast<const char*>(kslot + (size_t)pstart * kH);
-      held_lines[st] = max(0, min(pstart + rows, p.discard_len) - pstart) * (ROWB / 128);
-      if (lane == 0) {
+    if (lane == 0) {
+      for (int it = 0; it < n_it; ++it, ++g) {
+        const int st = (int)(g % STAGES);
+        if (g >= (uint32_t)STAGES) mbar_wait(&empty[st], ((g / STAGES) - 1) & 1);
+        const int pstart = pos0 + it * kRows;
+        const int rows = min(kRows, npos - it * kRows);
         const uint32_t bytes = (uint32_t)(rows * ROWB);
         mbar_arrive_expect_tx(&full[st], bytes);
         tma_bulk_g2s(ring + st * kRows * ROWB, kslot + (size_t)pstart * kH, bytes, &full[st], pol);
       }
-      __syncwarp();
-      if (g >= (uint32_t)(STAGES - 1)) land_and_drop(g - (STAGES - 1));
     }
   }
-  // drain: the last STAGES-1 stages
-  for (uint32_t j = g > (uint32_t)(STAGES - 1) ? g - (STAGES - 1) : 0; j < g; ++j) land_and_drop(j);
 }
 
 // Candidate epilogue of one split (MHA): scb[0..npos) holds the split's
@@ -714,35 +692,21 @@ __global__ void __launch_bounds__((kCWarps + 1) * 32)
   __syncthreads();
 
   if (warp == kCWarps) {
-    const uint64_t pol = l2_evict_first_policy();
-    const char* held[STAGES];
-    int held_lines[STAGES];
-#pragma unroll
-    for (int st = 0; st < STAGES; ++st) held_lines[st] = 0;
-    auto land_and_drop = [&](uint32_t j) {
-      const int sj = (int)(j % STAGES);
-      mbar_wait(&full[sj], (j / STAGES) & 1);
-      for (int l = lane; l < held_lines[sj]; l += 32) discard_l2_line(held[sj] + (size_t)l * 128);
-    };
-    const uint32_t total = 2u * (uint32_t)n_it;
-    for (uint32_t g = 0; g < total; ++g) {
-      const int st = (int)(g % STAGES);
-      if (g >= (uint32_t)STAGES) mbar_wait(&empty[st], ((g / STAGES) - 1) & 1);
-      const int it = (int)(g % (uint32_t)n_it);
-      const T* base = static_cast<const T*>(g < (uint32_t)n_it ? p.k : p.v) + slot_off;
-      const int pstart = pos0 + it * kRows;
-      const int rows = min(kRows, npos - it * kRows);
-      held[st] = reinterpret_cast<const char*>(base + (size_t)pstart * kH);
-      held_lines[st] = max(0, min(pstart + rows, p.discard_len) - pstart) * (ROWB / 128);
-      if (lane == 0) {
+    if (lane == 0) {
+      const uint64_t pol = l2_evict_first_policy();
+      const uint32_t total = 2u * (uint32_t)n_it;
+      for (uint32_t g = 0; g < total; ++g) {
+        const int st = (int)(g % STAGES);
+        if (g >= (uint32_t)STAGES) mbar_wait(&empty[st], ((g / STAGES) - 1) & 1);
+        const int it = (int)(g % (uint32_t)n_it);
+        const T* base = static_cast<const T*>(g < (uint32_t)n_it ? p.k : p.v) + slot_off;
+        const int pstart = pos0 + it * kRows;
+        const int rows = min(kRows, npos - it * kRows);
         const uint32_t bytes = (uint32_t)(rows * ROWB);
         mbar_arrive_expect_tx(&full[st], bytes);
         tma_bulk_g2s(ring + st * kRows * ROWB, base + (size_t)pstart * kH, bytes, &full[st], pol);
       }
-      __syncwarp();
-      if (g >= (uint32_t)(STAGES - 1)) land_and_drop(g - (STAGES - 1));
     }
-    for (uint32_t j = total > (uint32_t)(STAGES - 1) ? total - (STAGES - 1) : 0; j < total; ++j) land_and_drop(j);
     return;
   }
 
@@ -1040,19 +1004,7 @@ bool try_fast(const ScoreParams& p, cudaStream_t st) {
   }
 }
 
-__global__ void l2_flush_kernel(const uint4* p, size_t n16, uint32_t* sink) {
-  uint32_t acc = 0;
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n16; i += (size_t)gridDim.x * blockDim.x)
-    acc ^= p[i].x;
-  if (acc == 0x9e3779b9u) sink[0] = acc;  // keeps the loads alive
-}
-
 }  // namespace
-
-void l2_flush_launch(const void* scratch, size_t bytes, cudaStream_t st) {
-  l2_flush_kernel<<<148 * 8, 256, 0, st>>>(static_cast<const uint4*>(scratch), bytes / 16,
-                                          (uint32_t*)scratch + (bytes / 4 - 1));
-}
 
 int score_pick_chunk(int s, int rows, int override_chunk, int G) {
   if (override_chunk > 0) return ((override_chunk + kRows - 1) / kRows) * kRows;

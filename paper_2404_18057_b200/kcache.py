@@ -115,6 +115,9 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         "kc_profile_launch": (i32, [vp, C.c_char_p, u64, C.POINTER(C.c_double)]),
         "kc_profile_span": (i32, [vp, C.c_char_p, u64, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
         "kc_arg_topk": (i32, [vp, u64, u64, vp, p64]),
+        "kc_score_chunk_plan": (i32, [u64, u64, u64, C.POINTER(C.c_int64)]),
+        "kc_prefill_attention": (i32, [vp, vp, vp, u64, u64, u64, vp, i32]),
+        "kc_prefill_attention_device": (i32, [vp, vp, vp, u64, u64, u64, vp, vp]),
         "kc_fill_uniform": (i32, [vp, i32, u64, u64, u64, C.c_float, C.c_float, vp]),
     }
     for name, (res, args) in sig.items():
@@ -208,14 +211,14 @@ class TierPlacement:
     resident_layers: int = 0
     n_layers: int = 0
     bytes_per_element: int = 2
-    storage: str = "f16"
+    storage: str = "f32"
 
     @staticmethod
-    def baseline(n_layers: int, bytes_per_element: int = 2, storage: str = "f16") -> "TierPlacement":
+    def baseline(n_layers: int, bytes_per_element: int = 2, storage: str = "f32") -> "TierPlacement":
         return TierPlacement(n_layers, n_layers, bytes_per_element, storage)
 
     @staticmethod
-    def kcache(resident_layers: int, n_layers: int, bytes_per_element: int = 2, storage: str = "f16") -> "TierPlacement":
+    def kcache(resident_layers: int, n_layers: int, bytes_per_element: int = 2, storage: str = "f32") -> "TierPlacement":
         return TierPlacement(resident_layers, n_layers, bytes_per_element, storage)
 
     def validate(self) -> None:
@@ -642,6 +645,30 @@ def _observe(q, cache, layer, observer) -> None:
     n = cache.config.n_heads
     for slot in range(probs.shape[0]):
         observer(slot // n, slot % n, probs[slot])
+
+
+def score_chunk_plan(s: int, rows: int, group: int) -> int:
+    """The split length the store picks for s positions over `rows` (batch x
+    kv head) rows of GQA group `group` (set it as "score_chunk" on a shard to
+    reproduce the unsharded cache bit for bit)."""
+    c = C.c_int64(0)
+    _check(load().kc_score_chunk_plan(s, rows, group, C.byref(c)))
+    return c.value
+
+
+def prefill_attention(q, k, v, n_heads: int, device: int = -1) -> np.ndarray:
+    """prefill_attention (attention.hpp:40, attention.cpp:31-62): causal
+    attention of one sequence on the GPU; q, k, v: s x d fp32."""
+    q, k, v = _f32(q), _f32(k), _f32(v)
+    if q.shape != k.shape or q.shape != v.shape:
+        raise ShapeError("prefill_attention: Q/K/V shapes differ")
+    if n_heads == 0 or q.shape[1] % n_heads != 0:
+        raise ShapeError("prefill_attention: cols must divide into heads")
+    out = np.zeros_like(q)
+    if q.shape[0]:
+        _check(load().kc_prefill_attention(_ptr(q), _ptr(k), _ptr(v), q.shape[0], n_heads, q.shape[1] // n_heads,
+                                           _ptr(out), device))
+    return out
 
 
 # ---------------------------------------------------------------------------

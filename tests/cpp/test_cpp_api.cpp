@@ -2,7 +2,7 @@
 // reference's own tests and Engine use it, compiled against include/kcache/
 // and linked to libkcache_b200.so. Proves source compatibility of the
 // drop-in: this file would compile against the
-// reference headers too (plus the B200-only TierPlacement::storage field).
+// reference headers too (except engine_step_cases: kcache/b200.hpp).
 // Cases restate proj/tests/test_attention.cpp and test_kv_cache.cpp.
 #include <cmath>
 #include <cstdio>
@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "kcache/attention.hpp"
+#include "kcache/b200.hpp"
 #include "kcache/errors.hpp"
 #include "kcache/kv_cache.hpp"
 #include "kcache/matrix.hpp"
@@ -66,7 +67,6 @@ static Matrix random_matrix(std::size_t rows, std::size_t cols, SeededRng& rng, 
 static TieredKVCache make_cache(const ModelConfig& c, std::size_t batch, std::size_t resident,
                                 const Matrix& k, const Matrix& v) {
   TierPlacement pl = TierPlacement::kcache(resident, c.n_layers);
-  pl.storage = StorageType::f32;  // keep the reference's fp32 data unrounded
   TieredKVCache cache(c, batch, pl);
   for (std::size_t layer = 0; layer < c.n_layers; ++layer) {
     cache.append_kv(layer, k, v);
@@ -165,9 +165,8 @@ static void kv_cache_cases() {
 
   // gather rows are returned bitwise (fp32 storage)
   const ModelConfig c3 = small_config(1, 64, 4);
-  TierPlacement pl = TierPlacement::kcache(0, c3.n_layers);
-  pl.storage = StorageType::f32;
-  TieredKVCache g(c3, 2, pl);
+  // (fp32 is the default storage: TierPlacement as the reference builds it)
+  TieredKVCache g(c3, 2, TierPlacement::kcache(0, c3.n_layers));
   const Matrix k = random_matrix(40, 64, rng);
   const Matrix v = random_matrix(40, 64, rng);
   g.append_kv(0, k, v);
@@ -206,13 +205,13 @@ static void engine_step_cases() {
   const Matrix v = random_matrix(s * batch, c.d_model, rng);
   TieredKVCache a = make_cache(c, batch, 1, k, v);
   TieredKVCache b = make_cache(c, batch, 1, k, v);
-  read_step_stats(a);
+  b200::read_step_stats(a);
   for (std::size_t layer = 0; layer < c.n_layers; ++layer) {
     const Matrix kr = random_matrix(batch, c.d_model, rng);
     const Matrix vr = random_matrix(batch, c.d_model, rng);
     const Matrix q = random_matrix(batch, c.d_model, rng);
     const bool topn = layer >= 1;
-    const Matrix got = decode_step_attention(q, kr, vr, a, layer, topn, N, false);
+    const Matrix got = b200::decode_step_attention(q, kr, vr, a, layer, topn, N, false);
     b.append_kv(layer, kr, vr);
     if (topn) {
       const TopNResult want = decode_attention_topn(q, b, layer, N, false);
@@ -221,7 +220,7 @@ static void engine_step_cases() {
       CHECK(got.data == decode_attention_full(q, b, layer).data);
     }
   }
-  const StepStats st = read_step_stats(a);
+  const b200::DeviceStepStats st = b200::read_step_stats(a);
   CHECK(st.h2d_bytes == 2ull * batch * c.n_heads * N * c.head_dim);
   CHECK(st.d2h_bytes == 2ull * batch * c.d_model);  // layer 1's new V row goes to the slow tier
   std::uint64_t total = 0;
@@ -229,8 +228,8 @@ static void engine_step_cases() {
   CHECK(total == batch * c.n_heads * N);
   CHECK(st.mean_dropped_mass > 0.0 && st.mean_dropped_mass < 1.0);
   CHECK(a.current_len() == s + 1);
-  CHECK_THROWS_AS(decode_step_attention(random_matrix(batch, c.d_model, rng), random_matrix(batch, 16, rng),
-                                        random_matrix(batch, c.d_model, rng), a, 0, true, N, false),
+  CHECK_THROWS_AS(b200::decode_step_attention(random_matrix(batch, c.d_model, rng), random_matrix(batch, 16, rng),
+                                              random_matrix(batch, c.d_model, rng), a, 0, true, N, false),
                   ShapeError);
 }
 

@@ -73,7 +73,7 @@ def test_tie_flood_selects_lowest_positions(kc, oracle):
     the candidate capacity, so this also runs the capacity fallback."""
     b, n, h, s, N = 1, 2, 128, 20000, 64
     cfg = kc.small_config(1, n * h, n, s)
-    cache = kc.TieredKVCache(cfg, b, kc.TierPlacement.kcache(0, 1))
+    cache = kc.TieredKVCache(cfg, b, kc.TierPlacement.kcache(0, 1, 2, "f16"))
     k = np.full((s * b, n * h), 0.25, np.float32)
     v = synth_matrix(3, s * b, n * h)
     cache.append_kv(0, k, v)
@@ -96,7 +96,7 @@ def test_underflow_ties_take_lowest_positions(kc, oracle):
     b, n, h, s, N = 1, 2, 128, 3000, 16
     hot = [2500, 700, 1999]
     cfg = kc.small_config(1, n * h, n, s)
-    cache = kc.TieredKVCache(cfg, b, kc.TierPlacement.kcache(0, 1))
+    cache = kc.TieredKVCache(cfg, b, kc.TierPlacement.kcache(0, 1, 2, "f16"))
     k = np.full((s * b, n * h), -2.0, np.float32)
     for j in hot:
         k[j, :] = 8.0
@@ -130,7 +130,7 @@ def test_pipeline_variants_bitwise(kc, tune, n_kv):
     """Row groups, host-gather DMA recall, the hybrid recall and candidate
     selection reproduce the default path bit for bit; another split length
     changes only the rounding of the softmax statistics."""
-    b, n, h, s, N, L = 2, 8, 128, 3000, 64, 3
+    b, n, h, s, N, L = 2, 8, 128, 3000, 64, 7  # L > kRing (3): ring slots are reused
     if n_kv != n and "select_cand" in tune:
         pytest.skip("candidate selection is MHA-only")
     cache, ks, vs = build_cache(kc, b, n, n_kv, h, s, "f16", n_layers=L)
@@ -154,7 +154,7 @@ def test_pipeline_variants_bitwise(kc, tune, n_kv):
         if "score_chunk" in tune:
             np.testing.assert_array_equal(got[l]["indices"], base[l]["indices"])
             for key in ("out", "weights"):
-                np.testing.assert_allclose(got[l][key], base[l][key], rtol=1e-5, atol=1e-9)
+                np.testing.assert_allclose(got[l][key], base[l][key], rtol=1e-5, atol=5e-9)
             np.testing.assert_allclose(got[l]["dropped"], base[l]["dropped"], atol=1e-6)
             continue
         for key in ("out", "indices", "weights", "dropped"):

@@ -222,7 +222,7 @@ def _full_size(kc, oracle, b, n, n_kv, s, N, samples, seed_q=1, seeds=(2, 3)):
     import torch
     h = 128
     cfg = kc.small_config(1, n * h, n, s, kv_heads=n_kv)
-    cache = kc.TieredKVCache(cfg, b, kc.TierPlacement.kcache(0, 1))
+    cache = kc.TieredKVCache(cfg, b, kc.TierPlacement.kcache(0, 1, 2, "f16"))
     rows = s * b
     k = torch.empty(rows, n_kv * h, dtype=torch.float16, device="cuda")
     kc.fill_uniform(k, seeds[0])

@@ -417,3 +417,43 @@ def test_arg_topk_selection_property_and_reference_equality(kc, oracle):
         assert len(idx) == min(k, n)
         assert np.all(np.diff(idx.astype(np.int64)) > 0)
         np.testing.assert_array_equal(idx, oracle.arg_topk(vals, k))
+
+
+# ---------------- prefill_attention (attention.cpp:31-62) ----------------
+@pytest.mark.parametrize("s,n,h", [(1, 4, 16), (33, 4, 16), (77, 2, 64), (300, 2, 128), (130, 1, 256)])
+def test_prefill_attention_matches_reference(kc, s, n, h):
+    """GPU causal prefill vs the reference's own prefill_attention: same dot,
+    max, ordered exp-sum and ascending P.V order, so outputs agree to float
+    rounding of expf (GPU) vs std::exp (glibc); most elements are bitwise."""
+    from oracle.oracle import Reference
+    d = n * h
+    q = synth_matrix(51, s, d, dtype="f32")
+    k = synth_matrix(52, s, d, dtype="f32")
+    v = synth_matrix(53, s, d, dtype="f32")
+    got = kc.prefill_attention(q, k, v, n)
+    if Reference.available():
+        want = Reference().prefill_attention(q, k, v, n)
+    else:  # restated from attention.cpp:31-62 in float64 (no _ref on this box)
+        want = np.zeros((s, d), np.float64)
+        scale = float(np.float32(1.0) / np.sqrt(np.float32(h)))
+        for hd in range(n):
+            sl = slice(hd * h, (hd + 1) * h)
+            sc = (q[:, sl].astype(np.float64) @ k[:, sl].T.astype(np.float64)) * scale
+            sc[np.triu_indices(s, 1)] = -np.inf
+            p = np.exp(sc - sc.max(axis=1, keepdims=True))
+            p /= p.sum(axis=1, keepdims=True)
+            want[:, sl] = p @ v[:, sl].astype(np.float64)
+    np.testing.assert_allclose(got, want, rtol=2e-5, atol=2e-6)
+    # position 0 attends to itself only: out = v[0] exactly
+    np.testing.assert_array_equal(got[0], v[0])
+
+
+def test_prefill_attention_errors(kc):
+    """attention.cpp:32-37"""
+    q = np.zeros((4, 8), np.float32)
+    with pytest.raises(kc.ShapeError):
+        kc.prefill_attention(q, np.zeros((4, 6), np.float32), q, 2)
+    with pytest.raises(kc.ShapeError):
+        kc.prefill_attention(q, q, q, 3)
+    with pytest.raises(kc.ShapeError):
+        kc.prefill_attention(q, q, q, 0)

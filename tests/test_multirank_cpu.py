@@ -83,6 +83,50 @@ def test_gloo_world2_sharded_step_matches_unsharded():
     assert all(p.exitcode == 0 for p in procs)
 
 
+def _units_worker(rank, world, port, result):
+    """sharding.UnitShard over the CPU oracle: each rank serves a contiguous run
+    of (batch, kv head) units as one flattened batch-1 cache (GQA group 2)."""
+    import torch
+    import torch.distributed as dist
+
+    from oracle.oracle import Restatement, synth_matrix
+    from paper_2404_18057_b200.sharding import UnitShard, gather_units
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    ora = Restatement()
+    B, n, n_kv, h, s, N = 3, 6, 3, 16, 40, 7
+    G = n // n_kv
+    q = synth_matrix(1, B, n * h)
+    k = synth_matrix(2, s * B, n_kv * h)
+    v = synth_matrix(3, s * B, n_kv * h)
+    sh = UnitShard(B, n_kv, G, h, world, rank)
+    out = ora.decode_topn(sh.q_rows(q), sh.kv_rows(k), sh.kv_rows(v), 1, sh.n_units * G, sh.n_units, h, s, N,
+                          False)[0]
+    full = gather_units(torch.from_numpy(out), sh)
+    if rank == 0:
+        ref_out = ora.decode_topn(q, k, v, B, n, n_kv, h, s, N, False)[0]
+        result.put(bool(np.array_equal(full.numpy(), ref_out)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_gloo_world2_unit_shards_match_unsharded():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_units_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    ok = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+    assert ok
+    assert all(p.exitcode == 0 for p in procs)
+
+
 def _max_worker(rank, world, port, out):
     import torch.distributed as dist
 

@@ -24,7 +24,7 @@ from paper_2404_18057_b200 import kcache as kc  # noqa: E402
 def build(L, b, n, h, s, resident):
     d = n * h
     cfg = kc.ModelConfig(L, d, n, h, kc.ModelConfig.default_ffn_hidden(d), 32000, s, n)
-    cache = kc.TieredKVCache(cfg, b, kc.TierPlacement.kcache(L if resident else 0, L))
+    cache = kc.TieredKVCache(cfg, b, kc.TierPlacement.kcache(L if resident else 0, L, 2, "f16"))
     kb = torch.empty(s * b, d, dtype=torch.float16, device="cuda")
     vb = torch.empty_like(kb)
     for layer in range(L):

@@ -39,7 +39,7 @@ def main():
     rows = []
     for s in [int(x) for x in args.contexts.split(",")]:
         cfg = kc.ModelConfig(L, d, n, h, kc.ModelConfig.default_ffn_hidden(d), 32000, s, n)
-        cache = kc.TieredKVCache(cfg, b, kc.TierPlacement.kcache(0, L))
+        cache = kc.TieredKVCache(cfg, b, kc.TierPlacement.kcache(0, L, 2, "f16"))
         kb = torch.empty(s * b, d, dtype=torch.float16, device="cuda")
         vb = torch.empty_like(kb)
         for layer in range(L):

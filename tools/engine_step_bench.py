@@ -40,7 +40,7 @@ def main():
     groups = [int(x) for x in args.groups.split(",")]
     total_steps = (args.steps + 4) * len(groups) * len(args.graph.split(","))
     cfg = kc.ModelConfig(L, d, n, h, kc.ModelConfig.default_ffn_hidden(d), 32000, s + total_steps, n)
-    cache = kc.TieredKVCache(cfg, b, kc.TierPlacement.kcache(0, L))
+    cache = kc.TieredKVCache(cfg, b, kc.TierPlacement.kcache(0, L, 2, "f16"))
     kb = torch.empty(s * b, d, dtype=torch.float16, device="cuda")
     vb = torch.empty_like(kb)
     for layer in range(L):

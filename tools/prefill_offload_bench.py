@@ -44,7 +44,7 @@ def main():
         times = []
         for _ in range(args.reps):
             cfg = kc.ModelConfig(1, d, n, h, kc.ModelConfig.default_ffn_hidden(d), 32000, s, n)
-            cache = kc.TieredKVCache(cfg, b, kc.TierPlacement.kcache(resident, 1))
+            cache = kc.TieredKVCache(cfg, b, kc.TierPlacement.kcache(resident, 1, 2, "f16"))
             torch.cuda.synchronize()
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)

@@ -33,7 +33,7 @@ def main():
     L, b, n, n_kv, h, s, N = args.layers, args.batch, 32, args.kv, 128, args.s, 128
     d = n * h
     cfg = kc.ModelConfig(L, d, n, h, kc.ModelConfig.default_ffn_hidden(d), 32000, s, n_kv)
-    cache = kc.TieredKVCache(cfg, b, kc.TierPlacement.kcache(0, L))
+    cache = kc.TieredKVCache(cfg, b, kc.TierPlacement.kcache(0, L, 2, "f16"))
     kb = torch.empty(s * b, n_kv * h, dtype=torch.float16, device="cuda")
     vb = torch.empty_like(kb)
     for l in range(L):
