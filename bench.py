@@ -217,20 +217,20 @@ class RankWorkload:
     sequences (data seeded per rank); "units": the rank's (batch, kv head)
     units of the global batch (sharding.UnitShard; the global data, sliced)."""
 
-    def __init__(self, kc, torch, cfg, dev, rank, world, shard, resident=False, tune=()):
+    def __init__(self, kc, torch, cfg, dev, rank, world, shard, resident=False, tune=(), extra_seq=0):
         from paper_2404_18057_b200.sharding import UnitShard, gpu_numa_node
         L, B, n, n_kv, h, s = (cfg[k] for k in ("n_layers", "batch", "n_heads", "n_kv", "h", "s"))
         G = n // n_kv
         self.numa = gpu_numa_node(dev.index)
         if shard == "units":
             self.shard = UnitShard(B, n_kv, G, h, world, rank)
-            mcfg = self.shard.model_config(kc, L, s)
+            mcfg = self.shard.model_config(kc, L, s + extra_seq)
             self.b, self.rows = 1, self.shard.n_units
             seed_off = 0
         else:
             self.shard = None
             d = n * h
-            mcfg = kc.ModelConfig(L, d, n, h, kc.ModelConfig.default_ffn_hidden(d), 32000, s, n_kv)
+            mcfg = kc.ModelConfig(L, d, n, h, kc.ModelConfig.default_ffn_hidden(d), 32000, s + extra_seq, n_kv)
             self.b, self.rows = B, B * n_kv
             seed_off = 1_000_003 * rank
         self.d = mcfg.d_model
@@ -266,6 +266,48 @@ class RankWorkload:
     def close(self):
         self.cache.close()
         self.qs = []
+
+
+ENGINE_STEPS = 8
+
+
+def engine_step(kc, torch, wl, cfg, dev, args, barrier):
+    """The engine-realistic decode step (Engine::forward_decode,
+    engine.cpp:124-165): layer l+1's q needs layer l's output, so every layer
+    is its own library call -- kc_decode_step: append this token's K/V row
+    (the new V row to the host arena), score, select, recall + P.V -- with
+    only the intra-layer overlap of row groups (recall of group g under the
+    scoring of group g+1). Run after the headline legs: it grows the cache by
+    warm-up + timed steps positions."""
+    L, N = cfg["n_layers"], cfg["top_n"]
+    cache = wl.cache
+    b, d, kvw = wl.b, wl.d, cache.kv_width
+    q16 = [torch.empty(b, d, dtype=torch.float16, device=dev) for _ in range(L)]
+    kv16 = [torch.empty(2, b, kvw, dtype=torch.float16, device=dev) for _ in range(L)]
+    for layer in range(L):
+        kc.fill_uniform(q16[layer], 900 + layer)
+        kc.fill_uniform(kv16[layer], 950 + layer)
+    out = torch.empty(b, d, dtype=torch.float32, device=dev)
+    stream = torch.cuda.Stream(device=dev)
+
+    def step():
+        for layer in range(L):
+            cache.decode_step_device(layer, q16[layer], kv16[layer][0], kv16[layer][1], out, N, stream=stream)
+
+    for _ in range(2):
+        step()
+    torch.cuda.synchronize()
+    barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(ENGINE_STEPS):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    cache.step_stats(reset=True)
+    return e0.elapsed_time(e1) / ENGINE_STEPS
 
 
 def full_kv_step(kc, torch, cfg, dev, rank, world, shard, args, barrier):
@@ -333,7 +375,8 @@ def run_ours(args, cfg):
                               "MemAvailable %.1f GiB" % (local_world, v_bytes_rank / 2**30, avail / 2**30)}))
         sys.exit(3)
     t0 = time.time()
-    wl = RankWorkload(kc, torch, cfg, dev, rank, world, shard, tune=args.tune)
+    wl = RankWorkload(kc, torch, cfg, dev, rank, world, shard, tune=args.tune,
+                      extra_seq=0 if args.no_engine else ENGINE_STEPS + 2)
     cache, qs, b, d, slots = wl.cache, wl.qs, wl.b, wl.d, wl.slots
     numa = wl.numa
     v_arena = cache.v_arena_kind()
@@ -430,8 +473,12 @@ def run_ours(args, cfg):
         full_out = gather_units(outs[0]["out"], wl.shard)
         gathered = {"shape": list(full_out.shape), "abs_sum": float(full_out.abs().sum())}
 
+    # ---- the engine-realistic step (no cross-layer pipelining), labelled apart ----
+    engine_ms_local = 0.0 if args.no_engine else engine_step(kc, torch, wl, cfg, dev, args, barrier)
+
     from paper_2404_18057_b200.sharding import max_over_ranks
-    ms, e2e_ms, neg_h2d = max_over_ranks([ms_local, e2e_ms_local, -h2d_local], device=dev)
+    ms, e2e_ms, neg_h2d, engine_ms = max_over_ranks([ms_local, e2e_ms_local, -h2d_local, engine_ms_local],
+                                                    device=dev)
     h2d_bw = -neg_h2d
     wl.close()
     del qs, outs, cache
@@ -518,6 +565,15 @@ def run_ours(args, cfg):
     }
     if gathered is not None:
         line["gathered_layer0_out"] = gathered
+    if not args.no_engine:
+        line["engine_ms_per_step"] = engine_ms
+        line["engine"] = {
+            "value": global_batch / (engine_ms * 1e-3), "unit": UNIT, "ms_per_step": engine_ms,
+            "steps": ENGINE_STEPS, "frac_of_max_roofline": max(t_k, t_v) * 1e3 / engine_ms,
+            "note": "engine-realistic decode step: one kc_decode_step per layer (append + TopN, engine.cpp:124-165), "
+                    "layer l+1 waits for layer l (no cross-layer overlap), row groups overlap recall with scoring "
+                    "inside a layer; NOT the headline (which pipelines the recall of layer l under the scoring of "
+                    "layer l+1, the attention-only bench of SURVEY.md section 7)"}
     line["roofline"]["achieved_isolated"] = k_bytes_layer / (iso["score"][0] / max(iso["score"][1], 1) * 1e-3) / 1e9
     if full is not None:
         full_ms = full["ms_per_step"]
@@ -548,6 +604,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-full-kv", action="store_true", help="skip the full-KV-in-HBM comparator")
+    ap.add_argument("--no-engine", action="store_true", help="skip the engine-realistic (per-layer) step")
     ap.add_argument("--tune", action="append", default=[], help="kc_set_tuning key=value")
     ap.add_argument("--shard", default="auto", choices=["auto", "batch", "units"],
                     help="N>1: own batch per rank (weak) or (batch, kv head) units of one batch (strong)")

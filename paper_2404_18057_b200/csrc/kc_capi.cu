@@ -23,9 +23,7 @@
 
 #include <memory>
 
-#include <cuda.h>  // green-context types; entry points via cudaGetDriverEntryPoint (no libcuda link)
 
-#include "kc_gather.hpp"
 #include "kc_kernels.cuh"
 #include "kcache_c.h"
 
@@ -114,19 +112,11 @@ struct LedgerEvent {
 struct LayerState {
   uint64_t len = 0;
   bool offloaded = false;
+  int stage = -1;  // prefill V staged in HBM slot `stage` (see kc_cache::v_stage), -1: in its arena
   uint64_t k_elems = 0, vfast_elems = 0, vslow_elems = 0;
 };
 
 constexpr int kRing = 3;
-
-// V recall strategies for offloaded layers (kc_set_tuning "recall_mode"):
-// zero-copy SM loads of the selected rows from the mapped host arena (bounded
-// by the GPU's page walks for the scattered 4-KB host pages),
-// host-side compaction + one DMA per layer (kc_gather.hpp; bounded by host
-// memory latency and cores), or both at once on disjoint row ranges: the
-// first host_frac of the (batch, kv head) rows are gathered by host threads
-// and DMA'd, the rest are pulled zero-copy, so the two independent limits add.
-constexpr int kRecallAuto = 0, kRecallZeroCopy = 1, kRecallDma = 2, kRecallHybrid = 3;
 
 bool host_pinned(const void* p) {
   cudaPointerAttributes a{};
@@ -135,19 +125,6 @@ bool host_pinned(const void* p) {
     return false;
   }
   return a.type == cudaMemoryTypeHost;
-}
-
-// driver entry points of the green-context API, resolved through the runtime
-// (the library does not link libcuda)
-template <typename F>
-F driver_fn(const char* name) {
-  void* p = nullptr;
-  cudaDriverEntryPointQueryResult q{};
-  if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess) {
-    cudaGetLastError();
-    return nullptr;
-  }
-  return reinterpret_cast<F>(p);
 }
 
 }  // namespace
@@ -189,7 +166,6 @@ struct kc_cache {
   DevBuf cand, cand_meta, fb_flags;  // candidate-mode selection scratch
   DevBuf part_ml;                    // fused full attention: split (m, l)
   DevBuf step_dev;                   // kc_decode_step: StepStatsDev accumulator
-  DevBuf row_done;                   // fused selection: per-row split completion counters
   cudaGraphExec_t step_exec = nullptr;  // kc_step_graph_*: the instantiated step graph
   cudaStream_t capture_st = nullptr;    // stream being captured (nullptr: none)
   kc_step_stats step_host{};         // kc_decode_step: host-known counters
@@ -198,13 +174,9 @@ struct kc_cache {
   DevBuf q_all;  // host-mode multi-layer calls: every layer's q, staged up front
   cudaStream_t in_st = nullptr;  // host-mode q uploads (off the scoring stream)
   cudaEvent_t ev_q0 = nullptr, ev_qall = nullptr;
-  // DMA recall: pinned copy of the selection, pinned compacted rows, HBM copy
-  PinnedBuf idx_host[kRing], stage_host[kRing];
-  DevBuf stage_dev[kRing];
-  std::unique_ptr<kc::GatherPool> pool;
-  cudaStream_t main_st = nullptr, side_st = nullptr, gather_st = nullptr, out_st = nullptr;
+  cudaStream_t main_st = nullptr, side_st = nullptr, out_st = nullptr;
   cudaEvent_t ev_start = nullptr, ev_end = nullptr, ev_sel[kRing] = {}, ev_rec[kRing] = {},
-              ev_gath[kRing] = {}, ev_scored[kRing] = {}, ev_out[kRing] = {}, ev_cp[kRing] = {},
+              ev_out[kRing] = {}, ev_cp[kRing] = {},
               ev_stats = nullptr;
   bool cp_pending[kRing] = {};  // ev_cp[slot] guards a device-mode copy of that slot
   // kc_append_kv_device enqueues on the caller's stream: ev_append marks the
@@ -212,23 +184,48 @@ struct kc_cache {
   cudaEvent_t ev_append = nullptr;
   bool append_pending = false;
   void order_after_appends(cudaStream_t st) {
-    if (!append_pending) return;
-    CK(cudaStreamWaitEvent(st, ev_append, 0));
+    if (append_pending) CK(cudaStreamWaitEvent(st, ev_append, 0));
+    order_after_offloads(st);
+  }
+
+  // Prefill V staging (the paper's overlapped offload): the
+  // prefill V of an offloaded layer is appended into one of two HBM stages
+  // and leaves for the host arena as ONE copy-engine D2H at
+  // offload_prefill_v, on off_st -- behind the caller's next layer instead of
+  // as PCIe stores inside the append kernel. A layer whose first append finds
+  // both stages still owned (offload not called yet) is appended straight
+  // into the arena (mapped stores), as are decode-phase rows.
+  DevBuf v_stage[2];
+  int stage_owner[2] = {-1, -1};  // layer appended into the slot and not yet offloaded
+  bool stage_copy[2] = {};        // ev_off[slot] marks an enqueued D2H of the slot
+  int next_stage = 0;
+  bool off_pending = false;       // some D2H may still be running
+  int prefill_stage = 1;          // tuning: 0 = always mapped stores (the r01 path)
+  cudaStream_t off_st = nullptr;
+  cudaEvent_t ev_staged[2] = {}, ev_off[2] = {};
+  void order_after_offloads(cudaStream_t st) {
+    if (!off_pending) return;
+    bool busy = false;
+    for (int k = 0; k < 2; ++k) {
+      if (!stage_copy[k]) continue;
+      if (cudaEventQuery(ev_off[k]) == cudaSuccess) {
+        stage_copy[k] = false;
+        continue;
+      }
+      cudaGetLastError();
+      busy = true;
+      CK(cudaStreamWaitEvent(st, ev_off[k], 0));
+    }
+    off_pending = busy;
   }
 
   // tuning
   int score_chunk = 0;
   int pipeline = 1;
-  int recall_mode = kRecallAuto;
   int select_global = 0;
   int score_stages = 4;
-  // persistent scoring grid (ctas_per_sm x SMs); 0 = one CTA per work item,
-  // the default: with the recall kernel co-running, the hardware block
-  // scheduler's dynamic balancing beats a static persistent split (measured)
-  int score_ctas_per_sm = 0;
-  int host_frac_pct = 50;  // hybrid recall: % of rows gathered by host threads
-  int auto_recall_mode = kRecallZeroCopy;  // what recall_mode 0 resolves to
-  int score_groups = 0;   // row groups per layer (score -> select -> recall each); 0 = auto
+  int score_groups = 0;
+  int group_first_pct = 0;  // row groups: % of the rows in the first group (0: equal groups)   // row groups per layer (score -> select -> recall each); 0 = auto
   int tlb_ahead = -1;      // K translation warm-up distance in rows (-1 auto: ~3 CTA waves, 0 off); r01: -2 %
   int score_mma = 1;       // GQA scoring on the tensor cores (TF32 split-q mma.sync)
   int k_policy = 0;        // L2 policy of the K stream (kc_device.cuh l2_policy)
@@ -236,26 +233,11 @@ struct kc_cache {
   // dense select), 1 always, 2 never
   int select_cand = 0;
   int cand_force_fallback = 0;  // test hook: every candidate-mode row takes the dense redo
-  int select_on_side = 0;  // pipelined: selection on the side stream too (measured: no gain)
   int full_fused = 1;      // decode_attention_full: fused K+V pass when V is in HBM
   int keep_logits = 0;     // leave dead logits in L2 instead of discarding them
-  int pdl = 0;             // scoring launched behind the preceding selection (PDL; measured neutral, r01)
-  int fuse_select = 0;     // MHA dense rows: the scoring kernel selects each row (kc_rowsel.cuh;
-                           // measured slower than the separate kernel)
   int recall_pipe = -1;   // software-pipelined recall kernel: -1 auto = GQA only (r01, managed
                           // arena: C3 8.35 -> 7.9 ms per step; MHA C2 no gain)
   int recall_ctas = 32;  // CTAs of the recall kernel (0: one per (batch, kv head)); 32 measured best at C2
-  int gather_threads = 0;  // 0: 3/4 of the host cores
-  // SM partition (green contexts): the pipelined call scores on score_sms SMs
-  // and runs the selection and the recall on the rest, so the selection of
-  // layer i leaves the critical path (0 = off)
-  int score_sms = 0;
-  int green_flags = 0;  // cuDevSmResourceSplitByCount useFlags (1: ignore SM co-scheduling, finer groups)
-  int green_sms = 0;                      // partition the streams below were built for
-  CUgreenCtx green[2] = {};               // [0] scoring SMs, [1] the rest
-  cudaStream_t gst_score = nullptr, gst_sel = nullptr, gst_rec = nullptr;
-  cudaEvent_t ev_gfork = nullptr, ev_gjoin = nullptr;
-
   // per-kernel CUDA-event timing (kc_profile): [kind] -> (start, stop) pairs
   bool prof_on = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof[3];
@@ -284,15 +266,14 @@ struct kc_cache {
     prof[kind].push_back({a, b});
   }
 
-  // scoring buffer lb (0/1) of logits / partials / candidates
-  float* logits_buf(int lb) { return logits.as<float>() + (size_t)lb * batch * n_q * (size_t)lstride; }
-  float2* partials_buf(int lb) { return partials.as<float2>() + (size_t)lb * batch * n_q * (size_t)max_splits; }
-  uint2* cand_buf(int lb) { return cand.as<uint2>() + (size_t)lb * rows * (size_t)lstride; }
-  uint2* cand_meta_buf(int lb) { return cand_meta.as<uint2>() + (size_t)lb * rows * (size_t)max_splits; }
   void* k_layer(uint64_t layer) const { return (char*)k_arena + layer * k_layer_bytes; }
   // offloaded layer j = layer - L: managed layers first, the rest (beyond the
   // driver's managed-memory cap) in the pinned arena
   void* v_layer(uint64_t layer) const {
+    if (layer >= L && layers[layer].stage >= 0) return v_stage[layers[layer].stage].p;
+    return v_arena_layer(layer);
+  }
+  void* v_arena_layer(uint64_t layer) const {
     if (layer < L) return (void*)((char*)v_dev + layer * v_layer_bytes);
     const uint64_t j = layer - L;
     if (j < v_managed.size()) return v_managed[j];
@@ -327,7 +308,6 @@ struct kc_cache {
 };
 
 namespace {
-void release_green(kc_cache* c);  // green-context SM partition (below)
 
 template <typename F>
 int guarded(F&& f) {
@@ -412,18 +392,16 @@ void destroy(kc_cache* c) {
   cudaSetDevice(c->device);
   if (c->main_st) cudaStreamSynchronize(c->main_st);
   if (c->side_st) cudaStreamSynchronize(c->side_st);
-  if (c->gather_st) cudaStreamSynchronize(c->gather_st);
   if (c->out_st) cudaStreamSynchronize(c->out_st);
+  if (c->off_st) cudaStreamSynchronize(c->off_st);
   cudaDeviceSynchronize();
-  c->pool.reset();
-  for (int i = 0; i < kRing; ++i) {
-    c->idx_host[i].release();
-    c->stage_host[i].release();
-    c->stage_dev[i].release();
-    if (c->ev_gath[i]) cudaEventDestroy(c->ev_gath[i]);
-  }
-  if (c->gather_st) cudaStreamDestroy(c->gather_st);
   if (c->out_st) cudaStreamDestroy(c->out_st);
+  if (c->off_st) cudaStreamDestroy(c->off_st);
+  for (int k = 0; k < 2; ++k) {
+    c->v_stage[k].release();
+    if (c->ev_staged[k]) cudaEventDestroy(c->ev_staged[k]);
+    if (c->ev_off[k]) cudaEventDestroy(c->ev_off[k]);
+  }
   if (c->in_st) cudaStreamDestroy(c->in_st);
   if (c->ev_q0) cudaEventDestroy(c->ev_q0);
   if (c->ev_qall) cudaEventDestroy(c->ev_qall);
@@ -438,13 +416,12 @@ void destroy(kc_cache* c) {
   c->v_managed.clear();
   for (DevBuf* b : {&c->logits, &c->partials, &c->keys, &c->part_out, &c->stage_src, &c->stage_k,
                     &c->stage_v, &c->sel_rows, &c->sel_pos, &c->gather_out, &c->cand, &c->cand_meta,
-                    &c->fb_flags, &c->part_ml, &c->step_dev, &c->row_done})
+                    &c->fb_flags, &c->part_ml, &c->step_dev})
     b->release();
   for (int i = 0; i < kRing; ++i) {
     c->q32[i].release(); c->idx[i].release(); c->w[i].release(); c->dropped[i].release();
     c->norm[i].release(); c->out_tmp[i].release(); c->idx_exp[i].release();
     if (c->ev_sel[i]) cudaEventDestroy(c->ev_sel[i]);
-    if (c->ev_scored[i]) cudaEventDestroy(c->ev_scored[i]);
     if (c->ev_out[i]) cudaEventDestroy(c->ev_out[i]);
     if (c->ev_cp[i]) cudaEventDestroy(c->ev_cp[i]);
     if (c->ev_rec[i]) cudaEventDestroy(c->ev_rec[i]);
@@ -457,9 +434,6 @@ void destroy(kc_cache* c) {
   if (c->ev_stats) cudaEventDestroy(c->ev_stats);
   if (c->ev_append) cudaEventDestroy(c->ev_append);
   if (c->step_exec) cudaGraphExecDestroy(c->step_exec);
-  release_green(c);
-  if (c->ev_gfork) cudaEventDestroy(c->ev_gfork);
-  if (c->ev_gjoin) cudaEventDestroy(c->ev_gjoin);
   if (c->main_st) cudaStreamDestroy(c->main_st);
   if (c->side_st) cudaStreamDestroy(c->side_st);
   delete c;
@@ -492,8 +466,35 @@ void append_account(kc_cache* c, uint64_t layer, uint64_t rows) {
                            std::to_string(c->cap) + " bytes");
 }
 
+// Prefill V of an offloaded layer: on its first append, take a free HBM stage
+// (the stream waits for the stage's previous D2H). No free stage -> the layer
+// is appended straight into its host arena.
+void acquire_stage(kc_cache* c, uint64_t layer, cudaStream_t st) {
+  LayerState& ls = c->layers[layer];
+  if (!c->prefill_stage || c->phase != KC_PREFILL || layer < c->L || ls.offloaded || ls.stage >= 0 || ls.len > 0)
+    return;
+  for (int k = 0; k < 2; ++k) {
+    const int slot = (c->next_stage + k) & 1;
+    if (c->stage_owner[slot] >= 0) continue;
+    if (!c->v_stage[slot].p) {
+      if (cudaMalloc(&c->v_stage[slot].p, c->v_layer_bytes) != cudaSuccess) {
+        cudaGetLastError();  // HBM too tight for a stage: mapped stores instead
+        c->v_stage[slot].p = nullptr;
+        return;
+      }
+      c->v_stage[slot].bytes = c->v_layer_bytes;
+    }
+    if (c->stage_copy[slot]) CK(cudaStreamWaitEvent(st, c->ev_off[slot], 0));
+    c->stage_owner[slot] = (int)layer;
+    ls.stage = slot;
+    c->next_stage = slot ^ 1;
+    return;
+  }
+}
+
 void enqueue_append(kc_cache* c, uint64_t layer, const void* k, const void* v, int dt, uint64_t rows,
                     cudaStream_t st) {
+  acquire_stage(c, layer, st);
   kc::AppendParams ap{};
   ap.n_rows = (int64_t)rows;
   ap.max_seq = (int64_t)c->cfg.max_seq;
@@ -508,6 +509,8 @@ void enqueue_append(kc_cache* c, uint64_t layer, const void* k, const void* v, i
   ap.dst = c->v_layer(layer);
   kc::append_launch(ap, dt, c->dtype, st);
   CK(cudaGetLastError());
+  const int slot = c->layers[layer].stage;
+  if (slot >= 0) CK(cudaEventRecord(c->ev_staged[slot], st));
 }
 
 // ---- decode ----------------------------------------------------------------
@@ -538,28 +541,18 @@ StepGeom geom(kc_cache* c, uint64_t top_n, int chunk_g = -1) {
 }
 
 void enqueue_score(kc_cache* c, uint64_t layer, const float* q32, const StepGeom& g, cudaStream_t st,
-                   int row0, int nrows, bool cand = false, int lb = 0, int slot = -1, bool pdl = false) {
+                   int row0, int nrows, bool cand = false) {
   kc::ScoreParams sp{};
   sp.row0 = row0;
-  sp.pdl = pdl ? 1 : 0;
-  if (slot >= 0) {  // fused selection into ring slot `slot`
-    sp.row_done = c->row_done.as<uint32_t>();
-    sp.sel_idx = c->idx[slot].as<uint32_t>();
-    sp.sel_w = c->w[slot].as<float>();
-    sp.sel_dropped = c->dropped[slot].as<double>();
-    sp.sel_norm = c->norm[slot].as<float>();
-    sp.sel_nc = g.nc;
-    sp.keep_logits = c->keep_logits;
-  }
   if (cand) {
-    sp.cand = c->cand_buf(lb);
-    sp.cand_meta = c->cand_meta_buf(lb);
+    sp.cand = c->cand.as<uint2>();
+    sp.cand_meta = c->cand_meta.as<uint2>();
     sp.cand_nc = g.nc;
   }
   sp.k = c->k_layer(layer);
   sp.q = q32;
-  sp.logits = c->logits_buf(lb);
-  sp.partials = c->partials_buf(lb);
+  sp.logits = c->logits.as<float>();
+  sp.partials = c->partials.as<float2>();
   sp.max_seq = (int64_t)c->cfg.max_seq;
   sp.lstride = c->lstride;
   sp.s = g.s;
@@ -572,7 +565,6 @@ void enqueue_score(kc_cache* c, uint64_t layer, const float* q32, const StepGeom
   sp.max_splits = c->max_splits;
   sp.scale = 1.0f / std::sqrt(static_cast<float>(c->h));  // attention.hpp:15-17
   sp.stages = c->score_stages;
-  sp.ctas_per_sm = c->score_ctas_per_sm;
   sp.k_policy = c->k_policy;
   sp.use_mma = c->score_mma;
   // ~3 waves of CTAs ahead (one CTA per item, 3 per SM)
@@ -647,78 +639,6 @@ const float* stage_q_all(kc_cache* c, uint64_t n, const void* const* q, int q_dt
   return all;
 }
 
-void release_green(kc_cache* c) {
-  using DestroyFn = CUresult (*)(CUgreenCtx);
-  for (cudaStream_t* s : {&c->gst_score, &c->gst_sel, &c->gst_rec})
-    if (*s) {
-      cudaStreamSynchronize(*s);
-      cudaStreamDestroy(*s);
-      *s = nullptr;
-    }
-  static DestroyFn destroy = driver_fn<DestroyFn>("cuGreenCtxDestroy");
-  for (CUgreenCtx& g : c->green)
-    if (g) {
-      if (destroy) destroy(g);
-      g = nullptr;
-    }
-  c->green_sms = 0;
-}
-
-// Green contexts for the SM partition: c->score_sms SMs (rounded up to the
-// driver's split granularity) for the scoring, the remaining SMs for the
-// selection and the (high-priority) recall. Kernels launched on a green
-// context's stream run only on its SMs; events order work across them.
-void ensure_green(kc_cache* c) {
-  if (c->green_sms == c->score_sms && c->gst_score) return;
-  release_green(c);
-  using DevGetFn = CUresult (*)(CUdevice*, int);
-  using ResFn = CUresult (*)(CUdevice, CUdevResource*, CUdevResourceType);
-  using SplitFn = CUresult (*)(CUdevResource*, unsigned int*, const CUdevResource*, CUdevResource*, unsigned int,
-                               unsigned int);
-  using DescFn = CUresult (*)(CUdevResourceDesc*, CUdevResource*, unsigned int);
-  using CreateFn = CUresult (*)(CUgreenCtx*, CUdevResourceDesc, CUdevice, unsigned int);
-  using StreamFn = CUresult (*)(CUstream*, CUgreenCtx, unsigned int, int);
-  static DevGetFn dev_get = driver_fn<DevGetFn>("cuDeviceGet");
-  static ResFn get_res = driver_fn<ResFn>("cuDeviceGetDevResource");
-  static SplitFn split = driver_fn<SplitFn>("cuDevSmResourceSplitByCount");
-  static DescFn gen = driver_fn<DescFn>("cuDevResourceGenerateDesc");
-  static CreateFn create = driver_fn<CreateFn>("cuGreenCtxCreate");
-  static StreamFn mk_stream = driver_fn<StreamFn>("cuGreenCtxStreamCreate");
-  if (!dev_get || !get_res || !split || !gen || !create || !mk_stream)
-    fail(KC_ECUDA, "score_sms: the driver has no green-context API");
-  auto ok = [](CUresult r, const char* what) {
-    if (r != CUDA_SUCCESS) fail(KC_ECUDA, std::string("score_sms: ") + what + " failed (" + std::to_string((int)r) + ")");
-  };
-  CUdevice dev{};
-  ok(dev_get(&dev, c->device), "cuDeviceGet");
-  CUdevResource all{};
-  ok(get_res(dev, &all, CU_DEV_RESOURCE_TYPE_SM), "cuDeviceGetDevResource");
-  if ((unsigned)c->score_sms >= all.sm.smCount) fail(KC_EARG, "score_sms must leave SMs for the selection and recall");
-  CUdevResource grp{}, rest{};
-  unsigned int nb = 1;
-  ok(split(&grp, &nb, &all, &rest, (unsigned)c->green_flags, (unsigned)c->score_sms), "cuDevSmResourceSplitByCount");
-  if (nb != 1 || rest.sm.smCount == 0) fail(KC_EARG, "score_sms: no SMs left for the selection and recall");
-  if (getenv("KCACHE_VERBOSE"))
-    fprintf(stderr, "kcache: SM partition %u scoring / %u selection+recall\n", grp.sm.smCount, rest.sm.smCount);
-  CUdevResourceDesc da{}, db{};
-  ok(gen(&da, &grp, 1), "cuDevResourceGenerateDesc");
-  ok(gen(&db, &rest, 1), "cuDevResourceGenerateDesc");
-  ok(create(&c->green[0], da, dev, CU_GREEN_CTX_DEFAULT_STREAM), "cuGreenCtxCreate");
-  ok(create(&c->green[1], db, dev, CU_GREEN_CTX_DEFAULT_STREAM), "cuGreenCtxCreate");
-  int lo = 0, hi = 0;
-  CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-  CUstream s0{}, s1{}, s2{};
-  ok(mk_stream(&s0, c->green[0], CU_STREAM_NON_BLOCKING, 0), "cuGreenCtxStreamCreate");
-  ok(mk_stream(&s1, c->green[1], CU_STREAM_NON_BLOCKING, 0), "cuGreenCtxStreamCreate");
-  ok(mk_stream(&s2, c->green[1], CU_STREAM_NON_BLOCKING, hi), "cuGreenCtxStreamCreate");
-  c->gst_score = (cudaStream_t)s0;
-  c->gst_sel = (cudaStream_t)s1;
-  c->gst_rec = (cudaStream_t)s2;
-  if (!c->ev_gfork) CK(cudaEventCreateWithFlags(&c->ev_gfork, cudaEventDisableTiming));
-  if (!c->ev_gjoin) CK(cudaEventCreateWithFlags(&c->ev_gjoin, cudaEventDisableTiming));
-  c->green_sms = c->score_sms;
-}
-
 void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const void* const* q,
                       int q_dtype, uint64_t top_n, uint32_t flags, kc_topn_out* outs,
                       cudaStream_t user_st) {
@@ -730,6 +650,7 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
   const bool io_device = flags & KC_IO_DEVICE;
   cudaStream_t st = io_device ? user_st : c->main_st;
   if (!io_device) c->order_after_appends(st);
+  else c->order_after_offloads(st);
   const StepGeom g = geom(c, top_n);
   const uint64_t nc = (uint64_t)g.nc;
   const uint64_t slots = c->batch * c->n_q;
@@ -757,109 +678,61 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
   if (!io_device && c->capture_st) fail(KC_ESTATE, "host-memory I/O inside a step graph capture");
   bool out_used = false;  // c->out_st carries work of this call
   const float* q_all = c->capture_st ? nullptr : stage_q_all(c, n, q, q_dtype, io_device, st);
-  // SM partition: fork onto the green-context streams (scoring / selection /
-  // recall), joined back into the caller's stream at the end
-  const bool green = c->score_sms > 0 && c->pipeline && !c->capture_st;
-  const cudaStream_t call_st = st;
-  if (green) {
-    ensure_green(c);
-    CK(cudaEventRecord(c->ev_gfork, call_st));
-    for (cudaStream_t s : {c->gst_score, c->gst_sel, c->gst_rec}) CK(cudaStreamWaitEvent(s, c->ev_gfork, 0));
-    st = c->gst_score;
-  }
-  cudaStream_t side = c->pipeline ? (green ? c->gst_rec : c->side_st) : st;
-  // the selection runs on the side stream too (or its own green stream), so
-  // the main stream is scoring only: scoring(i+1) overlaps selection(i) as
-  // well as recall(i)
-  const bool side_select = side != st && (c->select_on_side || green);
-  cudaStream_t selst = side_select ? (green ? c->gst_sel : side) : st;
-  // Programmatic dependent launch: the scoring of layer i (group g) may start
-  // behind the selection before it when nothing launches q in between (q
-  // direct or staged up front) and that selection reads the other scoring
-  // buffer (lb alternates per layer); scoring i waits for selection i-2 (the
-  // last reader of its buffer) by event.
-  const bool q_direct = q_all || (io_device && q_dtype == KC_F32);
-  const bool pdl_ok = c->pdl && side != st && !side_select && q_direct;
+  // The main stream runs q staging, scoring and selection of layer i; a
+  // high-priority side stream runs the recall + P.V of layer i under the
+  // scoring of layer i+1. A ring of kRing selection slots orders the two.
+  cudaStream_t side = c->pipeline ? c->side_st : st;
   CK(cudaEventRecord(c->ev_start, st));
   if (side != st) CK(cudaStreamWaitEvent(side, c->ev_start, 0));
 
   for (uint64_t i = 0; i < n; ++i) {
     const int slot = (int)(i % kRing);
     const uint64_t layer = layers[i];
-    // selection on the side stream: scoring buffer i % 2, free once the
-    // selection of layer i-2 (which also released q32[slot]) has finished
-    const int lb = (side_select || pdl_ok) ? (int)(i & 1) : 0;
-    if ((side_select || pdl_ok) && i >= 2) CK(cudaStreamWaitEvent(st, c->ev_sel[(i - 2) % kRing], 0));
     if (q_all && i == 1) CK(cudaStreamWaitEvent(st, c->ev_qall, 0));
     const float* q32 = q_all ? q_all + i * (c->batch * c->n_q * c->h)
                              : stage_q(c, slot, q[i], q_dtype, io_device, st, i, n);
     kc_topn_out& o = outs[i];
-    // Offloaded layer in DMA mode: compact the selected rows on the host (pool
-    // threads, stream-ordered via cudaLaunchHostFunc on gather_st), then one DMA.
-    const bool offl = layer >= c->L;
-    const int mode = c->recall_mode == kRecallAuto ? c->auto_recall_mode : c->recall_mode;
-    // rows [0, host_rows) are host-gathered + DMA'd, [host_rows, rows) zero-copy
-    const int host_rows = !offl ? 0
-                          : mode == kRecallDma ? (int)c->rows
-                          : mode == kRecallHybrid ? (int)std::min<int64_t>((int64_t)c->rows, ((int64_t)c->rows * c->host_frac_pct + 50) / 100)
-                          : 0;
-    const bool dma = host_rows > 0;
     // Row groups: score -> select -> recall per group of (batch, kv head)
     // rows, so the recall of group g overlaps the scoring of group g+1.
     // score_groups 0 = auto: one group when layers pipeline against each
     // other, two for a single-layer call (the engine's per-layer block),
     // where only the intra-layer overlap is available (r01: 730 -> 690 us)
     const int64_t want_groups = c->score_groups > 0 ? c->score_groups : (n == 1 ? 2 : 1);
-    const int n_groups = dma ? 1 : (int)std::max<int64_t>(1, std::min<int64_t>(want_groups, (int64_t)c->rows));
+    const int n_groups = (int)std::max<int64_t>(1, std::min<int64_t>(want_groups, (int64_t)c->rows));
     // Candidate mode (MHA, N <= 128): scoring emits only each split's
     // possible top-N positions instead of an fp32 logit per position, and the
     // selection ranks ~1.3 N per split -- automatic for rows longer than the
     // register-resident dense selection.
     const bool cand = (c->select_cand == 1 || (c->select_cand == 0 && g.s > kc::kDenseRegMaxS)) &&
                       !c->select_global && kc::score_cand_supported(c->dtype, (int)c->h, (int)c->G, g.chunk, g.nc);
-    // Fused selection (MHA dense rows, N <= 256): the scoring CTA that
-    // completes a row's last split selects the row; no selection launch.
-    const bool fused = !cand && c->fuse_select && !c->select_global &&
-                       kc::score_fused_select_supported(c->dtype, (int)c->h, (int)c->G, g.chunk, g.nc,
-                                                        c->score_ctas_per_sm);
-    if (fused && !c->row_done.p) {
-      c->row_done.ensure(c->rows * 4);
-      CK(cudaMemsetAsync(c->row_done.p, 0, c->rows * 4, st));
-    }
     if (cand) {
-      c->cand.ensure(2 * checked_mul({c->rows, (uint64_t)c->lstride, 8}));
-      c->cand_meta.ensure(2 * checked_mul({c->rows, (uint64_t)c->max_splits, 8}));
+      c->cand.ensure(checked_mul({c->rows, (uint64_t)c->lstride, 8}));
+      c->cand_meta.ensure(checked_mul({c->rows, (uint64_t)c->max_splits, 8}));
       c->fb_flags.ensure(c->rows * 4);
     }
-    const int gsz = (int)((c->rows + n_groups - 1) / n_groups);
+    // group sizes: the first group takes group_first_pct % of the rows (0:
+    // equal groups), the rest split evenly -- a smaller last group shortens
+    // the tail (its selection + recall) that nothing overlaps
+    const int rows_i = (int)c->rows;
+    int first = (rows_i + n_groups - 1) / n_groups;
+    if (n_groups > 1 && c->group_first_pct > 0)
+      first = std::max(1, std::min(rows_i - (n_groups - 1), (rows_i * c->group_first_pct + 50) / 100));
+    const int rest = n_groups > 1 ? (rows_i - first + n_groups - 2) / (n_groups - 1) : 0;
     for (int gi = 0; gi < n_groups; ++gi) {
-      const int r0 = gi * gsz;
-      const int nr = std::min<int>(gsz, (int)c->rows - r0);
+      const int r0 = gi == 0 ? 0 : first + (gi - 1) * rest;
+      const int nr = std::min<int>(gi == 0 ? first : rest, rows_i - r0);
       if (nr <= 0) break;
-      enqueue_score(c, layer, q32, g, st, r0, nr, cand, lb, fused ? slot : -1, pdl_ok && (i > 0 || gi > 0));
-      if (side_select) {
-        CK(cudaEventRecord(c->ev_scored[slot], st));
-        CK(cudaStreamWaitEvent(selst, c->ev_scored[slot], 0));
-        // the selection overwrites ring slot `slot`: its recall (layer i-3),
-        // the device copies and host D2H of its outputs (on out_st) must be
-        // done -- also when selst == side, where only the recall is ordered
-        if (gi == 0 && i >= (uint64_t)kRing) {
-          CK(cudaStreamWaitEvent(selst, c->ev_rec[slot], 0));
-          if (c->cp_pending[slot]) CK(cudaStreamWaitEvent(selst, c->ev_cp[slot], 0));
-        }
-      } else if (gi == 0 && i >= (uint64_t)kRing && side != st) {
+      enqueue_score(c, layer, q32, g, st, r0, nr, cand);
+      // the selection overwrites ring slot `slot`: the recall of layer i-kRing
+      // and the copies of its outputs must be done
+      if (gi == 0 && i >= (uint64_t)kRing && side != st) {
         CK(cudaStreamWaitEvent(st, c->ev_rec[slot], 0));
         if (c->cp_pending[slot]) CK(cudaStreamWaitEvent(st, c->ev_cp[slot], 0));
       }
-      // the scoring above may have started behind the previous selection
-      // (PDL), which orders nothing after it: make this selection wait for
-      // the previous one explicitly (they share scratch: keys, fb_flags)
-      if (pdl_ok && (i > 0 || gi > 0))
-        CK(cudaStreamWaitEvent(st, c->ev_sel[gi > 0 ? slot : (int)((i - 1) % kRing)], 0));
 
       kc::SelectParams sp{};
-      sp.logits = c->logits_buf(lb);
-      sp.partials = c->partials_buf(lb);
+      sp.logits = c->logits.as<float>();
+      sp.partials = c->partials.as<float2>();
       sp.keys = c->keys.as<uint32_t>();
       sp.idx = c->idx[slot].as<uint32_t>();
       sp.w = c->w[slot].as<float>();
@@ -878,8 +751,8 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
       sp.force_global = c->select_global;
       sp.keep_logits = c->keep_logits;
       if (cand) {
-        sp.cand = c->cand_buf(lb);
-        sp.cand_meta = c->cand_meta_buf(lb);
+        sp.cand = c->cand.as<uint2>();
+        sp.cand_meta = c->cand_meta.as<uint2>();
         sp.fb_flags = c->fb_flags.as<uint32_t>();
         sp.chunk = g.chunk;
         sp.k = c->k_layer(layer);
@@ -890,46 +763,18 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
         sp.scale = 1.0f / std::sqrt(static_cast<float>(c->h));  // attention.hpp:15-17
         sp.force_fallback = c->cand_force_fallback;
       }
-      if (!fused) c->timed(1, selst, [&] {
+      c->timed(1, st, [&] {
         if (cand) {
-          if (!kc::select_cand_launch(sp, selst)) fail(KC_ECUDA, "candidate selection unavailable for this shape");
+          if (!kc::select_cand_launch(sp, st)) fail(KC_ECUDA, "candidate selection unavailable for this shape");
         } else {
-          kc::select_launch(sp, selst);
+          kc::select_launch(sp, st);
         }
       });
-      CK(cudaEventRecord(c->ev_sel[slot], selst));
-      if (side != selst) CK(cudaStreamWaitEvent(side, c->ev_sel[slot], 0));
+      CK(cudaEventRecord(c->ev_sel[slot], st));
+      if (side != st) CK(cudaStreamWaitEvent(side, c->ev_sel[slot], 0));
 
       kc::RecallParams rp{};
       rp.v = c->v_layer(layer);
-      const size_t stage_bytes = (size_t)host_rows * nc * c->h * c->esz;
-      if (dma) {
-        c->idx_host[slot].ensure((size_t)host_rows * nc * 4);
-        c->stage_host[slot].ensure(stage_bytes);
-        c->stage_dev[slot].ensure(stage_bytes);
-        if (!c->pool) {
-          int t = c->gather_threads;
-          if (t <= 0) t = std::max(1, (int)std::thread::hardware_concurrency() * 3 / 4);
-          c->pool = std::make_unique<kc::GatherPool>(t - 1);
-        }
-        CK(cudaStreamWaitEvent(c->gather_st, c->ev_sel[slot], 0));
-        CK(cudaMemcpyAsync(c->idx_host[slot].p, c->idx[slot].p, (size_t)host_rows * nc * 4, cudaMemcpyDeviceToHost,
-                           c->gather_st));
-        auto* job = new kc::GatherJob{c->pool.get(),
-                                      c->v_host_layer(layer),
-                                      c->cfg.max_seq * c->h * c->esz,
-                                      c->h * c->esz,
-                                      static_cast<const uint32_t*>(c->idx_host[slot].p),
-                                      (uint64_t)host_rows,
-                                      nc,
-                                      static_cast<char*>(c->stage_host[slot].p)};
-        cudaError_t he = cudaLaunchHostFunc(c->gather_st, kc::gather_host_fn, job);
-        if (he != cudaSuccess) {
-          delete job;
-          CK(he);
-        }
-        CK(cudaEventRecord(c->ev_gath[slot], c->gather_st));
-      }
       rp.staged = 0;
       rp.grid = c->recall_ctas;
       rp.pipelined = c->recall_pipe < 0 ? (c->G > 1 ? 1 : 0) : c->recall_pipe;
@@ -942,26 +787,11 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
       rp.h = (int)c->h;
       rp.n_kv = (int)c->n_kv;
       rp.G = (int)c->G;
-      rp.rows = dma ? nr - host_rows : nr;
+      rp.rows = nr;
       rp.renormalize = (flags & KC_RENORMALIZE) ? 1 : 0;
       rp.reverse = (flags & KC_REVERSE_ACCUM) ? 1 : 0;
-      rp.row_offset = dma ? host_rows : r0;
-      c->timed(2, side, [&] {
-        // zero-copy rows first (they need nothing but the selection), then the
-        // host-gathered rows once their DMA has landed
-        if (rp.rows > 0) kc::recall_launch(rp, c->dtype, side);
-        if (dma) {
-          CK(cudaStreamWaitEvent(side, c->ev_gath[slot], 0));
-          CK(cudaMemcpyAsync(c->stage_dev[slot].p, c->stage_host[slot].p, stage_bytes, cudaMemcpyHostToDevice,
-                             side));
-          kc::RecallParams hp = rp;
-          hp.v = c->stage_dev[slot].p;
-          hp.staged = 1;
-          hp.row_offset = 0;
-          hp.rows = host_rows;
-          kc::recall_launch(hp, c->dtype, side);
-        }
-      });
+      rp.row_offset = r0;
+      c->timed(2, side, [&] { kc::recall_launch(rp, c->dtype, side); });
     }
 
     // device mode: the selection outputs depend on the selection only --
@@ -1033,11 +863,6 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
       CK(cudaEventRecord(c->ev_end, c->out_st));
       CK(cudaStreamWaitEvent(st, c->ev_end, 0));
     }
-  }
-  if (green) {  // join the partition back into the caller's stream
-    CK(cudaEventRecord(c->ev_gjoin, st));
-    CK(cudaStreamWaitEvent(call_st, c->ev_gjoin, 0));
-    st = call_st;
   }
   if (!io_device) {
     CK(cudaStreamSynchronize(st));
@@ -1121,17 +946,21 @@ int kc_cache_create(const kc_config* cfg, uint64_t batch, uint64_t resident_laye
       c->lstride = (int64_t)((cfg->max_seq + 31) & ~31ull);
       c->kstride = c->lstride;
       c->max_splits = (int)((cfg->max_seq + 63) / 64);
-      // two scoring buffers: scoring of layer i+1 writes one while the
-      // selection of layer i reads the other (selection on the side stream)
-      c->logits.ensure(2 * checked_mul({batch, c->n_q, (uint64_t)c->lstride, 4}));
-      c->partials.ensure(2 * checked_mul({batch, c->n_q, (uint64_t)c->max_splits, 8}));
+      // one scoring buffer: the selection of layer i runs on the scoring
+      // stream before the scoring of layer i+1
+      c->logits.ensure(checked_mul({batch, c->n_q, (uint64_t)c->lstride, 4}));
+      c->partials.ensure(checked_mul({batch, c->n_q, (uint64_t)c->max_splits, 8}));
       c->keys.ensure(checked_mul({c->rows, (uint64_t)c->kstride, 4}));
       int lo = 0, hi = 0;
       CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
       CK(cudaStreamCreateWithFlags(&c->main_st, cudaStreamNonBlocking));
       CK(cudaStreamCreateWithPriority(&c->side_st, cudaStreamNonBlocking, hi));
-      CK(cudaStreamCreateWithPriority(&c->gather_st, cudaStreamNonBlocking, hi));
       CK(cudaStreamCreateWithFlags(&c->out_st, cudaStreamNonBlocking));
+      CK(cudaStreamCreateWithFlags(&c->off_st, cudaStreamNonBlocking));
+      for (int k = 0; k < 2; ++k) {
+        CK(cudaEventCreateWithFlags(&c->ev_staged[k], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&c->ev_off[k], cudaEventDisableTiming));
+      }
       CK(cudaStreamCreateWithFlags(&c->in_st, cudaStreamNonBlocking));
       CK(cudaEventCreateWithFlags(&c->ev_q0, cudaEventDisableTiming));
       CK(cudaEventCreateWithFlags(&c->ev_qall, cudaEventDisableTiming));
@@ -1141,11 +970,9 @@ int kc_cache_create(const kc_config* cfg, uint64_t batch, uint64_t resident_laye
       CK(cudaEventCreateWithFlags(&c->ev_append, cudaEventDisableTiming));
       for (int i = 0; i < kRing; ++i) {
         CK(cudaEventCreateWithFlags(&c->ev_sel[i], cudaEventDisableTiming));
-        CK(cudaEventCreateWithFlags(&c->ev_scored[i], cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&c->ev_out[i], cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&c->ev_cp[i], cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&c->ev_rec[i], cudaEventDisableTiming));
-        CK(cudaEventCreateWithFlags(&c->ev_gath[i], cudaEventDisableTiming));
       }
     } catch (...) {
       destroy(c);
@@ -1198,6 +1025,23 @@ int kc_offload_prefill_v(kc_cache* c, uint64_t layer) {
     if (st.offloaded)
       fail(KC_ESTATE, "offload_prefill_v: layer " + std::to_string(layer) + " already offloaded");
     const uint64_t elements = st.vfast_elems;
+    if (st.stage >= 0) {
+      // the staged prefill V -> its host arena: one copy-engine D2H behind the
+      // layer's last append, asynchronous to the caller (readers of the layer
+      // wait on ev_off: order_after_offloads)
+      set_dev(c);
+      const int slot = st.stage;
+      const size_t pitch = (size_t)c->cfg.max_seq * c->h * c->esz;
+      CK(cudaStreamWaitEvent(c->off_st, c->ev_staged[slot], 0));
+      if (st.len > 0)
+        CK(cudaMemcpy2DAsync(c->v_arena_layer(layer), pitch, c->v_stage[slot].p, pitch, st.len * c->h * c->esz,
+                             c->rows, cudaMemcpyDefault, c->off_st));
+      CK(cudaEventRecord(c->ev_off[slot], c->off_st));
+      c->stage_copy[slot] = true;
+      c->stage_owner[slot] = -1;
+      c->off_pending = true;
+      st.stage = -1;
+    }
     st.vslow_elems += elements;
     st.vfast_elems = 0;
     st.offloaded = true;
@@ -1210,6 +1054,16 @@ int kc_begin_decode(kc_cache* c) {
     for (uint64_t l = c->L; l < c->layers.size(); ++l)
       if (!c->layers[l].offloaded)
         fail(KC_ESTATE, "begin_decode: layer " + std::to_string(l) + " was never offloaded");
+    // every prefill stage has been handed to the copy engine: once its D2H
+    // lands the HBM goes back to the caller
+    if (c->v_stage[0].p || c->v_stage[1].p) {
+      set_dev(c);
+      CK(cudaStreamSynchronize(c->off_st));
+      c->v_stage[0].release();
+      c->v_stage[1].release();
+      c->stage_copy[0] = c->stage_copy[1] = false;
+      c->off_pending = false;
+    }
     c->phase = KC_DECODE;
   });
 }
@@ -1234,6 +1088,7 @@ int kc_decode_step(kc_cache* c, uint64_t layer, const void* q, const void* k_new
     set_dev(c);
     cudaStream_t st = io_device ? (cudaStream_t)stream : c->main_st;
     if (!io_device) c->order_after_appends(st);
+    else c->order_after_offloads(st);
     // engine.cpp:143 -- this step's K/V row of every batch row
     const uint64_t rows = c->batch;
     append_checks(c, layer, rows);
@@ -1300,13 +1155,9 @@ void prepare_step_buffers(kc_cache* c, uint64_t top_n, cudaStream_t st) {
     c->q32[r].ensure(slots * c->h * sizeof(float));
   }
   if (c->G == 1 && c->select_cand != 2) {  // candidate mode may switch on as the rows grow
-    c->cand.ensure(2 * checked_mul({c->rows, (uint64_t)c->lstride, 8}));
-    c->cand_meta.ensure(2 * checked_mul({c->rows, (uint64_t)c->max_splits, 8}));
+    c->cand.ensure(checked_mul({c->rows, (uint64_t)c->lstride, 8}));
+    c->cand_meta.ensure(checked_mul({c->rows, (uint64_t)c->max_splits, 8}));
     c->fb_flags.ensure(c->rows * 4);
-  }
-  if (!c->row_done.p) {
-    c->row_done.ensure(c->rows * 4);
-    CK(cudaMemsetAsync(c->row_done.p, 0, c->rows * 4, st));
   }
   if (!c->step_dev.p) {
     c->step_dev.ensure(sizeof(kc::StepStatsDev));
@@ -1329,7 +1180,6 @@ int kc_step_graph_begin(kc_cache* c, uint64_t top_n, void* stream) {
     // have to order against (their events would cross the capture boundary)
     CK(cudaStreamSynchronize(c->side_st));
     CK(cudaStreamSynchronize(c->out_st));
-    CK(cudaStreamSynchronize(c->gather_st));
     CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
     c->capture_st = st;
   });
@@ -1404,6 +1254,7 @@ int kc_decode_full(kc_cache* c, uint64_t layer, const void* q, int q_dtype, uint
     cudaStream_t st = io_device ? (cudaStream_t)stream : c->main_st;
     if (!io_device && c->capture_st) fail(KC_ESTATE, "host-memory I/O inside a step graph capture");
     if (!io_device) c->order_after_appends(st);
+    else c->order_after_offloads(st);
     const StepGeom g = geom(c, 1, 1);  // fused full kernel: MHA split sizing
     const float* q32 = stage_q(c, 0, q, q_dtype, io_device, st);
     const uint64_t slots = c->batch * c->n_q;
@@ -1616,8 +1467,7 @@ int kc_v_arena_kind(const kc_cache* c, int* kind) {
 int kc_sync(kc_cache* c) {
   return guarded([&] {
     set_dev(c);
-    for (cudaStream_t s : {c->main_st, c->side_st, c->gather_st, c->out_st, c->in_st, c->gst_score, c->gst_sel,
-                           c->gst_rec})
+    for (cudaStream_t s : {c->main_st, c->side_st, c->out_st, c->in_st, c->off_st})
       if (s) CK(cudaStreamSynchronize(s));
     if (c->append_pending) CK(cudaEventSynchronize(c->ev_append));
   });
@@ -1629,7 +1479,6 @@ int kc_set_tuning(kc_cache* c, const char* key, int64_t value) {
     else if (k == "pipeline") c->pipeline = value ? 1 : 0;
     else if (k == "select_global") c->select_global = value ? 1 : 0;
     else if (k == "score_stages") c->score_stages = (int)value;
-    else if (k == "score_ctas_per_sm") c->score_ctas_per_sm = (int)value;
     else if (k == "recall_ctas") c->recall_ctas = (int)value;
     else if (k == "recall_pipe") c->recall_pipe = value < 0 ? -1 : (value ? 1 : 0);
     else if (k == "side_priority") {
@@ -1642,18 +1491,12 @@ int kc_set_tuning(kc_cache* c, const char* key, int64_t value) {
       CK(cudaStreamCreateWithPriority(&c->side_st, cudaStreamNonBlocking, value ? hi : lo));
     }
     else if (k == "keep_logits") c->keep_logits = value ? 1 : 0;
+    else if (k == "prefill_stage") c->prefill_stage = value ? 1 : 0;
+    else if (k == "group_first_pct") {
+      if (value < 0 || value > 100) fail(KC_EARG, "group_first_pct: 0..100");
+      c->group_first_pct = (int)value;
+    }
     else if (k == "full_fused") c->full_fused = value ? 1 : 0;
-    else if (k == "fuse_select") c->fuse_select = value ? 1 : 0;
-    else if (k == "pdl") c->pdl = value ? 1 : 0;
-    else if (k == "select_on_side") c->select_on_side = value ? 1 : 0;
-    else if (k == "green_flags") {
-      c->green_flags = (int)value;
-      c->green_sms = -1;  // rebuild the partition
-    }
-    else if (k == "score_sms") {
-      if (value < 0) fail(KC_EARG, "score_sms must be >= 0 (0 = no SM partition)");
-      c->score_sms = (int)value;
-    }
     else if (k == "select_cand") {
       if (value < 0 || value > 2) fail(KC_EARG, "select_cand: 0 auto, 1 on, 2 off");
       c->select_cand = (int)value;
@@ -1665,19 +1508,6 @@ int kc_set_tuning(kc_cache* c, const char* key, int64_t value) {
     else if (k == "score_groups") {
       if (value < 0) fail(KC_EARG, "score_groups must be >= 0 (0 = auto)");
       c->score_groups = (int)value;
-    }
-    else if (k == "host_frac_pct") {
-      if (value < 0 || value > 100) fail(KC_EARG, "host_frac_pct: 0..100");
-      c->host_frac_pct = (int)value;
-    } else if (k == "recall_mode") {
-      if (value < 0 || value > 3) fail(KC_EARG, "recall_mode: 0 auto, 1 zero-copy, 2 dma, 3 hybrid");
-      c->recall_mode = (int)value;
-    } else if (k == "gather_threads") {
-      if (c->main_st) cudaStreamSynchronize(c->main_st);
-      if (c->side_st) cudaStreamSynchronize(c->side_st);
-      if (c->gather_st) cudaStreamSynchronize(c->gather_st);
-      c->gather_threads = (int)value;
-      c->pool.reset();
     }
     else fail(KC_EARG, "unknown tuning key '" + k + "'");
   });

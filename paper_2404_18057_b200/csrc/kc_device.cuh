@@ -207,15 +207,7 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
   return m;
 }
 
-// Programmatic dependent launch: once every CTA of this grid has executed
-// this, a kernel launched after it with programmaticStreamSerialization may
-// start on the SMs this grid frees (the next layer's scoring, which reads
-// nothing this grid writes, overlaps the selection's last wave).
-__device__ __forceinline__ void allow_dependent_launch() {
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-}
-
-// ---- selection keys (kc_select.cu, kc_rowsel.cuh) ---------------------------
+// ---- selection keys (kc_select.cu) -------------------------------------------
 // Order-preserving bits of a float; -0.0 and +0.0 compare equal, so they must
 // tie (one key).
 __device__ __forceinline__ uint32_t ordered_bits(float x) {

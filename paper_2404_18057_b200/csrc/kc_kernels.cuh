@@ -29,7 +29,6 @@ struct ScoreParams {
   int max_splits;
   float scale;          // 1/sqrt(h) as the reference computes it
   int stages;           // TMA ring depth (4, 6 or 8 stages of 64 positions)
-  int ctas_per_sm;      // persistent grid = ctas_per_sm x SMs (0: one CTA per item)
   int row0;             // first row of this launch (row groups); rows = rows in this launch
   // candidate mode (MHA, h=128 16-bit fast path, cand_nc > 0): instead of the
   // dense logits, every split writes the positions that can still be in the
@@ -42,19 +41,7 @@ struct ScoreParams {
   int k_policy;         // L2 policy of the K stream (0 evict_first; see l2_policy)
   int use_mma;          // GQA (2 <= G <= 8): tensor-core scoring (score_mma_kernel)
   int tlb_ahead;        // rows ahead whose K translations the producer warms (0: off)
-  // fused selection (MHA dense path, one CTA per item; kc_rowsel.cuh): the
-  // last CTA to finish a row's splits selects the row's top sel_nc itself.
-  uint32_t* row_done;   // [rows] completion counters, zero between launches; nullptr: off
-  uint32_t* sel_idx;    // [rows][sel_nc]
-  float* sel_w;         // [rows][sel_nc]
-  double* sel_dropped;  // [rows]
-  float* sel_norm;      // [rows]
-  int sel_nc;
-  int keep_logits;      // 1: leave the dead logits in L2
-  int pdl;              // programmatic dependent launch behind the preceding selection
 };
-// Read `bytes` of a scratch buffer larger than L2: evicts (and so writes back)
-// every dirty L2 line, after which all stored K is clean in DRAM.
 // dtype: KC_F32 / KC_F16 / KC_BF16 (storage)
 void score_launch(const ScoreParams& p, int dtype, cudaStream_t st);
 // positions per CTA for a given shape (tuning override when > 0)
@@ -63,8 +50,6 @@ int score_pick_chunk(int s, int rows, int override_chunk, int G = 1);
 int sm_count();
 // whether the candidate-mode scoring kernel covers this shape
 bool score_cand_supported(int dtype, int h, int G, int chunk, int nc);
-// whether the scoring kernel can select the rows itself (ScoreParams::row_done)
-bool score_fused_select_supported(int dtype, int h, int G, int chunk, int nc, int ctas_per_sm);
 
 struct SelectParams {
   const float* logits;    // [batch][n_q][lstride]

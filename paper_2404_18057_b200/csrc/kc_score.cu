@@ -5,11 +5,10 @@
 //
 // Work items are (row, split): row = b*n_kv + kv_head, split = a chunk of
 // positions. A row's K for one split is one contiguous run of chunk*h
-// elements in the [b][kv][pos][h] arena. The kernel is persistent: a grid of
-// ctas_per_sm x 148 CTAs walks the items (item = blockIdx.x, +gridDim.x, ...),
-// so the TMA ring never drains between items and every SM keeps headroom for
-// the selection / recall kernels that run concurrently on the side stream.
-// In each CTA one elected producer lane streams K stages (64 positions = 16 KB)
+// elements in the [b][kv][pos][h] arena; one CTA per item (the hardware block
+// scheduler balances the items against the recall kernel that runs
+// concurrently on the side stream -- a persistent grid measured 20-25 %
+// slower). In each CTA one elected producer lane streams K stages (64 positions = 16 KB)
 // into a STAGES-deep shared-memory ring with 1-D TMA bulk copies
 // (cp.async.bulk, L2 evict-first) on mbarriers; eight consumer warps score
 // them against every q head of the GQA group held in registers (the K tile is
@@ -19,15 +18,12 @@
 // fp32, log2(LPR) xor-shuffles per row. Writes fp32 logits (score * scale, the
 // multiply after the sum like dot_scaled) and a per-split online (max, sum
 // exp) per q head; softmax_stats combines the splits into the global softmax.
-// As soon as a stage has landed the producer warp drops its K lines from L2
-// (produce_k below).
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 
 #include "kc_device.cuh"
 #include "kc_kernels.cuh"
-#include "kc_rowsel.cuh"
 #include "kcache_c.h"
 
 namespace kc {
@@ -182,7 +178,7 @@ __device__ __forceinline__ void emit_candidates(const float* scb, float* mx, uin
   if (ct == 0) *meta = make_uint2(tot, __float_as_uint(bound));
 }
 
-template <typename T, int G, int LPR, int STAGES, bool CAND, bool FUSE = false>
+template <typename T, int G, int LPR, int STAGES, bool CAND>
 __global__ void __launch_bounds__((kCWarps + 1) * 32, (G >= 2 ? 2 : KC_MHA_MINB))
     score_fast_kernel(const ScoreParams p) {
   constexpr int CPL = 16 / LPR;            // 16-B chunks per lane per row
@@ -339,32 +335,6 @@ __global__ void __launch_bounds__((kCWarps + 1) * 32, (G >= 2 ? 2 : KC_MHA_MINB)
       emit_candidates(scb, mx, wcnt, npos, p.cand_nc, pos0, p.cand + (size_t)row * p.lstride + pos0,
                       p.cand_meta + (size_t)row * p.max_splits + split);
     named_sync(1, kCWarps * 32);  // red / scb are reused by the next item
-    if constexpr (FUSE) {
-      static_assert(G == 1 && !CAND, "fused selection: MHA dense rows");
-      // fused selection: the CTA that completes the row's last split selects
-      // the row (kc_rowsel.cuh) in its now idle ring while the others stream
-      {
-        __shared__ uint32_t s_last;
-        // the barrier orders every thread's logits / partials before thread
-        // 0's release fence (cumulative), which orders them before the count
-        named_sync(1, kCWarps * 32);
-        if (threadIdx.x == 0) {
-          __threadfence();
-          s_last = atomicAdd(&p.row_done[row], 1u) == (uint32_t)(p.n_splits - 1);
-          if (s_last) __threadfence();  // acquire: the other splits' writes
-        }
-        named_sync(1, kCWarps * 32);
-        if (s_last) {
-          constexpr int kRingBytes = STAGES * kRows * ROWB;
-          constexpr int cap = (kRingBytes - rowsel::kSharedBytes) / 8 < 4096 ? (kRingBytes - rowsel::kSharedBytes) / 8 : 4096;
-          const rowsel::RowOut ro{p.sel_idx + (size_t)row * p.sel_nc, p.sel_w + (size_t)row * p.sel_nc,
-                                  p.sel_dropped + row, p.sel_norm + row};
-          rowsel::select_row(ring, cap, p.logits + (size_t)row * p.lstride, p.partials + (size_t)row * p.max_splits,
-                             p.n_splits, p.s, p.sel_nc, ro, p.keep_logits != 0);
-          if (threadIdx.x == 0) p.row_done[row] = 0u;  // ready for the next launch
-        }
-      }
-    }
   }
 }
 
@@ -894,24 +864,6 @@ int num_sms() {
   return n[dev & 63] > 0 ? n[dev & 63] : 148;
 }
 
-// Scoring launch; with p.pdl the kernel may start while the preceding kernel
-// in the stream (a selection: allow_dependent_launch) is still running -- the
-// caller guarantees it reads nothing that kernel writes.
-template <typename K>
-void launch_score(K kern, int grid, int block, size_t smem, cudaStream_t st, const ScoreParams& p) {
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3((unsigned)grid);
-  cfg.blockDim = dim3((unsigned)block);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = p.pdl ? 1 : 0;
-  cudaLaunchKernelEx(&cfg, kern, p);
-}
-
 template <typename T, int G, int LPR, int STAGES, bool CAND>
 void launch_fast_s(const ScoreParams& p, cudaStream_t st) {
   constexpr int ROWB = kH * (int)sizeof(T);
@@ -927,21 +879,7 @@ void launch_fast_s(const ScoreParams& p, cudaStream_t st) {
     configured |= 1ull << (dev & 63);
   }
   const int n_items = p.rows * p.n_splits;
-  const int per_sm = p.ctas_per_sm > 0 ? p.ctas_per_sm : 1 << 20;  // 0: one CTA per item
-  const int grid = (int)std::min<long long>(n_items, (long long)per_sm * num_sms());
-  if constexpr (G == 1 && !CAND) {
-    if (p.row_done) {  // fused selection (its own instantiation: the plain kernel keeps its registers)
-      static unsigned long long configured_f = 0;
-      if (!(configured_f >> (dev & 63) & 1ull)) {
-        cudaFuncSetAttribute(score_fast_kernel<T, G, LPR, STAGES, false, true>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        configured_f |= 1ull << (dev & 63);
-      }
-      launch_score(score_fast_kernel<T, G, LPR, STAGES, false, true>, n_items, (kCWarps + 1) * 32, smem, st, p);
-      return;
-    }
-  }
-  launch_score(score_fast_kernel<T, G, LPR, STAGES, CAND>, grid, (kCWarps + 1) * 32, smem, st, p);
+  score_fast_kernel<T, G, LPR, STAGES, CAND><<<n_items, (kCWarps + 1) * 32, smem, st>>>(p);
 }
 
 template <typename T, int G, int LPR, bool CAND>
@@ -968,9 +906,7 @@ void launch_mma_s(const ScoreParams& p, cudaStream_t st) {
     configured |= 1ull << (dev & 63);
   }
   const int n_items = p.rows * p.n_splits;
-  const int per_sm = p.ctas_per_sm > 0 ? p.ctas_per_sm : 1 << 20;
-  const int grid = (int)std::min<long long>(n_items, (long long)per_sm * num_sms());
-  launch_score(score_mma_kernel<T, STAGES, NCW>, grid, (NCW + 1) * 32, smem, st, p);
+  score_mma_kernel<T, STAGES, NCW><<<n_items, (NCW + 1) * 32, smem, st>>>(p);
 }
 
 template <typename T>
@@ -1034,12 +970,6 @@ bool full_fast_launch(const FullParams& p, int dtype, cudaStream_t st) {
   return false;
 }
 
-bool score_fused_select_supported(int dtype, int h, int G, int chunk, int nc, int ctas_per_sm) {
-  // one CTA per item (the ring is idle after it), MHA 16-bit fast path, the
-  // selection's warp-local bound (N <= 256)
-  return (dtype == KC_F16 || dtype == KC_BF16) && h == kH && G == 1 && chunk % kRows == 0 && nc >= 1 &&
-         nc <= rowsel::kMaxNc && ctas_per_sm == 0;
-}
 
 bool score_cand_supported(int dtype, int h, int G, int chunk, int nc) {
   // nc <= 128: the bound is the nc-th largest of the 256 consumer threads'

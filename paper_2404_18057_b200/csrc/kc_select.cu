@@ -295,7 +295,6 @@ __device__ __forceinline__ void drop_rows(const float* base, int64_t stride, int
 template <int KPT>
 __device__ __forceinline__ void select_reg_body(const SelectParams& p) {
   __shared__ SelShared S;
-  allow_dependent_launch();
   const int row = p.row0 + blockIdx.x;
   if (!fallback_prologue(p, row)) return;
   const int b = row / p.n_kv;
@@ -558,7 +557,6 @@ __global__ void __launch_bounds__(kT, 1) select_reg_kernel(const SelectParams p)
 // Any length: keys in a global scratch row (L2-resident), same rule.
 __global__ void __launch_bounds__(kT) select_kernel(const SelectParams p) {
   __shared__ SelShared S;
-  allow_dependent_launch();
   const int row = p.row0 + blockIdx.x;
   if (!fallback_prologue(p, row)) return;
   const int b = row / p.n_kv;
@@ -826,7 +824,6 @@ constexpr int kCandKPT = 16;  // up to 16384 candidates per row
 __global__ void __launch_bounds__(kT, 1) select_cand_kernel(const SelectParams p) {
   __shared__ SelShared S;
   extern __shared__ uint2 csm[];  // [kT * kCandKPT] candidates, then prefix[n_splits + 1]
-  allow_dependent_launch();
   uint32_t* pre = reinterpret_cast<uint32_t*>(csm + kT * kCandKPT);
   const int row = p.row0 + blockIdx.x;
   const int b = row / p.n_kv;

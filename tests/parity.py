@@ -7,7 +7,12 @@
 * outputs |out - ref| <= atol + OUT_RTOL*|ref| with atol = 1e-6*max|V|*sum(p_sel)
   (raw) or 1e-5*max|V| (renormalised), ref recomputed in fp64 over the GPU's own
   index set with the oracle's probabilities (so a legal boundary swap does not
-  count twice);
+  count twice). When the caller passes the group's logit magnitude
+  L1 = scale * max_j sum_i |q_i k_ji| (large for peaked rows: ~60 for keys of
+  6-8 against q in [0.5, 1]), atol grows by LOGIT_C * 2^-24 * sqrt(h) * L1 *
+  max|V| * sum(p_sel): an fp32 dot of that magnitude summed in another order
+  differs by ~u*sqrt(h)*L1 in the logit, which moves every p by that relative
+  amount -- visible where the output cancels to ~0;
 * ledger bytes exact.
 """
 import numpy as np
@@ -16,6 +21,7 @@ EPS_KEY = 1e-5
 W_RTOL = 1e-4
 DROP_ATOL = 1e-6
 OUT_RTOL = 1e-3
+LOGIT_C = 4.0
 
 
 def softmax_rows(q, kslot, h):
@@ -26,7 +32,7 @@ def softmax_rows(q, kslot, h):
 
 
 def check_group(gpu_idx, gpu_w, gpu_dropped, gpu_out, probs, vslot, top_n, renormalize, ora_idx=None,
-                ora_w=None, ora_dropped=None, ora_out=None):
+                ora_w=None, ora_dropped=None, ora_out=None, logit_mag=0.0):
     """One (batch, kv head) group. probs [G][s] oracle fp32 probabilities,
     vslot [s][h]. gpu_* for the G q heads: idx [nc] (shared), w [G][nc],
     dropped [G], out [G][h]."""
@@ -53,10 +59,12 @@ def check_group(gpu_idx, gpu_w, gpu_dropped, gpu_out, probs, vslot, top_n, renor
         ref = wsel @ v
         vmax = float(np.abs(vslot).max()) if vslot.size else 0.0
         atol = 1e-5 * vmax if renormalize else 1e-6 * vmax * pw.sum()
+        atol += LOGIT_C * 2.0**-24 * np.sqrt(vslot.shape[1]) * logit_mag * vmax * (1.0 if renormalize else pw.sum())
         atol = max(atol, 1e-7)
         err = np.abs(gpu_out[g].astype(np.float64) - ref)
         bound = atol + OUT_RTOL * np.abs(ref)
-        assert np.all(err <= bound), f"head {g}: max err {err.max()} vs bound {bound[err.argmax()]}"
+        worst = int(np.argmax(err - bound))
+        assert np.all(err <= bound), f"head {g}: err {err[worst]} vs bound {bound[worst]} (ref {ref[worst]})"
         if ora_out is not None and diff.size == 0:
             err2 = np.abs(gpu_out[g].astype(np.float64) - ora_out[g].astype(np.float64))
             assert np.all(err2 <= atol + OUT_RTOL * np.abs(ora_out[g])), f"head {g}: vs oracle {err2.max()}"

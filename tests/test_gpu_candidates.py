@@ -16,8 +16,8 @@ from tests.test_gpu_parity import build_cache, compare_all
 
 pytestmark = pytest.mark.gpu
 
-DEFAULTS = {"select_cand": 0, "cand_force_fallback": 0, "score_groups": 0, "recall_mode": 0, "score_chunk": 0,
-            "recall_pipe": -1, "score_mma": 1, "recall_ctas": 32, "select_on_side": 0, "tlb_ahead": -1, "fuse_select": 0, "pdl": 0, "score_sms": 0}
+DEFAULTS = {"select_cand": 0, "cand_force_fallback": 0, "score_groups": 0, "score_chunk": 0,
+            "recall_pipe": -1, "score_mma": 1, "recall_ctas": 32, "tlb_ahead": -1}
 
 
 def _run(kc, cache, q, N, renorm=False, **tune):
@@ -59,10 +59,8 @@ def test_candidates_equal_dense_bitwise(kc, oracle, case):
         cand = _run(kc, cache, q, N, renorm)
         dense = _run(kc, cache, q, N, renorm, select_cand=2)
         redo = _run(kc, cache, q, N, renorm, cand_force_fallback=1)
-        fused = _run(kc, cache, q, N, renorm, select_cand=2, fuse_select=1)
         _assert_same(cand, dense)
         _assert_same(redo, dense)
-        _assert_same(fused, dense)  # selection fused into scoring == its own kernel
     if s <= 5000:
         compare_all(oracle, cand, q, ks[0], vs[0], b, n, n, h, s, N, True)
 
@@ -84,7 +82,6 @@ def test_tie_flood_selects_lowest_positions(kc, oracle):
     np.testing.assert_array_equal(res.selection.indices, np.tile(np.arange(N, dtype=np.uint32), (b * n, 1)))
     dense = _run(kc, cache, q, N, select_cand=2)
     _assert_same(res, dense)
-    _assert_same(res, _run(kc, cache, q, N, select_cand=2, fuse_select=1))
     cache.close()
 
 
@@ -112,24 +109,23 @@ def test_underflow_ties_take_lowest_positions(kc, oracle):
         np.testing.assert_array_equal(o_idx[slot], want)
         np.testing.assert_array_equal(res.selection.indices[slot], want)
     _assert_same(res, _run(kc, cache, q, N, select_cand=2))
-    _assert_same(res, _run(kc, cache, q, N, select_cand=2, fuse_select=1))
     cache.close()
 
 
-@pytest.mark.parametrize("tune", [dict(score_groups=2), dict(score_groups=5), dict(recall_mode=2),
-                                  dict(recall_mode=3), dict(select_cand=1), dict(select_cand=1, score_groups=3),
-                                  dict(recall_pipe=1), dict(recall_pipe=1, recall_ctas=0), dict(recall_pipe=0), dict(select_on_side=1),
-                                  dict(tlb_ahead=0), dict(score_chunk=4096), dict(fuse_select=1),
-                                  dict(fuse_select=1, score_groups=2), dict(pdl=1), dict(pdl=1, score_groups=2),
-                                  dict(score_sms=120), dict(score_sms=64, score_groups=2)],
-                         ids=["groups2", "groups5", "dma", "hybrid", "cand", "cand-groups3", "recall-pipe",
-                              "recall-pipe-per-row", "recall-plain", "side-select", "no-tlb-warm", "chunk4096", "fused-select",
-                                  "fused-select-groups2", "pdl", "pdl-groups2", "sm-partition", "sm-partition-groups2"])
+VARIANTS = {
+    "groups2": dict(score_groups=2), "groups5": dict(score_groups=5), "cand": dict(select_cand=1),
+    "cand-groups3": dict(select_cand=1, score_groups=3), "recall-pipe": dict(recall_pipe=1),
+    "recall-pipe-per-row": dict(recall_pipe=1, recall_ctas=0), "recall-plain": dict(recall_pipe=0),
+    "recall-ctas128": dict(recall_ctas=128), "no-tlb-warm": dict(tlb_ahead=0), "chunk4096": dict(score_chunk=4096),
+}
+
+
+@pytest.mark.parametrize("tune", list(VARIANTS.values()), ids=list(VARIANTS))
 @pytest.mark.parametrize("n_kv", [8, 2], ids=["mha", "gqa4"])
 def test_pipeline_variants_bitwise(kc, tune, n_kv):
-    """Row groups, host-gather DMA recall, the hybrid recall and candidate
-    selection reproduce the default path bit for bit; another split length
-    changes only the rounding of the softmax statistics."""
+    """Row groups, the recall variants and candidate selection reproduce the
+    default path bit for bit; another split length changes only the rounding
+    of the softmax statistics."""
     b, n, h, s, N, L = 2, 8, 128, 3000, 64, 7  # L > kRing (3): ring slots are reused
     if n_kv != n and "select_cand" in tune:
         pytest.skip("candidate selection is MHA-only")

@@ -161,15 +161,12 @@ def test_prepared_host_call_pinned_and_pageable(kc):
             assert info[l] == (nc, 2 * b * n_kv * nc * h)
 
 
-@pytest.mark.parametrize("recall_mode", [0, 1])
-def test_repeated_decode_and_decode_appends(kc, oracle, recall_mode):
-    """Decode is idempotent across calls (the scoring kernel drops consumed,
-    clean K lines from L2 -- it must never lose data), and K/V appended in the
+def test_repeated_decode_and_decode_appends(kc, oracle):
+    """Decode is idempotent across calls, and K/V appended in the
     decode phase (engine.cpp:143: append before attention) are scored and
     recalled; the appended V goes to the host arena with a D2H ledger event."""
     b, n, n_kv, h, s, N = 2, 8, 4, 128, 700, 64
     cache, ks, vs = build_cache(kc, b, n, n_kv, h, s, "f16", max_seq=s + 8)
-    cache.set_tuning("recall_mode", recall_mode)
     q = synth_matrix(1, b, n * h)
     first = kc.decode_attention_topn(q, cache, 0, N, False)
     for _ in range(4):
@@ -313,3 +310,54 @@ def test_long_rows_global_key_selection(kc, oracle, case):
     res = kc.decode_attention_topn(q, cache, 0, N, False)
     compare_all(oracle, res, q, ks[0], vs[0], b, n, n_kv, h, s, N, False)
     cache.close()
+
+
+@pytest.mark.parametrize("order", ["engine", "all-appends-first"])
+def test_prefill_staged_offload_equals_mapped_stores(kc, order):
+    """Prefill V of offloaded layers through the HBM stages + copy-engine D2H
+    (prefill_stage 1) vs straight mapped stores (prefill_stage 0): rows read
+    back before and after offload_prefill_v, the ledger, and the decode
+    results are identical. "all-appends-first" appends every layer before the
+    first offload, so layers beyond the two stages take the direct path."""
+    b, n, n_kv, h, s, N, L = 2, 8, 4, 128, 900, 64, 4
+    ks = [synth_matrix(2 + 100 * l, s * b, n_kv * h) for l in range(L)]
+    vs = [synth_matrix(3 + 100 * l, s * b, n_kv * h) for l in range(L)]
+    q = synth_matrix(1, b, n * h)
+    results = []
+    for stage in (0, 1):
+        cfg = kc.small_config(L, n * h, n, s, kv_heads=n_kv)
+        cache = kc.TieredKVCache(cfg, b, kc.TierPlacement.kcache(1, L, 2, "f16"))
+        cache.set_tuning("prefill_stage", stage)
+
+        def append(l):
+            for c0 in range(0, s, 300):
+                cache.append_kv(l, ks[l][c0 * b:(c0 + 300) * b], vs[l][c0 * b:(c0 + 300) * b])
+            np.testing.assert_array_equal(cache.v_row(l, s - 1, 1), vs[l][(s - 1) * b + 1])
+
+        if order == "engine":
+            for l in range(L):
+                append(l)
+                cache.offload_prefill_v(l)
+                np.testing.assert_array_equal(cache.v_row(l, 7, 0), vs[l][7 * b])
+        else:
+            for l in range(L):
+                append(l)
+            for l in range(L):
+                cache.offload_prefill_v(l)
+        cache.begin_decode()
+        got = [kc.decode_attention_topn(q, cache, l, N, False) for l in range(L)]
+        sel = [[0, 5, s - 1]] * (b * n)
+        gv = cache.gather_v(L - 1, sel)
+        for slot in range(b * n):
+            bb, hd = divmod(slot, n)
+            kvh = hd // (n // n_kv)
+            want = vs[L - 1][np.array(sel[slot]) * b + bb][:, kvh * h:(kvh + 1) * h]
+            np.testing.assert_array_equal(np.asarray(gv.blocks[slot]).reshape(3, h), want)
+        results.append((got, cache.ledger_jsonl()))
+        cache.close()
+    (a, la), (c, lc) = results
+    assert la == lc
+    for x, y in zip(a, c):
+        np.testing.assert_array_equal(x.out, y.out)
+        np.testing.assert_array_equal(x.selection.indices, y.selection.indices)
+        np.testing.assert_array_equal(x.selection.dropped_mass, y.selection.dropped_mass)
