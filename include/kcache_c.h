@@ -222,6 +222,11 @@ int kc_profile_launch(kc_cache* cache, const char* kernel, uint64_t i, double* m
 /* start / end of launch i in ms since the first profiled event (timelines) */
 int kc_profile_span(kc_cache* cache, const char* kernel, uint64_t i, double* t0, double* t1);
 
+/* Development probes (not part of the reference interface): "consume" copies
+ * the dataflow consumer's per-row phase timestamps ([rows][8] u64 ns; tuning
+ * consume_dbg 1) of the last decode call. */
+int kc_debug_read(kc_cache* cache, const char* what, void* out, uint64_t bytes);
+
 /* The split length (positions per scoring work item) the store picks on its
  * own ("score_chunk" 0) for s positions over `rows` (batch x kv head) rows of
  * GQA group `group`. Setting it explicitly on a cache holding a subset of the

@@ -163,6 +163,16 @@ struct kc_cache {
   int64_t lstride = 0, kstride = 0;
   int max_splits = 0;
   DevBuf logits, partials, keys, part_out, stage_src, stage_k, stage_v, sel_rows, sel_pos, gather_out;
+  // dataflow path (kc_consume.cu): a second scoring buffer (slot 1; slot 0 is
+  // logits/partials above), per-row split counters per slot, the consumer's
+  // error word, and "slot s is free" events
+  DevBuf logits_b, partials_b, row_done[2], cons_err;
+  cudaEvent_t ev_cons[2] = {}, ev_scored = nullptr;
+  bool cons_pending[2] = {};
+  bool cons_dirty = false;   // a scoring launch signalled rows no consumer read
+  uint64_t cons_seq = 0;     // layers scored on the dataflow path (slot = seq & 1)
+  float* logits_slot(int ls) const { return ls ? logits_b.as<float>() : logits.as<float>(); }
+  float2* partials_slot(int ls) const { return ls ? partials_b.as<float2>() : partials.as<float2>(); }
   DevBuf cand, cand_meta, fb_flags;  // candidate-mode selection scratch
   DevBuf part_ml;                    // fused full attention: split (m, l)
   DevBuf step_dev;                   // kc_decode_step: StepStatsDev accumulator
@@ -238,6 +248,19 @@ struct kc_cache {
   int recall_pipe = -1;   // software-pipelined recall kernel: -1 auto = GQA only (r01, managed
                           // arena: C3 8.35 -> 7.9 ms per step; MHA C2 no gain)
   int recall_ctas = 32;  // CTAs of the recall kernel (0: one per (batch, kv head)); 32 measured best at C2
+  // dataflow consumer (selection + recall + P.V per row as the scoring
+  // completes it, kc_consume.cu): 1 on, 0 the stream-ordered select + recall
+  //   1 (default) MHA only: GQA keys need the 4 heads' exp per position twice
+  //   per row, which the consumer cannot hide behind the shorter GQA scoring
+  //   (C3: 329 vs 241 us per layer), 2 every supported shape
+  int consume = 1;
+  // persistent consumer CTAs; 0 auto: 64 for multi-layer calls (C2 pipelined
+  // 338 vs 376 us per layer at 48), 40 for single-layer calls (the engine's
+  // layer-by-layer step: 372 vs 425 us at 64 -- fewer CTAs queue fewer PCIe
+  // reads ahead of the last rows')
+  int consume_ctas = 0;
+  int consume_dbg = 0;    // development probe: consumer phase timestamps (kc_debug_read "consume")
+  DevBuf cons_dbg;
   // per-kernel CUDA-event timing (kc_profile): [kind] -> (start, stop) pairs
   bool prof_on = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof[3];
@@ -414,6 +437,10 @@ void destroy(kc_cache* c) {
   }
   for (void* p : c->v_managed) cudaFree(p);
   c->v_managed.clear();
+  for (DevBuf* b : {&c->logits_b, &c->partials_b, &c->row_done[0], &c->row_done[1], &c->cons_err}) b->release();
+  for (int i = 0; i < 2; ++i)
+    if (c->ev_cons[i]) cudaEventDestroy(c->ev_cons[i]);
+  if (c->ev_scored) cudaEventDestroy(c->ev_scored);
   for (DevBuf* b : {&c->logits, &c->partials, &c->keys, &c->part_out, &c->stage_src, &c->stage_k,
                     &c->stage_v, &c->sel_rows, &c->sel_pos, &c->gather_out, &c->cand, &c->cand_meta,
                     &c->fb_flags, &c->part_ml, &c->step_dev})
@@ -541,9 +568,10 @@ StepGeom geom(kc_cache* c, uint64_t top_n, int chunk_g = -1) {
 }
 
 void enqueue_score(kc_cache* c, uint64_t layer, const float* q32, const StepGeom& g, cudaStream_t st,
-                   int row0, int nrows, bool cand = false) {
+                   int row0, int nrows, bool cand = false, int ls = 0, uint32_t* row_done = nullptr) {
   kc::ScoreParams sp{};
   sp.row0 = row0;
+  sp.row_done = row_done;
   if (cand) {
     sp.cand = c->cand.as<uint2>();
     sp.cand_meta = c->cand_meta.as<uint2>();
@@ -551,8 +579,8 @@ void enqueue_score(kc_cache* c, uint64_t layer, const float* q32, const StepGeom
   }
   sp.k = c->k_layer(layer);
   sp.q = q32;
-  sp.logits = c->logits.as<float>();
-  sp.partials = c->partials.as<float2>();
+  sp.logits = c->logits_slot(ls);
+  sp.partials = c->partials_slot(ls);
   sp.max_seq = (int64_t)c->cfg.max_seq;
   sp.lstride = c->lstride;
   sp.s = g.s;
@@ -692,6 +720,85 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
     const float* q32 = q_all ? q_all + i * (c->batch * c->n_q * c->h)
                              : stage_q(c, slot, q[i], q_dtype, io_device, st, i, n);
     kc_topn_out& o = outs[i];
+    // Dataflow (default): the scoring kernel signals each (batch, kv head) row
+    // as its splits complete and a persistent consumer grid on the side stream
+    // selects, recalls and reduces the row meanwhile (kc_consume.cu) -- the
+    // scoring stream carries nothing but scoring. Scoring buffers alternate
+    // between two slots so layer i+1's scoring never waits for layer i's
+    // consumer; layer i+2's waits for it (ev_cons).
+    const bool flow = (c->consume == 2 || (c->consume == 1 && c->G == 1)) &&
+                      kc::consume_supported((int)c->G, (int)c->h) && !c->select_global && c->select_cand != 1;
+    if (flow) {
+      const int ls = (int)(c->cons_seq & 1);
+      const int rows_i = (int)c->rows;
+      if (ls == 1) {
+        c->logits_b.ensure(c->logits.bytes);
+        c->partials_b.ensure(c->partials.bytes);
+      }
+      for (DevBuf* b : {&c->row_done[ls], &c->cons_err}) {
+        const size_t want = b == &c->cons_err ? 4 : c->rows * 4 * kc::kRowDoneStride;
+        if (b->bytes < want) {
+          b->ensure(want);
+          CK(cudaMemsetAsync(b->p, 0, b->bytes, st));
+        }
+      }
+      if (c->cons_dirty) {  // an earlier call threw between a scoring launch and its consumer
+        for (int k = 0; k < 2; ++k)
+          if (c->row_done[k].p) CK(cudaMemsetAsync(c->row_done[k].p, 0, c->row_done[k].bytes, st));
+        c->cons_dirty = false;
+      }
+      if (c->cons_pending[ls]) CK(cudaStreamWaitEvent(st, c->ev_cons[ls], 0));
+      c->cons_dirty = true;
+      enqueue_score(c, layer, q32, g, st, 0, rows_i, false, ls, c->row_done[ls].as<uint32_t>());
+      cudaStream_t cs = side;
+      if (cs != st) {
+        // ring slot `slot` is rewritten: the output copies of layer i-kRing must be done
+        if (i >= (uint64_t)kRing) {
+          CK(cudaStreamWaitEvent(cs, c->ev_rec[slot], 0));
+          if (c->cp_pending[slot]) CK(cudaStreamWaitEvent(cs, c->ev_cp[slot], 0));
+        }
+        if (c->capture_st) {  // inside a graph the consumer follows the scoring (no spinning node)
+          CK(cudaEventRecord(c->ev_scored, st));
+          CK(cudaStreamWaitEvent(cs, c->ev_scored, 0));
+        }
+      }
+      kc::ConsumeParams cp{};
+      cp.logits = c->logits_slot(ls);
+      cp.partials = c->partials_slot(ls);
+      cp.idx = c->idx[slot].as<uint32_t>();
+      cp.w = c->w[slot].as<float>();
+      cp.dropped = c->dropped[slot].as<double>();
+      cp.norm = c->norm[slot].as<float>();
+      cp.lstride = c->lstride;
+      cp.s = g.s;
+      cp.nc = g.nc;
+      cp.n_kv = (int)c->n_kv;
+      cp.G = (int)c->G;
+      cp.n_splits = g.n_splits;
+      cp.max_splits = c->max_splits;
+      cp.row0 = 0;
+      cp.rows = rows_i;
+      cp.keep_logits = c->keep_logits;
+      cp.v = c->v_layer(layer);
+      cp.out = io_device ? o.out : c->out_tmp[slot].as<float>();
+      cp.max_seq = (int64_t)c->cfg.max_seq;
+      cp.h = (int)c->h;
+      cp.renormalize = (flags & KC_RENORMALIZE) ? 1 : 0;
+      cp.reverse = (flags & KC_REVERSE_ACCUM) ? 1 : 0;
+      cp.row_done = c->row_done[ls].as<uint32_t>();
+      cp.err = c->cons_err.as<uint32_t>();
+      if (c->consume_dbg) {
+        c->cons_dbg.ensure(c->rows * 8 * sizeof(uint64_t));
+        cp.dbg = c->cons_dbg.as<uint64_t>();
+      }
+      const int ctas = c->consume_ctas > 0 ? c->consume_ctas : (n == 1 ? 40 : 64);
+      c->timed(1, cs, [&] { kc::consume_launch(cp, c->dtype, ctas, cs); });
+      c->cons_dirty = false;
+      ++c->cons_seq;
+      CK(cudaEventRecord(c->ev_cons[ls], cs));
+      c->cons_pending[ls] = true;
+      CK(cudaEventRecord(c->ev_sel[slot], cs));
+    } else {
     // Row groups: score -> select -> recall per group of (batch, kv head)
     // rows, so the recall of group g overlaps the scoring of group g+1.
     // score_groups 0 = auto: one group when layers pipeline against each
@@ -793,6 +900,7 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
       rp.row_offset = r0;
       c->timed(2, side, [&] { kc::recall_launch(rp, c->dtype, side); });
     }
+    }  // stream-ordered path
 
     // device mode: the selection outputs depend on the selection only --
     // expand + copy them on their own stream so the side stream runs nothing
@@ -968,6 +1076,8 @@ int kc_cache_create(const kc_config* cfg, uint64_t batch, uint64_t resident_laye
       CK(cudaEventCreateWithFlags(&c->ev_end, cudaEventDisableTiming));
       CK(cudaEventCreateWithFlags(&c->ev_stats, cudaEventDisableTiming));
       CK(cudaEventCreateWithFlags(&c->ev_append, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&c->ev_scored, cudaEventDisableTiming));
+      for (int i = 0; i < 2; ++i) CK(cudaEventCreateWithFlags(&c->ev_cons[i], cudaEventDisableTiming));
       for (int i = 0; i < kRing; ++i) {
         CK(cudaEventCreateWithFlags(&c->ev_sel[i], cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&c->ev_out[i], cudaEventDisableTiming));
@@ -1163,6 +1273,16 @@ void prepare_step_buffers(kc_cache* c, uint64_t top_n, cudaStream_t st) {
     c->step_dev.ensure(sizeof(kc::StepStatsDev));
     CK(cudaMemsetAsync(c->step_dev.p, 0, sizeof(kc::StepStatsDev), st));
   }
+  // dataflow path: both scoring slots, the row counters and the error word
+  c->logits_b.ensure(c->logits.bytes);
+  c->partials_b.ensure(c->partials.bytes);
+  for (DevBuf* b : {&c->row_done[0], &c->row_done[1], &c->cons_err}) {
+    const size_t want = b == &c->cons_err ? 4 : c->rows * 4 * kc::kRowDoneStride;
+    if (b->bytes < want) {
+      b->ensure(want);
+      CK(cudaMemsetAsync(b->p, 0, b->bytes, st));
+    }
+  }
   if (c->L > 0) {  // full attention on the V-resident layers
     c->part_out.ensure(checked_mul({slots, (uint64_t)c->max_splits, c->h, 4}));
     c->part_ml.ensure(checked_mul({slots, (uint64_t)c->max_splits, 8}));
@@ -1180,6 +1300,10 @@ int kc_step_graph_begin(kc_cache* c, uint64_t top_n, void* stream) {
     // have to order against (their events would cross the capture boundary)
     CK(cudaStreamSynchronize(c->side_st));
     CK(cudaStreamSynchronize(c->out_st));
+    // everything before the capture is complete: the dataflow slot events
+    // recorded outside it must not be waited on inside it
+    CK(cudaStreamSynchronize(c->main_st));
+    c->cons_pending[0] = c->cons_pending[1] = false;
     CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
     c->capture_st = st;
   });
@@ -1505,6 +1629,18 @@ int kc_set_tuning(kc_cache* c, const char* key, int64_t value) {
     else if (k == "tlb_ahead") c->tlb_ahead = (int)value;
     else if (k == "score_mma") c->score_mma = (int)std::max<int64_t>(0, std::min<int64_t>(2, value));
     else if (k == "cand_force_fallback") c->cand_force_fallback = value ? 1 : 0;
+    else if (k == "consume") {
+      if (value < 0 || value > 2) fail(KC_EARG, "consume: 0 off, 1 MHA, 2 every supported shape");
+      c->consume = (int)value;
+    }
+
+
+
+    else if (k == "consume_dbg") c->consume_dbg = value ? 1 : 0;
+    else if (k == "consume_ctas") {
+      if (value < 0) fail(KC_EARG, "consume_ctas must be >= 0 (0 = auto)");
+      c->consume_ctas = (int)value;
+    }
     else if (k == "score_groups") {
       if (value < 0) fail(KC_EARG, "score_groups must be >= 0 (0 = auto)");
       c->score_groups = (int)value;
@@ -1570,6 +1706,19 @@ int kc_profile_launch(kc_cache* c, const char* kernel, uint64_t i, double* ms) {
     float t = 0.0f;
     CK(cudaEventElapsedTime(&t, c->prof[kind][i].first, c->prof[kind][i].second));
     *ms = t;
+  });
+}
+
+int kc_debug_read(kc_cache* c, const char* what, void* out, uint64_t bytes) {
+  return guarded([&] {
+    const std::string w = what ? what : "";
+    const DevBuf* src = w == "consume" ? &c->cons_dbg : w == "logits0" ? &c->logits : w == "logits1" ? &c->logits_b
+                                                                                      : nullptr;
+    if (!src || !out) fail(KC_EARG, "kc_debug_read: unknown probe");
+    set_dev(c);
+    CK(cudaDeviceSynchronize());
+    if (!src->p) fail(KC_ESTATE, "kc_debug_read: probe buffer not allocated");
+    CK(cudaMemcpy(out, src->p, std::min<uint64_t>(bytes, src->bytes), cudaMemcpyDeviceToHost));
   });
 }
 

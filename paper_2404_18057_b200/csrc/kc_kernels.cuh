@@ -41,7 +41,12 @@ struct ScoreParams {
   int k_policy;         // L2 policy of the K stream (0 evict_first; see l2_policy)
   int use_mma;          // GQA (2 <= G <= 8): tensor-core scoring (score_mma_kernel)
   int tlb_ahead;        // rows ahead whose K translations the producer warms (0: off)
+  // dataflow (consume_launch): every CTA bumps row_done[row] (release) once
+  // its split's logits and statistics are written; null: no signalling
+  uint32_t* row_done;
 };
+// row_done counters: one per kRowDoneStride words (a 128-B line per row)
+constexpr int kRowDoneStride = 32;
 // dtype: KC_F32 / KC_F16 / KC_BF16 (storage)
 void score_launch(const ScoreParams& p, int dtype, cudaStream_t st);
 // positions per CTA for a given shape (tuning override when > 0)
@@ -93,6 +98,41 @@ constexpr int kDenseRegMaxS = 32 * 1024;
 // candidate-mode selection (MHA, fast scoring path) + the dense redo of any
 // row it flags; returns false when the shape is outside candidate mode
 bool select_cand_launch(const SelectParams& p, cudaStream_t st);
+
+// Dataflow consumer (kc_consume.cu): a persistent grid that, row by row as
+// the scoring kernel completes them (row_done[row] == n_splits), runs the
+// selection, the V recall and P.V of the row -- bit-identical to
+// select_launch + recall_launch -- while the scoring streams later rows.
+struct ConsumeParams {
+  const float* logits;     // [batch][n_q][lstride]
+  const float2* partials;  // [batch][n_q][max_splits]
+  uint32_t* idx;           // [rows][nc]
+  float* w;                // [batch*n_q][nc]
+  double* dropped;         // [batch*n_q]
+  float* norm;             // [batch*n_q]
+  int64_t lstride;
+  int s;
+  int nc;
+  int n_kv;
+  int G;
+  int n_splits;
+  int max_splits;
+  int row0;
+  int rows;
+  int keep_logits;
+  const void* v;           // layer's V [rows][max_seq][h] (device or mapped host); null: select only
+  float* out;              // [batch][n_q*h]
+  int64_t max_seq;
+  int h;
+  int renormalize;
+  int reverse;
+  uint32_t* row_done;      // [rows][kRowDoneStride] split completion counters; null: rows are complete
+  uint32_t* err;           // set before trapping on a row that never completes
+  uint64_t* dbg;           // development probe: [rows][8] phase timestamps (ns), or null
+};
+bool consume_supported(int G, int h);
+// grid: persistent CTAs (<= rows); vdtype: V storage dtype
+void consume_launch(const ConsumeParams& p, int vdtype, int grid, cudaStream_t st);
 
 // p = exp(s - M)/Z for every position of every (batch, q head) -> probs
 // [batch*n_q][s] (ScoreObserver debug path).

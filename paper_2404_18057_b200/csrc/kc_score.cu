@@ -45,6 +45,16 @@ __device__ __forceinline__ void named_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
+// Dataflow signal (kc_consume.cu): after the barrier that follows the item's
+// last logits / statistics write, one thread publishes the split at GPU scope
+// (fence + relaxed add = release; the consumer's acquire load pairs with it).
+__device__ __forceinline__ void signal_row(const ScoreParams& p, int row) {
+  if (p.row_done && threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(p.row_done + (size_t)row * kRowDoneStride, 1u);
+  }
+}
+
 template <int LPR>
 __device__ __forceinline__ int chunk_of(int ci, int rl, int sub) {
   if constexpr (LPR == 4) {
@@ -335,6 +345,7 @@ __global__ void __launch_bounds__((kCWarps + 1) * 32, (G >= 2 ? 2 : KC_MHA_MINB)
       emit_candidates(scb, mx, wcnt, npos, p.cand_nc, pos0, p.cand + (size_t)row * p.lstride + pos0,
                       p.cand_meta + (size_t)row * p.max_splits + split);
     named_sync(1, kCWarps * 32);  // red / scb are reused by the next item
+    signal_row(p, row);
   }
 }
 
@@ -574,6 +585,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32) score_mma_kernel(const ScorePa
       p.partials[((size_t)b * n_q + kvh * G + gh) * p.max_splits + split] = make_float2(m, l);
     }
     named_sync(1, NCW * 32);  // red is reused by the next item
+    signal_row(p, row);
   }
 }
 
@@ -615,6 +627,8 @@ __global__ void __launch_bounds__(256) score_generic_kernel(const ScoreParams p)
     for (int w = 0; w < 8; ++w) ml_combine(m, l, wstat[w * G + g].x, wstat[w * G + g].y);
     p.partials[((size_t)b * n_q + kvh * G + g) * p.max_splits + split] = make_float2(m, l);
   }
+  __syncthreads();
+  signal_row(p, row);
 }
 
 // ---- decode_attention_full, fused (attention.cpp:91-114) -------------------
@@ -870,13 +884,13 @@ void launch_fast_s(const ScoreParams& p, cudaStream_t st) {
   const size_t smem = STAGES * kRows * ROWB + 2 * STAGES * sizeof(uint64_t) +
                       kCWarps * G * sizeof(float2) +
                       (CAND ? (size_t)kMaxCandChunk * 4 + 3 * kCWarps * 4 : 0);
-  static unsigned long long configured = 0;  // one bit per device
+  static int configured[64] = {0};  // dynamic smem opted in, per device (grows with the split length)
   int dev = 0;
   cudaGetDevice(&dev);
-  if (!(configured >> (dev & 63) & 1ull)) {
+  if (configured[dev & 63] < (int)smem) {
     cudaFuncSetAttribute(score_fast_kernel<T, G, LPR, STAGES, CAND>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    configured |= 1ull << (dev & 63);
+    configured[dev & 63] = (int)smem;
   }
   const int n_items = p.rows * p.n_splits;
   score_fast_kernel<T, G, LPR, STAGES, CAND><<<n_items, (kCWarps + 1) * 32, smem, st>>>(p);

@@ -116,6 +116,7 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         "kc_profile_span": (i32, [vp, C.c_char_p, u64, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
         "kc_arg_topk": (i32, [vp, u64, u64, vp, p64]),
         "kc_score_chunk_plan": (i32, [u64, u64, u64, C.POINTER(C.c_int64)]),
+        "kc_debug_read": (i32, [vp, C.c_char_p, vp, u64]),
         "kc_prefill_attention": (i32, [vp, vp, vp, u64, u64, u64, vp, i32]),
         "kc_prefill_attention_device": (i32, [vp, vp, vp, u64, u64, u64, vp, vp]),
         "kc_fill_uniform": (i32, [vp, i32, u64, u64, u64, C.c_float, C.c_float, vp]),
@@ -464,6 +465,23 @@ class TieredKVCache:
             a, b = C.c_double(0), C.c_double(0)
             _check(self._lib.kc_profile_span(self._h, kernel.encode(), i, C.byref(a), C.byref(b)))
             out.append((a.value, b.value))
+        return out
+
+    def consume_stamps(self):
+        """Development probe (tuning consume_dbg 1): the dataflow consumer's
+        per-row phase timestamps of the last decode call, ns, [rows][8]:
+        0 row ready, 1 stats, 2 bound, 3 candidates, 4 selected, 5 finished,
+        6 recalled, 7 wait start."""
+        import numpy as np
+        out = np.zeros((self.batch * self.config.kv_heads, 8), dtype=np.uint64)
+        _check(self._lib.kc_debug_read(self._h, b"consume", out.ctypes.data, out.nbytes))
+        return out
+
+    def debug_buffer(self, what: str, nbytes: int):
+        """Development probe: raw bytes of an internal device buffer."""
+        import numpy as np
+        out = np.zeros(nbytes, dtype=np.uint8)
+        _check(self._lib.kc_debug_read(self._h, what.encode(), out.ctypes.data, nbytes))
         return out
 
     # ---- device-resident decode (bench / engine path) ----

@@ -17,7 +17,7 @@ from tests.test_gpu_parity import build_cache, compare_all
 pytestmark = pytest.mark.gpu
 
 DEFAULTS = {"select_cand": 0, "cand_force_fallback": 0, "score_groups": 0, "score_chunk": 0,
-            "recall_pipe": -1, "score_mma": 1, "recall_ctas": 32, "tlb_ahead": -1}
+            "recall_pipe": -1, "score_mma": 1, "recall_ctas": 32, "tlb_ahead": -1, "consume": 1, "consume_ctas": 0}
 
 
 def _run(kc, cache, q, N, renorm=False, **tune):

@@ -33,26 +33,46 @@ __device__ __forceinline__ unsigned smem_u32(const void* p) {
   return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
 
-template <int U>
-__global__ void __launch_bounds__(256) gather_ld16(const uint4* __restrict__ v, const unsigned* __restrict__ idx,
-                                                   float* sink) {
+template <int U, int HINT, int NT>
+__global__ void __launch_bounds__(NT) gather_ld16(const uint4* __restrict__ v, const unsigned* __restrict__ idx,
+                                                  float* sink) {
   float acc = 0.f;
   for (int row = blockIdx.x; row < kRows; row += gridDim.x) {
     const uint4* base = v + (size_t)row * kSeq * (kRowB / 16);
     const unsigned* ir = idx + row * kSel;
     constexpr int total = kSel * (kRowB / 16);  // 2048 16-B pieces
-    for (int v0 = threadIdx.x; v0 < total; v0 += 256 * U) {
+    for (int v0 = threadIdx.x; v0 < total; v0 += NT * U) {
       uint4 t[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const int e = v0 + u * 256;
-        if (e < total) t[u] = base[(size_t)ir[e >> 4] * 16 + (e & 15)];
+        const int e = v0 + u * NT;
+        if (e < total) {
+          const uint4* a = base + (size_t)ir[e >> 4] * 16 + (e & 15);
+          if (HINT == 1)
+            asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
+                         : "=r"(t[u].x), "=r"(t[u].y), "=r"(t[u].z), "=r"(t[u].w) : "l"(a));
+          else if (HINT == 2)
+            asm volatile("ld.global.nc.L1::no_allocate.L2::128B.v4.u32 {%0,%1,%2,%3}, [%4];"
+                         : "=r"(t[u].x), "=r"(t[u].y), "=r"(t[u].z), "=r"(t[u].w) : "l"(a));
+          else
+            t[u] = *a;
+        }
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) acc += __uint_as_float(t[u].x ^ t[u].w);
     }
   }
   if (acc == 1.2345f) sink[0] = acc;
+}
+
+// background HBM stream (stands in for the scoring kernel)
+__global__ void __launch_bounds__(512) hbm_stream(const uint4* __restrict__ a, size_t n16, float* sink) {
+  float acc = 0.f;
+  for (size_t i = blockIdx.x * 512ull + threadIdx.x; i < n16; i += (size_t)gridDim.x * 512) {
+    uint4 t = __ldcs(a + i);
+    acc += __uint_as_float(t.x ^ t.y);
+  }
+  if (acc == 1.2345f) sink[1] = acc;
 }
 
 // R rows per stage, 2 stages; thread 0 issues, everyone consumes (xor-sum)
@@ -172,19 +192,102 @@ int main() {
     std::printf("{\"method\": \"%s\", \"grid\": %d, \"avg_us\": %.1f, \"best_us\": %.1f, \"avg_gbs\": %.1f}\n", name,
                 grid, avg * 1e3, best * 1e3, gather_bytes / (avg * 1e-3) / 1e9);
   };
-  for (int grid : {32, 64, 128, 256}) {
-    run("ld16_u8", grid, [&](int g, unsigned* ix) { gather_ld16<8><<<g, 256>>>((const uint4*)v, ix, sink); });
-    run("ld16_u16", grid, [&](int g, unsigned* ix) { gather_ld16<16><<<g, 256>>>((const uint4*)v, ix, sink); });
+  for (int grid : {32, 64, 148, 296}) {
+    run("ld16_u8", grid, [&](int g, unsigned* ix) { gather_ld16<8, 0, 256><<<g, 256>>>((const uint4*)v, ix, sink); });
+    run("ld16_u8_l2_256", grid, [&](int g, unsigned* ix) { gather_ld16<8, 1, 256><<<g, 256>>>((const uint4*)v, ix, sink); });
+    run("ld16_u8_l2_128", grid, [&](int g, unsigned* ix) { gather_ld16<8, 2, 256><<<g, 256>>>((const uint4*)v, ix, sink); });
+    run("ld16_u2_t1024", grid, [&](int g, unsigned* ix) { gather_ld16<2, 0, 1024><<<g, 1024>>>((const uint4*)v, ix, sink); });
+    run("ld16_u2_t1024_l2_256", grid, [&](int g, unsigned* ix) { gather_ld16<2, 1, 1024><<<g, 1024>>>((const uint4*)v, ix, sink); });
     run("tma_r32", grid, [&](int g, unsigned* ix) {
       gather_tma<32><<<g, 256, 2 * 32 * kRowB>>>((const char*)v, ix, sink);
     });
     run("tma_r64", grid, [&](int g, unsigned* ix) {
       gather_tma<64><<<g, 256, 2 * 64 * kRowB>>>((const char*)v, ix, sink);
     });
-    run("tma_r128", grid, [&](int g, unsigned* ix) {
-      cudaFuncSetAttribute(gather_tma<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 128 * kRowB);
-      gather_tma<128><<<g, 256, 2 * 128 * kRowB>>>((const char*)v, ix, sink);
-    });
+  }
+  // under a concurrent HBM stream (the in-step condition)
+  {
+    const size_t hb = 8ull << 30;
+    void* hbm = nullptr;
+    CK(cudaMalloc(&hbm, hb));
+    CK(cudaMemset(hbm, 1, hb));
+    cudaStream_t bg;
+    CK(cudaStreamCreateWithPriority(&bg, cudaStreamNonBlocking, 0));
+    cudaEvent_t h0, h1;
+    CK(cudaEventCreate(&h0));
+    CK(cudaEventCreate(&h1));
+    CK(cudaEventRecord(h0, bg));
+    hbm_stream<<<148 * 2, 512, 0, bg>>>((const uint4*)hbm, hb / 16, sink);
+    CK(cudaEventRecord(h1, bg));
+    CK(cudaDeviceSynchronize());
+    float hms = 0;
+    CK(cudaEventElapsedTime(&hms, h0, h1));
+    std::printf("{\"method\": \"hbm_stream_alone\", \"ms\": %.3f, \"gbs\": %.1f}\n", hms, hb / (hms * 1e-3) / 1e9);
+    for (int grid : {32, 64, 148}) {
+      for (int m = 0; m < 3; ++m) {
+        float tot = 0;
+        const int reps = 6;
+        float hsum = 0;
+        for (int rep = 0; rep < reps; ++rep) {
+          CK(cudaEventRecord(h0, bg));
+          hbm_stream<<<148 * 2, 512, 0, bg>>>((const uint4*)hbm, hb / 16, sink);
+          CK(cudaEventRecord(h1, bg));
+          // let the stream ramp, then gather 8 layers back to back
+          CK(cudaEventRecord(a));
+          for (int l = 0; l < 8; ++l) {
+            unsigned* ix = didx + (size_t)((rep * 8 + l) % kReps) * kRows * kSel;
+            if (m == 0) gather_ld16<8, 0, 256><<<grid, 256>>>((const uint4*)v, ix, sink);
+            else if (m == 1) gather_ld16<8, 1, 256><<<grid, 256>>>((const uint4*)v, ix, sink);
+            else gather_tma<32><<<grid, 256, 2 * 32 * kRowB>>>((const char*)v, ix, sink);
+          }
+          CK(cudaEventRecord(b));
+          CK(cudaDeviceSynchronize());
+          float ms = 0;
+          CK(cudaEventElapsedTime(&ms, a, b));
+          tot += ms / 8;
+          CK(cudaEventElapsedTime(&ms, h0, h1));
+          hsum += ms;
+        }
+        const char* nm[3] = {"ld16_u8", "ld16_u8_l2_256", "tma_r32"};
+        std::printf("{\"method\": \"%s+hbm\", \"grid\": %d, \"avg_us\": %.1f, \"avg_gbs\": %.1f, \"hbm_ms\": %.3f}\n",
+                    nm[m], grid, tot / reps * 1e3, gather_bytes / (tot / reps * 1e-3) / 1e9, hsum / reps);
+      }
+    }
+  }
+  // copy engine, batched 256-B copies (pointer arrays prebuilt: the best case)
+  {
+    const size_t n = (size_t)kRows * kSel;
+    std::vector<void*> dsts(n), srcs(n);
+    std::vector<size_t> sizes(n, kRowB);
+    char* dbuf = nullptr;
+    CK(cudaMalloc(&dbuf, n * kRowB));
+    for (size_t i = 0; i < n; ++i) {
+      const size_t row = i / kSel;
+      dsts[i] = dbuf + i * kRowB;
+      srcs[i] = static_cast<char*>(v) + (row * kSeq + hidx[i]) * kRowB;
+    }
+    cudaMemcpyAttributes attr{};
+    attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+    attr.srcLocHint.type = cudaMemLocationTypeHost;
+    attr.dstLocHint.type = cudaMemLocationTypeDevice;
+    attr.dstLocHint.id = 0;
+    size_t aidx = 0, fail = 0;
+    cudaStream_t cs;
+    CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    float best = 1e9, tot = 0;
+    for (int rep = 0; rep < 6; ++rep) {
+      CK(cudaEventRecord(a, cs));
+      cudaError_t e = cudaMemcpyBatchAsync(dsts.data(), srcs.data(), sizes.data(), n, &attr, &aidx, 1, &fail, cs);
+      if (e != cudaSuccess) { std::printf("{\"method\": \"memcpy_batch\", \"error\": \"%s\"}\n", cudaGetErrorString(e)); cudaGetLastError(); break; }
+      CK(cudaEventRecord(b, cs));
+      CK(cudaEventSynchronize(b));
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, a, b));
+      best = std::min(best, ms);
+      if (rep) tot += ms;
+    }
+    std::printf("{\"method\": \"memcpy_batch_256B\", \"best_us\": %.1f, \"avg_us\": %.1f, \"gbs\": %.1f}\n", best * 1e3,
+                tot / 5 * 1e3, gather_bytes / (best * 1e-3) / 1e9);
   }
   // copy engine reference: pinned 256 MiB H2D
   {

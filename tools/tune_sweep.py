@@ -33,6 +33,8 @@ def main():
     ap.add_argument("--profile", action="store_true", help="also print per-kernel event times (perturbs overlap)")
     ap.add_argument("--per-step", action="store_true", help="print every step's time")
     ap.add_argument("--graph", action="store_true", help="capture every step into the cache's step graph")
+    ap.add_argument("--engine", action="store_true",
+                    help="one single-layer call per layer (layer l+1 ordered after layer l: the engine's dependency)")
     args = ap.parse_args()
     L, b, n, n_kv, h, s, N = args.layers, args.batch, args.heads, args.kv, 128, args.s, args.topn
     d = n * h
@@ -71,7 +73,11 @@ def main():
         def step():
             if args.graph:
                 cache.step_graph_begin(N, stream)
-            cache.decode_topn_layers_device(run, qs, N, outs, stream=stream)
+            if args.engine:
+                for i, l in enumerate(run):
+                    cache.decode_topn_layers_device([l], [qs[i]], N, [outs[i]], stream=stream)
+            else:
+                cache.decode_topn_layers_device(run, qs, N, outs, stream=stream)
             if args.graph:
                 cache.step_graph_launch(stream)
         for _ in range(3):
@@ -85,7 +91,7 @@ def main():
         torch.cuda.synchronize()
         ms = evs[0].elapsed_time(evs[-1]) / args.steps
         per_step = [round(evs[i].elapsed_time(evs[i + 1]), 2) for i in range(args.steps)]
-        rec = {"tune": dict(zip(keys, combo)), "step_ms": round(ms, 4), "per_layer_us": round(1e3 * ms / len(run), 1),
+        rec = {"tune": dict(zip(keys, combo)), "engine": args.engine, "step_ms": round(ms, 4), "per_layer_us": round(1e3 * ms / len(run), 1),
                "k_only_gbs": round(k_bytes / (ms * 1e-3) / 1e9, 1)}
         if args.per_step:
             rec["per_step_ms"] = per_step
