@@ -521,7 +521,11 @@ def run_ours(args, cfg):
     global_batch = B * world if shard == "batch" else B
     value = global_batch / (ms * 1e-3)
     e2e_value = global_batch / (e2e_ms * 1e-3)
-    launches_per_layer = 3 + (1 if G > 1 else 0)
+    # MHA: the dataflow path (scoring + the consumer: selection, recall and P.V
+    # of each row as the scoring completes it); GQA: scoring, selection, recall
+    # (+ the kv-head -> q-head index expansion of the outputs)
+    flow = n_kv == n
+    launches_per_layer = 2 if flow else 3 + (1 if G > 1 else 0)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
@@ -529,7 +533,11 @@ def run_ours(args, cfg):
         "vs_baseline": None, "dtype": "f16 storage / f32 accumulate",
         "data": "synthetic (SeededRng SplitMix64 U[-1,1], fp16-rounded)",
         "config": config_block(cfg, args, world, shard),
-        "placement": {"pipeline": "recall(l) overlaps scoring(l+1)", "v_arena_numa_node": numa,
+        "placement": {"pipeline": ("dataflow: a persistent consumer grid selects, recalls and reduces each (batch, "
+                                   "kv head) row while the scoring streams the later rows (kc_consume.cu)" if flow else
+                                   "stream-ordered: scoring(l) -> selection(l) on the main stream, recall(l) + P.V on "
+                                   "a side stream under scoring(l+1)"),
+                      "v_arena_numa_node": numa,
                       "v_arena": v_arena + " (UVM managed, host-resident: large GPU pages, no per-row page walks; "
                                  "pinned beyond the driver's managed-memory cap; KCACHE_V_ARENA=pinned forces pinned)"},
         "per_gpu_tokens_per_s": value / world,
@@ -547,7 +555,9 @@ def run_ours(args, cfg):
                           "t_roof_sum_ms": (t_k + t_v) * 1e3, "t_roof_max_ms": max(t_k, t_v) * 1e3,
                           "frac_of_sum_roofline": (t_k + t_v) * 1e3 / ms,
                           "frac_of_max_roofline": max(t_k, t_v) * 1e3 / ms},
-        "kernel_ms_per_step": {"score": all_score_ms / prof_steps, "select": select_ms / prof_steps,
+        "kernel_ms_per_step": {"score": all_score_ms / prof_steps,
+                               ("consume (select + recall + P.V, spans the scoring)" if flow else "select"):
+                                   select_ms / prof_steps,
                                "recall_pv": recall_ms / prof_steps, "profiled_step_ms": prof_ms,
                                "score_only_profiled_step_ms": score_prof_ms,
                                "note": "separate profiled passes (CUDA events around launches perturb the "
@@ -556,7 +566,8 @@ def run_ours(args, cfg):
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": L * b * d * 4,
                 "d2h_bytes_per_step": L * (b * d * 4 + slots * nc * 8 + slots * 8), "ms_per_step": e2e_ms,
                 "path": "kc_decode_topn_layers with pinned host q / outputs (TieredKVCache.prepare_topn_layers_host: buffers bound once, one C-ABI call per step)"},
-        "kernel_isolated_ms_per_launch": {k: iso[k][0] / max(iso[k][1], 1) for k in iso},
+        "kernel_isolated_ms_per_launch": {("consume" if flow and k == "select" else k): iso[k][0] / max(iso[k][1], 1)
+                                          for k in iso if not (flow and k == "recall")},
         "serial_step_ms": serial_ms,
         "gpu_launches": launches_per_layer * L * args.steps,
         "clocks": clocks,
@@ -571,8 +582,8 @@ def run_ours(args, cfg):
             "value": global_batch / (engine_ms * 1e-3), "unit": UNIT, "ms_per_step": engine_ms,
             "steps": ENGINE_STEPS, "frac_of_max_roofline": max(t_k, t_v) * 1e3 / engine_ms,
             "note": "engine-realistic decode step: one kc_decode_step per layer (append + TopN, engine.cpp:124-165), "
-                    "layer l+1 waits for layer l (no cross-layer overlap), row groups overlap recall with scoring "
-                    "inside a layer; NOT the headline (which pipelines the recall of layer l under the scoring of "
+                    "layer l+1 waits for layer l (no cross-layer overlap); inside a layer the dataflow consumer "
+                    "(MHA) or two row groups (GQA) overlap selection / recall with the scoring; NOT the headline (which pipelines the recall of layer l under the scoring of "
                     "layer l+1, the attention-only bench of SURVEY.md section 7)"}
     line["roofline"]["achieved_isolated"] = k_bytes_layer / (iso["score"][0] / max(iso["score"][1], 1) * 1e-3) / 1e9
     if full is not None:

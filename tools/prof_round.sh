@@ -1,26 +1,30 @@
 #!/bin/bash
-# Profiling pass for profiles/: launch list of the bench command, then one
-# ncu --set full capture per hot kernel (1 GPU, never multi-rank).
+# Profiling pass for profiles/ (1 GPU, never multi-rank): the launch lists of
+# the C2 and C3 bench commands, then one `ncu --set full` capture per hot
+# kernel, exported to raw CSV on the box (the .ncu-rep files are large).
 #   bash tools/prof_round.sh ; python tools/summarize_ncu.py <tag>
-# gpurun copies back at most 64 MiB of gpurun_out/: select parts with
-#   LAUNCHES=0|1  KERNELS="score_fast select_reg recall_pv"  EXTRA="full cand"
 mkdir -p gpurun_out
-CMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --no-full-kv"
-if [ "${LAUNCHES:-1}" = 1 ]; then
+CMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --no-full-kv --no-engine"
 ncu --metrics gpu__time_duration.sum --clock-control none -s 300 -c 300 --csv \
     --log-file gpurun_out/launches.csv $CMD > gpurun_out/launches_run.log 2>&1
-fi
-for k in ${KERNELS-score_fast select_reg recall_pv}; do
-  ncu --set full --clock-control none --import-source on -k regex:$k -s 200 -c 1 \
-      -o gpurun_out/prof_$k -f $CMD > gpurun_out/prof_${k}_run.log 2>&1
-done
-EXTRA=${EXTRA-full cand}
+ncu --metrics gpu__time_duration.sum --clock-control none -s 400 -c 400 --csv \
+    --log-file gpurun_out/launches_c3.csv $CMD --config c3 > gpurun_out/launches_c3_run.log 2>&1
+cap() {  # name, kernel regex, skip, extra bench args
+  ncu --set full --clock-control none --import-source on -k regex:$2 -s $3 -c 1 \
+      -o gpurun_out/prof_$1 -f $CMD $4 > gpurun_out/prof_$1_run.log 2>&1
+  ncu -i gpurun_out/prof_$1.ncu-rep --page raw --csv > gpurun_out/prof_$1_raw.csv 2>/dev/null
+}
+cap score_fast score_fast 200 ""
+cap consume consume_kernel 60 ""
+cap score_mma_c3 score_mma 200 "--config c3"
+cap select_reg_c3 select_reg 60 "--config c3"
+cap recall_pv_c3 recall_pv 60 "--config c3"
 # the full-KV comparator's fused kernel (bench's full_kv leg)
-[[ " $EXTRA " == *" full "* ]] && ncu --set full --clock-control none --import-source on -k regex:full_fast -s 40 -c 1 \
-    -o gpurun_out/prof_full_fast -f python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e \
+ncu --set full --clock-control none --import-source on -k regex:full_fast -s 40 -c 1 \
+    -o gpurun_out/prof_full_fast -f python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --no-engine \
     > gpurun_out/prof_full_fast_run.log 2>&1
-# candidate mode (auto beyond 32k positions): scoring epilogue + candidate selection at 64k
-[[ " $EXTRA " == *" cand "* ]] && ncu --set full --clock-control none --import-source on -k regex:"score_fast|select_cand" -s 6 -c 2 \
-    -o gpurun_out/prof_cand64k -f python tools/c5_crossover.py --contexts 65536 --topns 128 --layers 2 --steps 2 \
-    > gpurun_out/prof_cand64k_run.log 2>&1
+ncu -i gpurun_out/prof_full_fast.ncu-rep --page raw --csv > gpurun_out/prof_full_fast_raw.csv 2>/dev/null
+ncu -i gpurun_out/prof_consume.ncu-rep --page source --csv --print-source cuda,sass > gpurun_out/prof_consume_source.csv 2>/dev/null
+# keep only the consumer's report (source view); the rest travel as CSV
+for f in gpurun_out/prof_*.ncu-rep; do [ "$f" = gpurun_out/prof_consume.ncu-rep ] || rm -f "$f"; done
 ls -la gpurun_out

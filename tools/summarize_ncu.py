@@ -33,7 +33,10 @@ METRICS = [
 
 
 def raw_metrics(rep, launch=0):
-    txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    if rep.endswith(".csv"):
+        txt = open(rep).read()
+    else:
+        txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(txt)))
     hdr, units, vals = rows[0], rows[1], rows[2 + launch]
     out = {}
@@ -54,9 +57,11 @@ def to_bytes(v, u):
 def main():
     tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
     os.makedirs(PROF, exist_ok=True)
-    # launch list
-    lpath = os.path.join(OUT, "launches.csv")
-    if os.path.exists(lpath):
+    # launch lists (C2, C3)
+    for lname, suffix in (("launches.csv", ""), ("launches_c3.csv", "_c3")):
+        lpath = os.path.join(OUT, lname)
+        if not os.path.exists(lpath):
+            continue
         lines = open(lpath).read().splitlines()
         start = next(i for i, l in enumerate(lines) if l.startswith('"ID"'))
         rows = list(csv.DictReader(io.StringIO("\n".join(lines[start:]))))
@@ -71,20 +76,24 @@ def main():
             agg[name][0] += 1
             agg[name][1] += us
         total = sum(t for _, t in agg.values())
-        with open(os.path.join(PROF, f"{tag}_launches.csv"), "w") as f:
+        out = os.path.join(PROF, f"{tag}_launches{suffix}.csv")
+        with open(out, "w") as f:
             f.write("kernel,launches,total_us,mean_us,share\n")
             for k, (n, t) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
                 f.write(f"{k},{n},{t:.1f},{t / n:.1f},{t / total:.3f}\n")
-        print(open(os.path.join(PROF, f"{tag}_launches.csv")).read())
+        print(open(out).read())
     summary = {}
-    captures = [("score_fast", "prof_score_fast", 0, "python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --no-full-kv (C2)"),
-                ("select_reg", "prof_select_reg", 0, "same (C2)"),
-                ("recall_pv", "prof_recall_pv", 0, "same (C2)"),
-                ("full_fast", "prof_full_fast", 0, "python bench.py ... (C2 full-KV comparator leg, K+V in HBM)"),
-                ("score_fast_cand64k", "prof_cand64k", 0, "python tools/c5_crossover.py --contexts 65536 --topns 128 --layers 2"),
-                ("select_cand64k", "prof_cand64k", 1, "same (64k, N=128)")]
+    c2 = "python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --no-full-kv --no-engine (C2)"
+    captures = [("score_fast", "prof_score_fast", 0, c2),
+                ("consume", "prof_consume", 0, c2 + ": the dataflow consumer (selection + recall + P.V)"),
+                ("score_mma_c3", "prof_score_mma_c3", 0, c2.replace("(C2)", "--config c3")),
+                ("select_reg_c3", "prof_select_reg_c3", 0, "same (C3)"),
+                ("recall_pv_c3", "prof_recall_pv_c3", 0, "same (C3)"),
+                ("full_fast", "prof_full_fast", 0, "python bench.py ... (C2 full-KV comparator leg, K+V in HBM)")]
     for k, repname, launch, cmd in captures:
-        rep = os.path.join(OUT, f"{repname}.ncu-rep")
+        rep = os.path.join(OUT, f"{repname}_raw.csv")
+        if not os.path.exists(rep):
+            rep = os.path.join(OUT, f"{repname}.ncu-rep")
         if not os.path.exists(rep):
             continue
         try:
@@ -109,6 +118,16 @@ def main():
                    "dram_read": rd, "dram_write": wr, "algorithmic_bytes": 2 * 8 * 32 * 32768 * 128,
                    "ncu_duration_us": dur_us, "ncu_dram_gbs": (rd + wr) / (dur_us * 1e-6) / 1e9},
                   open(os.path.join(PROF, "ncu_score_summary.json"), "w"), indent=1)
+    if "score_mma_c3" in summary:
+        m = summary["score_mma_c3"]
+        rd = to_bytes(*m["dram__bytes_read.sum"])
+        wr = to_bytes(*m["dram__bytes_write.sum"])
+        dur = float(m["gpu__time_duration.sum"][0].replace(",", ""))
+        dur_us = dur / 1e3 if m["gpu__time_duration.sum"][1] == "nsecond" else dur
+        json.dump({"config": "c3", "tag": tag, "kernel": m["kernel"], "dram_bytes_per_launch": rd + wr,
+                   "dram_read": rd, "dram_write": wr, "algorithmic_bytes": 2 * 32 * 8 * 16384 * 128,
+                   "ncu_duration_us": dur_us, "ncu_dram_gbs": (rd + wr) / (dur_us * 1e-6) / 1e9},
+                  open(os.path.join(PROF, "ncu_score_summary_c3.json"), "w"), indent=1)
 
 
 if __name__ == "__main__":
