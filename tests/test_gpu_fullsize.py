@@ -11,8 +11,9 @@ copied back once, and sliced per slot for the oracle. Shapes:
 * C3: LLaMA3-8B GQA 32/8, b=32, s=16k, N=128 (reports the epsilon-window
   swap count of the GQA selection key);
 * C4: LLaMA2-13B, 40 x 128 (d=5120), b=7, s=32k, N=128;
-* C5 corners: 128k x N in {32, 128, 512} (candidate mode for N <= 128, the
-  global-key selection for N=512), GQA at 128k, and 4k x N=512.
+* C5 corners: 128k x N in {32, 128, 512} (MHA: the dataflow consumer's
+  streamed selection; GQA at 128k: the global-key selection kernel), and
+  4k x N=512.
 """
 import numpy as np
 import pytest
