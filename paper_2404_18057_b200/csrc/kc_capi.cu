@@ -210,7 +210,13 @@ struct kc_cache {
   bool stage_copy[2] = {};        // ev_off[slot] marks an enqueued D2H of the slot
   int next_stage = 0;
   bool off_pending = false;       // some D2H may still be running
-  int prefill_stage = 1;          // tuning: 0 = always mapped stores (the r01 path)
+  // tuning: 1 stage (default), 0 mapped stores inside the append (the r01 path)
+  int prefill_stage = 1;
+  // staged layers in host-resident managed memory leave through an SM copy
+  // kernel on off_st (the copy engine writes those pages at 2.2 GB/s, r02
+  // tools/prefill_offload_bench.py); pinned-arena layers through the copy
+  // engine. stage_copy_ctas: that kernel's grid
+  int stage_copy_ctas = 8;  // 8..64 CTAs all reach 52 GB/s (r02)
   cudaStream_t off_st = nullptr;
   cudaEvent_t ev_staged[2] = {}, ev_off[2] = {};
   void order_after_offloads(cudaStream_t st) {
@@ -726,7 +732,13 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
     // scoring stream carries nothing but scoring. Scoring buffers alternate
     // between two slots so layer i+1's scoring never waits for layer i's
     // consumer; layer i+2's waits for it (ev_cons).
-    const bool flow = (c->consume == 2 || (c->consume == 1 && c->G == 1)) &&
+    // auto (consume 1): MHA rows of >= 16 k positions with N <= 256 -- shorter
+    // rows and larger N measured faster stream-ordered (r02 C5 sweep: 4 k x
+    // N=128 237 vs 224 us per layer, 32 k x N=512 1097 vs 885: > 1024
+    // candidates take the consumer's exact path), and inside a step-graph
+    // capture the consumer could only follow its scoring
+    const bool flow_auto = c->G == 1 && g.nc <= 256 && g.s >= 16384 && !c->capture_st;
+    const bool flow = (c->consume == 2 || (c->consume == 1 && flow_auto)) &&
                       kc::consume_supported((int)c->G, (int)c->h) && !c->select_global && c->select_cand != 1;
     if (flow) {
       const int ls = (int)(c->cons_seq & 1);
@@ -1143,9 +1155,15 @@ int kc_offload_prefill_v(kc_cache* c, uint64_t layer) {
       const int slot = st.stage;
       const size_t pitch = (size_t)c->cfg.max_seq * c->h * c->esz;
       CK(cudaStreamWaitEvent(c->off_st, c->ev_staged[slot], 0));
-      if (st.len > 0)
-        CK(cudaMemcpy2DAsync(c->v_arena_layer(layer), pitch, c->v_stage[slot].p, pitch, st.len * c->h * c->esz,
-                             c->rows, cudaMemcpyDefault, c->off_st));
+      if (st.len > 0) {
+        if (layer - c->L < c->v_managed.size())
+          kc::copy_rows_launch(c->v_stage[slot].p, c->v_arena_layer(layer), (int64_t)pitch,
+                               (int64_t)(st.len * c->h * c->esz), (int)c->rows, c->stage_copy_ctas, c->off_st);
+        else
+          CK(cudaMemcpy2DAsync(c->v_arena_layer(layer), pitch, c->v_stage[slot].p, pitch, st.len * c->h * c->esz,
+                               c->rows, cudaMemcpyDefault, c->off_st));
+        CK(cudaGetLastError());
+      }
       CK(cudaEventRecord(c->ev_off[slot], c->off_st));
       c->stage_copy[slot] = true;
       c->stage_owner[slot] = -1;
@@ -1616,6 +1634,10 @@ int kc_set_tuning(kc_cache* c, const char* key, int64_t value) {
     }
     else if (k == "keep_logits") c->keep_logits = value ? 1 : 0;
     else if (k == "prefill_stage") c->prefill_stage = value ? 1 : 0;
+    else if (k == "stage_copy_ctas") {
+      if (value < 1) fail(KC_EARG, "stage_copy_ctas must be >= 1");
+      c->stage_copy_ctas = (int)value;
+    }
     else if (k == "group_first_pct") {
       if (value < 0 || value > 100) fail(KC_EARG, "group_first_pct: 0..100");
       c->group_first_pct = (int)value;

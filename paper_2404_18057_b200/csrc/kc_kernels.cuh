@@ -232,6 +232,9 @@ struct AppendParams {
   int h;
 };
 void append_launch(const AppendParams& p, int src_dtype, int dst_dtype, cudaStream_t st);
+// rows x row_bytes at a common pitch, src -> dst, on `grid` CTAs (SM copy)
+void copy_rows_launch(const void* src, void* dst, int64_t pitch, int64_t row_bytes, int rows, int grid,
+                      cudaStream_t st);
 
 void fill_uniform_launch(void* dst, int dtype, uint64_t n, uint64_t seed, uint64_t offset, float lo,
                          float hi, cudaStream_t st);

@@ -483,6 +483,39 @@ void pv_full_launch(const PvFullParams& p, int dtype, cudaStream_t st) {
                                                                     p.n_splits, p.h);
 }
 
+// Pitched row copy with 16-B accesses (prefill V stage -> its host arena when
+// the arena is host-resident managed memory: the copy engine writes those
+// pages at ~2 GB/s, SM stores at the PCIe rate). A small grid: it runs beside
+// the caller's next layer.
+__global__ void __launch_bounds__(256) copy_rows_kernel(const uint4* __restrict__ src, uint4* __restrict__ dst,
+                                                        int64_t pitch16, int64_t row16, int rows) {
+  const int64_t total = row16 * rows;
+  for (int64_t i = blockIdx.x * 256ll + threadIdx.x; i < total; i += (int64_t)gridDim.x * 256) {
+    const int64_t r = i / row16, c = i - r * row16;
+    dst[r * pitch16 + c] = __ldcs(src + r * pitch16 + c);
+  }
+}
+
+__global__ void __launch_bounds__(256) copy_rows_bytes_kernel(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst,
+                                                              int64_t pitch, int64_t row_bytes, int rows) {
+  const int64_t total = row_bytes * rows;
+  for (int64_t i = blockIdx.x * 256ll + threadIdx.x; i < total; i += (int64_t)gridDim.x * 256) {
+    const int64_t r = i / row_bytes, c = i - r * row_bytes;
+    dst[r * pitch + c] = src[r * pitch + c];
+  }
+}
+
+void copy_rows_launch(const void* src, void* dst, int64_t pitch, int64_t row_bytes, int rows, int grid,
+                      cudaStream_t st) {
+  if (rows <= 0 || row_bytes <= 0) return;
+  if ((pitch & 15) == 0 && (row_bytes & 15) == 0 && ((uintptr_t)src & 15) == 0 && ((uintptr_t)dst & 15) == 0)
+    copy_rows_kernel<<<grid, 256, 0, st>>>(static_cast<const uint4*>(src), static_cast<uint4*>(dst), pitch / 16,
+                                           row_bytes / 16, rows);
+  else
+    copy_rows_bytes_kernel<<<grid, 256, 0, st>>>(static_cast<const uint8_t*>(src), static_cast<uint8_t*>(dst),
+                                                 pitch, row_bytes, rows);
+}
+
 void append_launch(const AppendParams& p, int src_dtype, int dst_dtype, cudaStream_t st) {
   switch (src_dtype) {
     case KC_F16: append_dst<__half>(p, dst_dtype, st); break;

@@ -6,7 +6,9 @@ indices, weights, dropped mass, renormaliser-driven outputs -- on random rows,
 rows that take its exact path (N >= s, tie floods, p-underflow ties, N > 1024
 candidates), GQA groups, other head dims / storage types (generic scoring
 kernel), long rows, single and pipelined multi-layer calls that reuse every
-ring and scoring slot, and any consumer grid size.
+ring and scoring slot, and any consumer grid size. (consume 2 forces the
+consumer for these small shapes; by default it serves MHA rows of >= 16 k
+positions with N <= 256, covered at full size by test_gpu_fullsize.py.)
 """
 import numpy as np
 import pytest
@@ -72,7 +74,7 @@ def test_consumer_grid_sizes_bitwise(kc, ctas):
     cache, ks, vs = build_cache(kc, b, n, n, h, s, "f16")
     q = synth_matrix(5, b, n * h)
     ref = _decode(kc, cache, q, N, consume=0)
-    _same(_decode(kc, cache, q, N, consume=1, consume_ctas=ctas), ref)
+    _same(_decode(kc, cache, q, N, consume=2, consume_ctas=ctas), ref)
     cache.close()
 
 
@@ -139,7 +141,7 @@ def test_consumer_tie_flood_and_underflow(kc, oracle):
         cache.append_kv(0, k, v)
         cache.offload_prefill_v(0)
         cache.begin_decode()
-        flow = _decode(kc, cache, q, N, consume=1)
+        flow = _decode(kc, cache, q, N, consume=2)
         _same(flow, _decode(kc, cache, q, N, consume=0))
         o_out, o_idx, o_w, o_dr = oracle.decode_topn(q, k, v, b, n, n, h, s, N, False, True)
         for slot in range(b * n):

@@ -3,9 +3,10 @@
 Two paths for the prefill V of an offloaded layer (kc_set_tuning
 "prefill_stage"):
 * 1 (default): the append kernel writes V into an HBM stage; offload_prefill_v
-  hands the stage to the copy engine (one cudaMemcpy2DAsync D2H on the
-  cache's offload stream), so the transfer runs behind the next layer's work
-  -- the paper's overlapped offload (Eq. 1-2, perf_model.cpp:147-162);
+  sends the stage to the host arena on the cache's offload stream -- an SM
+  copy kernel for the (managed) arena, the copy engine for pinned layers -- so
+  the transfer runs behind the next layer's work: the paper's overlapped
+  offload (Eq. 1-2, perf_model.cpp:147-162);
 * 0: the append kernel writes V straight into the host arena (SM-issued PCIe
   stores, the r01 path): the transfer sits inside the append.
 
@@ -79,21 +80,24 @@ def main():
 
     rec = {"config": f"C2 layer prefill: batch {b}, {n}x{h}, {s} positions, fp16, chunks of {chunk}",
            "gpu": torch.cuda.get_device_name(0), "v_bytes_per_layer": 2 * b * s * d}
-    # 1. D2H rate of one staged offload
-    cache = make(False, 1)
-    append_layer(cache, 0)
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    cache.offload_prefill_v(0)
-    cache.sync()
-    dt = time.perf_counter() - t0
-    rec["staged_offload_ms"] = dt * 1e3
-    rec["staged_offload_gbs"] = 2 * b * s * d / dt / 1e9
-    rec["v_arena"] = cache.v_arena_kind()
-    cache.close()
+    # 1. D2H rate of one staged offload (SM copy kernel into the managed arena,
+    # by grid size)
+    rec["staged_offload_gbs"] = {}
+    for ctas in (8, 16, 32, 64):
+        cache = make(False, 1)
+        cache.set_tuning("stage_copy_ctas", ctas)
+        append_layer(cache, 0)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        cache.offload_prefill_v(0)
+        cache.sync()
+        dt = time.perf_counter() - t0
+        rec["staged_offload_gbs"][ctas] = 2 * b * s * d / dt / 1e9
+        rec["v_arena"] = cache.v_arena_kind()
+        cache.close()
     # 2. timelines
     rows = {}
-    for mode, resident, stage in (("v_in_hbm", True, 1), ("mapped_stores", False, 0), ("staged_copy_engine", False, 1)):
+    for mode, resident, stage in (("v_in_hbm", True, 1), ("mapped_stores", False, 0), ("staged", False, 1)):
         cache = make(resident, stage)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
