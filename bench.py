@@ -178,7 +178,7 @@ def config_block(cfg, args, world, shard):
         k_gpu = 2 * L * units * cfg["s"] * cfg["h"]
     return {"workload": cfg["workload"], "config": args.config, "layers": L, "global_batch": gb,
             "n_heads": cfg["n_heads"], "n_kv_heads": n_kv, "head_dim": cfg["h"], "s": cfg["s"],
-            "top_n": cfg["top_n"], "shard": shard, "parallelism": par,
+            "top_n": cfg["top_n"], "shard": shard, "parallelism": par, "data_dist": args.dist,
             "l2": "inputs larger than L2 (%.1f GiB K per GPU)" % (k_gpu / 2**30)}
 
 
@@ -217,7 +217,8 @@ class RankWorkload:
     sequences (data seeded per rank); "units": the rank's (batch, kv head)
     units of the global batch (sharding.UnitShard; the global data, sliced)."""
 
-    def __init__(self, kc, torch, cfg, dev, rank, world, shard, resident=False, tune=(), extra_seq=0):
+    def __init__(self, kc, torch, cfg, dev, rank, world, shard, resident=False, tune=(), extra_seq=0,
+                 dist="uniform"):
         from paper_2404_18057_b200.sharding import UnitShard, gpu_numa_node
         L, B, n, n_kv, h, s = (cfg[k] for k in ("n_layers", "batch", "n_heads", "n_kv", "h", "s"))
         G = n // n_kv
@@ -243,7 +244,20 @@ class RankWorkload:
         kbuf = torch.empty(s * B, n_kv * h, dtype=torch.float16, device=dev)
         vbuf = torch.empty_like(kbuf)
         for layer in range(L):
-            kc.fill_uniform(kbuf, SEED_K + 100 * layer + seed_off)
+            if dist == "peaked":
+                # SURVEY 8(d)'s realistic locality (verify.cpp:417-431): keys
+                # nearly orthogonal to q except 24 planted hot positions per
+                # (batch, kv head), each a constant row in [6, 8]
+                import numpy as np
+                kc.fill_uniform(kbuf, SEED_K + 100 * layer + seed_off, lo=-0.05, hi=0.05)
+                rng = np.random.default_rng(SEED_K + 100 * layer + seed_off)
+                hot = torch.as_tensor(np.concatenate([rng.choice(s, 24, replace=False) for _ in range(B * n_kv)]),
+                                      device=dev)
+                unit = torch.arange(B * n_kv, device=dev).repeat_interleave(24)
+                vals = torch.as_tensor(rng.uniform(6.0, 8.0, B * n_kv * 24), dtype=torch.float16, device=dev)
+                kbuf.view(s, B * n_kv, h)[hot, unit, :] = vals[:, None]
+            else:
+                kc.fill_uniform(kbuf, SEED_K + 100 * layer + seed_off)
             kc.fill_uniform(vbuf, SEED_V + 100 * layer + seed_off)
             if self.shard is None:
                 self.cache.append_kv_device(layer, kbuf, vbuf)
@@ -259,7 +273,10 @@ class RankWorkload:
         self.qs = []
         for layer in range(L):
             q16 = torch.empty(B, n * h, dtype=torch.float16, device=dev)
-            kc.fill_uniform(q16, SEED_Q + 100 * layer + seed_off)
+            if dist == "peaked":
+                kc.fill_uniform(q16, SEED_Q + 100 * layer + seed_off, lo=0.5, hi=1.0)
+            else:
+                kc.fill_uniform(q16, SEED_Q + 100 * layer + seed_off)
             q = q16.float()
             self.qs.append(q if self.shard is None else self.shard.q_rows(q).contiguous())
 
@@ -376,7 +393,7 @@ def run_ours(args, cfg):
         sys.exit(3)
     t0 = time.time()
     wl = RankWorkload(kc, torch, cfg, dev, rank, world, shard, tune=args.tune,
-                      extra_seq=0 if args.no_engine else ENGINE_STEPS + 2)
+                      extra_seq=0 if args.no_engine else ENGINE_STEPS + 2, dist=args.dist)
     cache, qs, b, d, slots = wl.cache, wl.qs, wl.b, wl.d, wl.slots
     numa = wl.numa
     v_arena = cache.v_arena_kind()
@@ -531,7 +548,9 @@ def run_ours(args, cfg):
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "weak" if shard == "batch" else "strong",
         "vs_baseline": None, "dtype": "f16 storage / f32 accumulate",
-        "data": "synthetic (SeededRng SplitMix64 U[-1,1], fp16-rounded)",
+        "data": ("synthetic (SeededRng SplitMix64 U[-1,1], fp16-rounded)" if args.dist == "uniform" else
+                 "synthetic, peaked: K U[-0.05,0.05] with 24 hot rows in [6,8] per (batch, kv head), q U[0.5,1], "
+                 "V U[-1,1], fp16-rounded"),
         "config": config_block(cfg, args, world, shard),
         "placement": {"pipeline": ("dataflow: a persistent consumer grid selects, recalls and reduces each (batch, "
                                    "kv head) row while the scoring streams the later rows (kc_consume.cu)" if flow else
@@ -617,6 +636,8 @@ def main():
     ap.add_argument("--no-full-kv", action="store_true", help="skip the full-KV-in-HBM comparator")
     ap.add_argument("--no-engine", action="store_true", help="skip the engine-realistic (per-layer) step")
     ap.add_argument("--tune", action="append", default=[], help="kc_set_tuning key=value")
+    ap.add_argument("--dist", default="uniform", choices=["uniform", "peaked"],
+                    help="synthetic K/q: U[-1,1], or near-orthogonal keys with 24 planted hot positions per row")
     ap.add_argument("--shard", default="auto", choices=["auto", "batch", "units"],
                     help="N>1: own batch per rank (weak) or (batch, kv head) units of one batch (strong)")
     args = ap.parse_args()

@@ -89,8 +89,9 @@ def main():
             nc = min(N, s)
             k_bytes = 2 * b * n * s * h
             v_bytes = 2 * b * n * nc * h
-            rec = {"s": s, "top_n": N, "path": "dataflow consumer (pipelined); per-kernel times from the "
-                                               "stream-ordered kernels run serially", "s_over_n": s / nc, "ms_per_step": ms, "tokens_per_s": b / (ms * 1e-3),
+            flow = s >= 16384 and min(N, s) <= 256  # the store's auto policy (kc_capi.cu decode_topn_impl)
+            rec = {"s": s, "top_n": N, "path": ("dataflow consumer" if flow else "stream-ordered") +
+                   " (default policy); per-kernel *_us from the stream-ordered kernels run serially", "s_over_n": s / nc, "ms_per_step": ms, "tokens_per_s": b / (ms * 1e-3),
                    "per_layer_us": 1e3 * ms / L, "k_bytes_per_layer": k_bytes, "vsel_bytes_per_layer": v_bytes,
                    "score_gbs": k_bytes / (per["score_us"] * 1e-6) / 1e9,
                    "recall_gbs": v_bytes / (per["recall_us"] * 1e-6) / 1e9,
