@@ -265,6 +265,7 @@ struct kc_cache {
   // layer-by-layer step: 372 vs 425 us at 64 -- fewer CTAs queue fewer PCIe
   // reads ahead of the last rows')
   int consume_ctas = 0;
+  int select_cached = 1;  // stream-ordered GQA: one-row CTAs with cached selection values
   int consume_dbg = 0;    // development probe: consumer phase timestamps (kc_debug_read "consume")
   DevBuf cons_dbg;
   // per-kernel CUDA-event timing (kc_profile): [kind] -> (start, stop) pairs
@@ -885,9 +886,35 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
       c->timed(1, st, [&] {
         if (cand) {
           if (!kc::select_cand_launch(sp, st)) fail(KC_ECUDA, "candidate selection unavailable for this shape");
-        } else {
-          kc::select_launch(sp, st);
+          return;
         }
+        // GQA launches of more rows than SMs: select_reg needs > 1 wave of its
+        // SM-wide CTAs, the cached one-row kernel holds two rows per SM (C3
+        // pipelined: 41.7 -> 37.1 us per layer; the engine's 128-row groups
+        // stay on select_reg, 337 vs 356 us per layer)
+        if (c->G > 1 && c->select_cached && !c->select_global && nr > kc::sm_count() &&
+            kc::consume_supported((int)c->G, (int)c->h)) {
+          kc::ConsumeParams cp{};
+          cp.logits = sp.logits;
+          cp.partials = sp.partials;
+          cp.idx = sp.idx;
+          cp.w = sp.w;
+          cp.dropped = sp.dropped;
+          cp.norm = sp.norm;
+          cp.lstride = sp.lstride;
+          cp.s = sp.s;
+          cp.nc = sp.nc;
+          cp.n_kv = sp.n_kv;
+          cp.G = sp.G;
+          cp.n_splits = sp.n_splits;
+          cp.max_splits = sp.max_splits;
+          cp.row0 = sp.row0;
+          cp.rows = sp.rows;
+          cp.keep_logits = sp.keep_logits;
+          cp.h = (int)c->h;
+          if (kc::select_rows_cached_launch(cp, st)) return;
+        }
+        kc::select_launch(sp, st);
       });
       CK(cudaEventRecord(c->ev_sel[slot], st));
       if (side != st) CK(cudaStreamWaitEvent(side, c->ev_sel[slot], 0));
@@ -1659,6 +1686,7 @@ int kc_set_tuning(kc_cache* c, const char* key, int64_t value) {
 
 
     else if (k == "consume_dbg") c->consume_dbg = value ? 1 : 0;
+    else if (k == "select_cached") c->select_cached = value ? 1 : 0;
     else if (k == "consume_ctas") {
       if (value < 0) fail(KC_EARG, "consume_ctas must be >= 0 (0 = auto)");
       c->consume_ctas = (int)value;

@@ -53,6 +53,7 @@ constexpr int kWsm = 2048;               // weights staged in smem when G*nc fit
 constexpr int kFastMaxNc = 1024;         // 8 warps x 128 group maxima
 constexpr int kMaxGq = 32;               // q heads per kv head (G*h <= 1024)
 constexpr int kRedG = 8;                 // heads reduced per finish round
+constexpr size_t kCachedSmemMax = 112 * 1024;  // select_rows_cached: two CTAs per SM
 
 struct CShared {
   union {
@@ -212,6 +213,7 @@ struct RowKeys {
   int G;
   const float* M;      // shared
   const float* rZ;
+  float* kcache = nullptr;  // shared-memory copy of the row's values (pass 1 -> pass 2), or null
   static constexpr int kR = GQ > 0 ? GQ : 1;  // raw float4 per position quad
   // loads in flight per lane in a streaming pass: U position quads
   static constexpr int U = GQ == 1 ? 8 : (GQ == 2 ? 4 : (GQ == 4 ? 2 : 1));
@@ -401,8 +403,12 @@ __device__ int cands_passes(const ConsumeParams& p, CShared& S, const RowCtx& r,
     float f[U][4];
     rk.batch(w0, w1, it0, n_it, lane, f);
 #pragma unroll
-    for (int u = 0; u < U; ++u)
+    for (int u = 0; u < U; ++u) {
       gmf[(it0 + u) & 3] = fmaxf(gmf[(it0 + u) & 3], fmaxf(fmaxf(f[u][0], f[u][1]), fmaxf(f[u][2], f[u][3])));
+      if (rk.kcache && it0 + u < n_it)
+        *reinterpret_cast<float4*>(rk.kcache + w0 + (it0 + u) * 128 + 4 * lane) =
+            make_float4(f[u][0], f[u][1], f[u][2], f[u][3]);
+    }
   }
   KC_STAMP(2);
   uint32_t gm[4];
@@ -418,7 +424,20 @@ __device__ int cands_passes(const ConsumeParams& p, CShared& S, const RowCtx& r,
   const uint32_t lt = lanemask_lt();
   for (int it0 = 0; it0 < n_it; it0 += U) {
     float f[U][4];
-    rk.batch(w0, w1, it0, n_it, lane, f);
+    if (rk.kcache) {  // the values pass 1 kept (the same bits; invalid positions stayed kInvalid)
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const float4 x = it0 + u < n_it ? *reinterpret_cast<const float4*>(rk.kcache + w0 + (it0 + u) * 128 + 4 * lane)
+                                        : make_float4(RowKeys<GQ>::kInvalid, RowKeys<GQ>::kInvalid,
+                                                      RowKeys<GQ>::kInvalid, RowKeys<GQ>::kInvalid);
+        f[u][0] = x.x;
+        f[u][1] = x.y;
+        f[u][2] = x.z;
+        f[u][3] = x.w;
+      }
+    } else {
+      rk.batch(w0, w1, it0, n_it, lane, f);
+    }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const bool c0 = f[u][0] >= tau_f, c1 = f[u][1] >= tau_f, c2 = f[u][2] >= tau_f, c3 = f[u][3] >= tau_f;
@@ -787,60 +806,106 @@ __device__ __forceinline__ void wait_row(const ConsumeParams& p, int row) {
   __syncthreads();
 }
 
+// One row's selection (stats, bound, candidates, exact select, dropped mass /
+// renormaliser, dead-logit discard): shared by the consumer and the
+// stream-ordered cached row selection. kcache: shared memory for the row's
+// selection values (pass 1 -> pass 2), or null.
+template <int GQ>
+__device__ __forceinline__ void select_row(const ConsumeParams& p, CShared& S, const RowCtx& r,
+                                           float* kcache = nullptr) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int G = r.G, n_q = r.n_q;
+  for (int g = warp; g < G; g += kCW) {
+    float m, z;
+    softmax_stats<true>(p.partials + ((size_t)r.b * n_q + r.kvh * G + g) * p.max_splits, p.n_splits, lane, m, z);
+    if (lane == 0) {
+      S.M[g] = m;
+      S.Z[g] = z;
+      S.rZ[g] = 1.0f / z;
+    }
+  }
+  __syncthreads();
+  KC_STAMP(1);
+  RowKeys<GQ> rk;
+  rk.lbase = p.logits + ((size_t)r.b * n_q + r.kvh * G) * p.lstride;
+  rk.lstride = p.lstride;
+  rk.G = G;
+  rk.M = S.M;
+  rk.rZ = S.rZ;
+  rk.kcache = kcache;
+  if (!select_fast(p, S, r, rk)) {
+    __syncthreads();
+    select_exact(p, S, r, rk);
+  }
+  __syncthreads();
+  KC_STAMP(4);
+  finish_rows(p, S, r);
+  KC_STAMP(5);
+  if (!p.keep_logits) {
+    // the row's logits are dead: drop them from L2 without write-back
+    const int lines = (p.s * 4 + 127) / 128;
+    for (int e = threadIdx.x; e < G * lines; e += kCT) {
+      const int g = e / lines, l = e - g * lines;
+      discard_l2_line(reinterpret_cast<const char*>(rk.lbase + (size_t)g * p.lstride) + (size_t)l * 128);
+    }
+  }
+}
+
+__device__ __forceinline__ RowCtx row_ctx(const ConsumeParams& p, int row) {
+  RowCtx r;
+  r.row = row;
+  r.b = row / p.n_kv;
+  r.kvh = row - r.b * p.n_kv;
+  r.G = p.G;
+  r.n_q = p.n_kv * p.G;
+  r.nc = p.nc;
+  r.s = p.s;
+  r.wsm_ok = p.G * p.nc <= kWsm;
+  return r;
+}
+
 template <typename T, int GQ>
 __global__ void __maxnreg__(88) consume_kernel(const ConsumeParams p) {
   __shared__ CShared S;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int G = p.G, n_q = p.n_kv * G;
   for (int row = p.row0 + blockIdx.x; row < p.row0 + p.rows; row += gridDim.x) {
-    RowCtx r;
-    r.row = row;
+    RowCtx r = row_ctx(p, row);
     KC_STAMP(7);
     wait_row(p, row);
     KC_STAMP(0);
-    r.b = row / p.n_kv;
-    r.kvh = row - r.b * p.n_kv;
-    r.G = G;
-    r.n_q = n_q;
-    r.nc = p.nc;
-    r.s = p.s;
-    r.wsm_ok = G * p.nc <= kWsm;
-    for (int g = warp; g < G; g += kCW) {
-      float m, z;
-      softmax_stats<true>(p.partials + ((size_t)r.b * n_q + r.kvh * G + g) * p.max_splits, p.n_splits, lane, m, z);
-      if (lane == 0) {
-        S.M[g] = m;
-        S.Z[g] = z;
-        S.rZ[g] = 1.0f / z;
-      }
-    }
-    __syncthreads();
-    KC_STAMP(1);
-    RowKeys<GQ> rk;
-    rk.lbase = p.logits + ((size_t)r.b * n_q + r.kvh * G) * p.lstride;
-    rk.lstride = p.lstride;
-    rk.G = G;
-    rk.M = S.M;
-    rk.rZ = S.rZ;
-    if (!select_fast(p, S, r, rk)) {
-      __syncthreads();
-      select_exact(p, S, r, rk);
-    }
-    __syncthreads();
-    KC_STAMP(4);
-    finish_rows(p, S, r);
-    KC_STAMP(5);
-    if (!p.keep_logits) {
-      // the row's logits are dead: drop them from L2 without write-back
-      const int lines = (p.s * 4 + 127) / 128;
-      for (int e = threadIdx.x; e < G * lines; e += kCT) {
-        const int g = e / lines, l = e - g * lines;
-        discard_l2_line(reinterpret_cast<const char*>(rk.lbase + (size_t)g * p.lstride) + (size_t)l * 128);
-      }
-    }
-    if (p.v) recall_row<T>(p, S, r);  // null: selection only (stream-ordered path)
+    select_row<GQ>(p, S, r);
+    if (p.v) recall_row<T>(p, S, r);  // null: selection only
     KC_STAMP(6);
   }
+}
+
+// Stream-ordered GQA selection: one row per CTA, the row's selection values
+// (sum_g p_g, G exp per position) computed once in pass 1 and kept in shared
+// memory for pass 2; two CTAs per SM hold all 256 rows of C3 in one wave
+// (select_reg_kernel: one 1024-thread CTA per SM, 1.73 waves).
+template <int GQ>
+__global__ void __launch_bounds__(kCT, 2) select_rows_cached_kernel(const ConsumeParams p) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  CShared& S = *reinterpret_cast<CShared*>(smem_raw);
+  float* kc = reinterpret_cast<float*>(smem_raw + ((sizeof(CShared) + 15) & ~size_t(15)));
+  for (int row = p.row0 + blockIdx.x; row < p.row0 + p.rows; row += gridDim.x)
+    select_row<GQ>(p, S, row_ctx(p, row), kc);
+}
+
+template <int GQ>
+bool launch_cached(const ConsumeParams& p, size_t smem, cudaStream_t st) {
+  static int configured[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (configured[dev & 63] < (int)smem) {
+    if (cudaFuncSetAttribute(select_rows_cached_kernel<GQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    configured[dev & 63] = (int)smem;
+  }
+  select_rows_cached_kernel<GQ><<<p.rows, kCT, smem, st>>>(p);
+  return true;
 }
 
 template <typename T>
@@ -855,6 +920,18 @@ void launch_g(const ConsumeParams& p, int grid, cudaStream_t st) {
 }
 
 }  // namespace
+
+bool select_rows_cached_launch(const ConsumeParams& p, cudaStream_t st) {
+  // the cache covers every position a warp segment can touch (s + 127)
+  const size_t smem = ((sizeof(CShared) + 15) & ~size_t(15)) + ((size_t)p.s + 128) * sizeof(float);
+  if (smem > kCachedSmemMax) return false;
+  switch (p.G) {
+    case 2: return launch_cached<2>(p, smem, st);
+    case 4: return launch_cached<4>(p, smem, st);
+    case 8: return launch_cached<8>(p, smem, st);
+    default: return false;
+  }
+}
 
 bool consume_supported(int G, int h) { return G >= 1 && G <= kMaxGq && G * h <= 1024 && h >= 1; }
 

@@ -131,6 +131,10 @@ struct ConsumeParams {
   uint64_t* dbg;           // development probe: [rows][8] phase timestamps (ns), or null
 };
 bool consume_supported(int G, int h);
+// stream-ordered GQA row selection with the selection values cached in shared
+// memory (one row per CTA); false when the shape is outside it (G not 2/4/8,
+// rows too long for the cache) -- the caller then uses select_launch
+bool select_rows_cached_launch(const ConsumeParams& p, cudaStream_t st);
 // grid: persistent CTAs (<= rows); vdtype: V storage dtype
 void consume_launch(const ConsumeParams& p, int vdtype, int grid, cudaStream_t st);
 

@@ -19,7 +19,7 @@ from tests.test_gpu_parity import build_cache, compare_all
 pytestmark = pytest.mark.gpu
 
 
-DEFAULTS = {"consume": 1, "consume_ctas": 0}
+DEFAULTS = {"consume": 1, "consume_ctas": 0, "select_cached": 1}
 
 
 def _decode(kc, cache, q, N, renorm=False, reverse=False, **tune):
@@ -147,3 +147,26 @@ def test_consumer_tie_flood_and_underflow(kc, oracle):
         for slot in range(b * n):
             np.testing.assert_array_equal(flow.selection.indices[slot], o_idx[slot])
         cache.close()
+
+
+@pytest.mark.parametrize("case", [(40, 8, 4, 3000, 64, "f16"), (160, 8, 1, 1500, 32, "bf16"),
+                                  (80, 8, 2, 8192, 128, "f16"), (80, 4, 2, 333, 32, "f16")],
+                         ids=["G2", "G8", "G4-8k", "G2-short"])
+def test_cached_gqa_selection_bitwise(kc, oracle, case):
+    """The stream-ordered GQA selection with shared-memory-cached selection
+    values (select_rows_cached_kernel, default) against select_reg_kernel
+    (select_cached 0) and the consumer: bit for bit. The cached kernel serves
+    launches of more rows than SMs (160 (batch, kv head) rows here)."""
+    b, n, n_kv, s, N, dtype = case
+    h = 128
+    cache, ks, vs = build_cache(kc, b, n, n_kv, h, s, dtype)
+    q = synth_matrix(3, b, n * h, dtype=dtype)
+    for renorm in (False, True):
+        cached = _decode(kc, cache, q, N, renorm, consume=0)
+        reg = _decode(kc, cache, q, N, renorm, consume=0, select_cached=0)
+        flow = _decode(kc, cache, q, N, renorm, consume=2)
+        _same(cached, reg)
+        _same(flow, reg)
+    if s <= 1000:
+        compare_all(oracle, cached, q, ks[0], vs[0], b, n, n_kv, h, s, N, True)
+    cache.close()
