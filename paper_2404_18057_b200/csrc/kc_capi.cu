@@ -185,6 +185,7 @@ struct kc_cache {
   cudaStream_t in_st = nullptr;  // host-mode q uploads (off the scoring stream)
   cudaEvent_t ev_q0 = nullptr, ev_qall = nullptr;
   cudaStream_t main_st = nullptr, side_st = nullptr, out_st = nullptr;
+  cudaStream_t cons_st = nullptr;  // dataflow with a separate recall: the consumer's stream
   cudaEvent_t ev_start = nullptr, ev_end = nullptr, ev_sel[kRing] = {}, ev_rec[kRing] = {},
               ev_out[kRing] = {}, ev_cp[kRing] = {},
               ev_stats = nullptr;
@@ -265,7 +266,11 @@ struct kc_cache {
   // layer-by-layer step: 372 vs 425 us at 64 -- fewer CTAs queue fewer PCIe
   // reads ahead of the last rows')
   int consume_ctas = 0;
-  int select_cached = 1;  // stream-ordered GQA: one-row CTAs with cached selection values
+  int select_cached = 1;
+  // dataflow recall: -1 auto (inside the consumer for single-layer calls, the
+  // recall kernel on the side stream for multi-layer calls), 1 / 0 force
+  int consume_recall = -1;
+  int flow_recall_ctas = 24;  // recall grid beside the select-only consumer (C2: 24 326 us, 32 334 us per layer)  // stream-ordered GQA: one-row CTAs with cached selection values
   int consume_dbg = 0;    // development probe: consumer phase timestamps (kc_debug_read "consume")
   DevBuf cons_dbg;
   // per-kernel CUDA-event timing (kc_profile): [kind] -> (start, stop) pairs
@@ -422,6 +427,7 @@ void destroy(kc_cache* c) {
   cudaSetDevice(c->device);
   if (c->main_st) cudaStreamSynchronize(c->main_st);
   if (c->side_st) cudaStreamSynchronize(c->side_st);
+  if (c->cons_st) cudaStreamSynchronize(c->cons_st);
   if (c->out_st) cudaStreamSynchronize(c->out_st);
   if (c->off_st) cudaStreamSynchronize(c->off_st);
   cudaDeviceSynchronize();
@@ -470,6 +476,7 @@ void destroy(kc_cache* c) {
   if (c->step_exec) cudaGraphExecDestroy(c->step_exec);
   if (c->main_st) cudaStreamDestroy(c->main_st);
   if (c->side_st) cudaStreamDestroy(c->side_st);
+  if (c->cons_st) cudaStreamDestroy(c->cons_st);
   delete c;
 }
 
@@ -718,7 +725,10 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
   // scoring of layer i+1. A ring of kRing selection slots orders the two.
   cudaStream_t side = c->pipeline ? c->side_st : st;
   CK(cudaEventRecord(c->ev_start, st));
-  if (side != st) CK(cudaStreamWaitEvent(side, c->ev_start, 0));
+  if (side != st) {
+    CK(cudaStreamWaitEvent(side, c->ev_start, 0));
+    CK(cudaStreamWaitEvent(c->cons_st, c->ev_start, 0));
+  }
 
   for (uint64_t i = 0; i < n; ++i) {
     const int slot = (int)(i % kRing);
@@ -763,7 +773,15 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
       if (c->cons_pending[ls]) CK(cudaStreamWaitEvent(st, c->ev_cons[ls], 0));
       c->cons_dirty = true;
       enqueue_score(c, layer, q32, g, st, 0, rows_i, false, ls, c->row_done[ls].as<uint32_t>());
-      cudaStream_t cs = side;
+      // Multi-layer calls: the consumer selects only (its own stream) and the
+      // recall + P.V of the layer runs as the stream-ordered recall kernel on
+      // the side stream under the next layer's scoring -- a consumer that also
+      // recalls slows the scoring it runs beside (C2: 334-348 vs 310 us per
+      // layer, r02). Single-layer calls (the engine's layer-by-layer step)
+      // recall inside the consumer, row by row, so the layer ends shortly after
+      // its scoring.
+      const bool own_recall = c->consume_recall < 0 ? n == 1 : c->consume_recall != 0;
+      cudaStream_t cs = (own_recall || side == st) ? side : c->cons_st;
       if (cs != st) {
         // ring slot `slot` is rewritten: the output copies of layer i-kRing must be done
         if (i >= (uint64_t)kRing) {
@@ -792,7 +810,7 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
       cp.row0 = 0;
       cp.rows = rows_i;
       cp.keep_logits = c->keep_logits;
-      cp.v = c->v_layer(layer);
+      cp.v = own_recall ? c->v_layer(layer) : nullptr;
       cp.out = io_device ? o.out : c->out_tmp[slot].as<float>();
       cp.max_seq = (int64_t)c->cfg.max_seq;
       cp.h = (int)c->h;
@@ -804,13 +822,34 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
         c->cons_dbg.ensure(c->rows * 8 * sizeof(uint64_t));
         cp.dbg = c->cons_dbg.as<uint64_t>();
       }
-      const int ctas = c->consume_ctas > 0 ? c->consume_ctas : (n == 1 ? 40 : 64);
+      const int ctas = c->consume_ctas > 0 ? c->consume_ctas : (own_recall ? 40 : 32);
       c->timed(1, cs, [&] { kc::consume_launch(cp, c->dtype, ctas, cs); });
       c->cons_dirty = false;
       ++c->cons_seq;
       CK(cudaEventRecord(c->ev_cons[ls], cs));
       c->cons_pending[ls] = true;
       CK(cudaEventRecord(c->ev_sel[slot], cs));
+      if (!own_recall) {
+        if (side != cs) CK(cudaStreamWaitEvent(side, c->ev_sel[slot], 0));
+        kc::RecallParams rp{};
+        rp.v = c->v_layer(layer);
+        rp.grid = c->flow_recall_ctas;
+        rp.pipelined = c->recall_pipe < 0 ? (c->G > 1 ? 1 : 0) : c->recall_pipe;
+        rp.idx = c->idx[slot].as<uint32_t>();
+        rp.w = c->w[slot].as<float>();
+        rp.norm = c->norm[slot].as<float>();
+        rp.out = cp.out;
+        rp.max_seq = (int64_t)c->cfg.max_seq;
+        rp.nc = g.nc;
+        rp.h = (int)c->h;
+        rp.n_kv = (int)c->n_kv;
+        rp.G = (int)c->G;
+        rp.rows = rows_i;
+        rp.renormalize = cp.renormalize;
+        rp.reverse = cp.reverse;
+        rp.row_offset = 0;
+        c->timed(2, side, [&] { kc::recall_launch(rp, c->dtype, side); });
+      }
     } else {
     // Row groups: score -> select -> recall per group of (batch, kv head)
     // rows, so the recall of group g overlaps the scoring of group g+1.
@@ -1102,6 +1141,7 @@ int kc_cache_create(const kc_config* cfg, uint64_t batch, uint64_t resident_laye
       CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
       CK(cudaStreamCreateWithFlags(&c->main_st, cudaStreamNonBlocking));
       CK(cudaStreamCreateWithPriority(&c->side_st, cudaStreamNonBlocking, hi));
+      CK(cudaStreamCreateWithPriority(&c->cons_st, cudaStreamNonBlocking, hi));
       CK(cudaStreamCreateWithFlags(&c->out_st, cudaStreamNonBlocking));
       CK(cudaStreamCreateWithFlags(&c->off_st, cudaStreamNonBlocking));
       for (int k = 0; k < 2; ++k) {
@@ -1344,6 +1384,7 @@ int kc_step_graph_begin(kc_cache* c, uint64_t top_n, void* stream) {
     // the cache's own streams must not hold work the captured step would
     // have to order against (their events would cross the capture boundary)
     CK(cudaStreamSynchronize(c->side_st));
+    CK(cudaStreamSynchronize(c->cons_st));
     CK(cudaStreamSynchronize(c->out_st));
     // everything before the capture is complete: the dataflow slot events
     // recorded outside it must not be waited on inside it
@@ -1636,7 +1677,7 @@ int kc_v_arena_kind(const kc_cache* c, int* kind) {
 int kc_sync(kc_cache* c) {
   return guarded([&] {
     set_dev(c);
-    for (cudaStream_t s : {c->main_st, c->side_st, c->out_st, c->in_st, c->off_st})
+    for (cudaStream_t s : {c->main_st, c->side_st, c->cons_st, c->out_st, c->in_st, c->off_st})
       if (s) CK(cudaStreamSynchronize(s));
     if (c->append_pending) CK(cudaEventSynchronize(c->ev_append));
   });
@@ -1687,6 +1728,11 @@ int kc_set_tuning(kc_cache* c, const char* key, int64_t value) {
 
     else if (k == "consume_dbg") c->consume_dbg = value ? 1 : 0;
     else if (k == "select_cached") c->select_cached = value ? 1 : 0;
+    else if (k == "consume_recall") c->consume_recall = value < 0 ? -1 : (value ? 1 : 0);
+    else if (k == "flow_recall_ctas") {
+      if (value < 0) fail(KC_EARG, "flow_recall_ctas must be >= 0 (0 = one CTA per row)");
+      c->flow_recall_ctas = (int)value;
+    }
     else if (k == "consume_ctas") {
       if (value < 0) fail(KC_EARG, "consume_ctas must be >= 0 (0 = auto)");
       c->consume_ctas = (int)value;

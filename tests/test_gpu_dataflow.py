@@ -19,7 +19,7 @@ from tests.test_gpu_parity import build_cache, compare_all
 pytestmark = pytest.mark.gpu
 
 
-DEFAULTS = {"consume": 1, "consume_ctas": 0, "select_cached": 1}
+DEFAULTS = {"consume": 1, "consume_ctas": 0, "select_cached": 1, "consume_recall": -1}
 
 
 def _decode(kc, cache, q, N, renorm=False, reverse=False, **tune):
@@ -99,11 +99,15 @@ def test_consumer_pipelined_layers_bitwise(kc, n_kv):
     cache.set_tuning("consume", 0)
     base = run_host()
     cache.set_tuning("consume", 2)
-    for _ in range(3):
+    # multi-layer calls: select-only consumer + the recall kernel (auto), and
+    # the consumer recalling itself
+    for own in (-1, 1, -1):
+        cache.set_tuning("consume_recall", own)
         got = run_host()
         for l in range(L):
             for key in ("out", "indices", "weights", "dropped"):
                 np.testing.assert_array_equal(got[l][key], base[l][key])
+    cache.set_tuning("consume_recall", -1)
     # device-resident calls on a user stream, back to back without a sync
     stream = torch.cuda.Stream()
     dq = [torch.from_numpy(q).cuda() for q in qs]
