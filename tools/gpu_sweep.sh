@@ -1,9 +1,7 @@
 mkdir -p gpurun_out
-O=gpurun_out/sweep_split2.txt
+O=gpurun_out/sweep_gqa_split.txt
 : > $O
-C2="--layers 16 --steps 10"
-for i in 1 2; do
-timeout 600 python tools/tune_sweep.py $C2 --grid consume_ctas=28,32,36,40 --grid recall_ctas=16,24,32 >> $O 2>&1
-done
-timeout 600 python tools/tune_sweep.py $C2 --grid recall_pipe=0,1 --grid recall_ctas=24,32 >> $O 2>&1
+C3="--layers 16 --steps 10 --batch 32 --kv 8 --s 16384"
+timeout 600 python tools/tune_sweep.py $C3 --grid consume=0 >> $O 2>&1
+timeout 600 python tools/tune_sweep.py $C3 --grid consume=2 --grid consume_recall=0 --grid consume_ctas=32,48,64,96 --grid flow_recall_ctas=24,32 >> $O 2>&1
 cat $O
