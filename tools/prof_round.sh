@@ -14,11 +14,15 @@ cap() {  # name, kernel regex, skip, extra bench args
       -o gpurun_out/prof_$1 -f $CMD $4 > gpurun_out/prof_$1_run.log 2>&1
   ncu -i gpurun_out/prof_$1.ncu-rep --page raw --csv > gpurun_out/prof_$1_raw.csv 2>/dev/null
 }
+if [ -z "$ONLY" ]; then
 cap score_fast score_fast 200 ""
 cap consume consume_kernel 60 ""
 cap score_mma_c3 score_mma 200 "--config c3"
-cap select_reg_c3 select_reg 60 "--config c3"
 cap recall_pv_c3 recall_pv 60 "--config c3"
+fi
+cap recall_pv recall_pv 60 ""
+cap select_cached_c3 select_rows_cached 60 "--config c3"
+[ -n "$ONLY" ] && exit 0
 # the full-KV comparator's fused kernel (bench's full_kv leg)
 ncu --set full --clock-control none --import-source on -k regex:full_fast -s 40 -c 1 \
     -o gpurun_out/prof_full_fast -f python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --no-engine \

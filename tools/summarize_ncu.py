@@ -85,9 +85,10 @@ def main():
     summary = {}
     c2 = "python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --no-full-kv --no-engine (C2)"
     captures = [("score_fast", "prof_score_fast", 0, c2),
-                ("consume", "prof_consume", 0, c2 + ": the dataflow consumer (selection + recall + P.V)"),
+                ("consume", "prof_consume", 0, c2 + ": the dataflow consumer, selecting only (multi-layer call)"),
+                ("recall_pv", "prof_recall_pv", 0, c2 + ": the recall kernel beside the select-only consumer"),
                 ("score_mma_c3", "prof_score_mma_c3", 0, c2.replace("(C2)", "--config c3")),
-                ("select_reg_c3", "prof_select_reg_c3", 0, "same (C3)"),
+                ("select_cached_c3", "prof_select_cached_c3", 0, "same (C3): the cached GQA row selection"),
                 ("recall_pv_c3", "prof_recall_pv_c3", 0, "same (C3)"),
                 ("full_fast", "prof_full_fast", 0, "python bench.py ... (C2 full-KV comparator leg, K+V in HBM)")]
     for k, repname, launch, cmd in captures:
