@@ -190,13 +190,22 @@ struct kc_cache {
               ev_out[kRing] = {}, ev_cp[kRing] = {},
               ev_stats = nullptr;
   bool cp_pending[kRing] = {};  // ev_cp[slot] guards a device-mode copy of that slot
-  // kc_append_kv_device enqueues on the caller's stream: ev_append marks the
-  // last such append; the cache's own streams wait on it before reading K/V
+  // Device-mode calls (kc_append_kv_device, device decode / full attention)
+  // enqueue on the caller's stream: ev_append marks the last of them; the
+  // cache's own streams -- and a device-mode call on another stream -- wait
+  // on it before touching K/V, logits or the selection ring. Not recorded
+  // inside a step-graph capture (a captured event cannot be waited on outside
+  // it; kc_step_graph_launch's caller orders the graph on its own stream).
   cudaEvent_t ev_append = nullptr;
   bool append_pending = false;
   void order_after_appends(cudaStream_t st) {
-    if (append_pending) CK(cudaStreamWaitEvent(st, ev_append, 0));
+    if (append_pending && !capture_st) CK(cudaStreamWaitEvent(st, ev_append, 0));
     order_after_offloads(st);
+  }
+  void mark_device_work(cudaStream_t st) {
+    if (capture_st) return;
+    CK(cudaEventRecord(ev_append, st));
+    append_pending = true;
   }
 
   // Prefill V staging (the paper's overlapped offload): the
@@ -691,8 +700,7 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
   set_dev(c);
   const bool io_device = flags & KC_IO_DEVICE;
   cudaStream_t st = io_device ? user_st : c->main_st;
-  if (!io_device) c->order_after_appends(st);
-  else c->order_after_offloads(st);
+  c->order_after_appends(st);
   const StepGeom g = geom(c, top_n);
   const uint64_t nc = (uint64_t)g.nc;
   const uint64_t slots = c->batch * c->n_q;
@@ -1050,6 +1058,7 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
       CK(cudaStreamWaitEvent(st, c->ev_end, 0));
     }
   }
+  if (io_device) c->mark_device_work(st);
   if (!io_device) {
     CK(cudaStreamSynchronize(st));
     for (uint64_t i = 0; i < n; ++i) {
@@ -1282,8 +1291,7 @@ int kc_decode_step(kc_cache* c, uint64_t layer, const void* q, const void* k_new
     if (!io_device && c->capture_st) fail(KC_ESTATE, "host-memory I/O inside a step graph capture");
     set_dev(c);
     cudaStream_t st = io_device ? (cudaStream_t)stream : c->main_st;
-    if (!io_device) c->order_after_appends(st);
-    else c->order_after_offloads(st);
+    c->order_after_appends(st);
     // engine.cpp:143 -- this step's K/V row of every batch row
     const uint64_t rows = c->batch;
     append_checks(c, layer, rows);
@@ -1332,6 +1340,7 @@ int kc_decode_step(kc_cache* c, uint64_t layer, const void* q, const void* k_new
     }
     c->step_host.h2d_bytes += o.h2d_bytes;
     c->step_host.selections += slots;
+    if (io_device) c->mark_device_work(st);  // after the StepStats join
     if (!io_device) CK(cudaStreamSynchronize(st));
   });
 }
@@ -1463,8 +1472,7 @@ int kc_decode_full(kc_cache* c, uint64_t layer, const void* q, int q_dtype, uint
     const bool io_device = flags & KC_IO_DEVICE;
     cudaStream_t st = io_device ? (cudaStream_t)stream : c->main_st;
     if (!io_device && c->capture_st) fail(KC_ESTATE, "host-memory I/O inside a step graph capture");
-    if (!io_device) c->order_after_appends(st);
-    else c->order_after_offloads(st);
+    c->order_after_appends(st);
     const StepGeom g = geom(c, 1, 1);  // fused full kernel: MHA split sizing
     const float* q32 = stage_q(c, 0, q, q_dtype, io_device, st);
     const uint64_t slots = c->batch * c->n_q;
@@ -1498,6 +1506,8 @@ int kc_decode_full(kc_cache* c, uint64_t layer, const void* q, int q_dtype, uint
       if (!io_device) {
         CK(cudaMemcpyAsync(out, c->out_tmp[0].p, slots * c->h * 4, cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
+      } else {
+        c->mark_device_work(st);
       }
       return;
     }
@@ -1521,6 +1531,7 @@ int kc_decode_full(kc_cache* c, uint64_t layer, const void* q, int q_dtype, uint
     pp.max_splits = c->max_splits;
     kc::pv_full_launch(pp, c->dtype, st);
     CK(cudaGetLastError());
+    if (io_device) c->mark_device_work(st);
     if (!io_device) {
       CK(cudaMemcpyAsync(out, c->out_tmp[0].p, slots * c->h * 4, cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));
