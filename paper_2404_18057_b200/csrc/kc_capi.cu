@@ -167,6 +167,12 @@ struct kc_cache {
   // logits/partials above), per-row split counters per slot, the consumer's
   // error word, and "slot s is free" events
   DevBuf logits_b, partials_b, row_done[2], cons_err;
+  // tcgen05 GQA scoring: one 2-D TMA tensor map of K per layer (kc_score_tc.cu)
+  struct alignas(64) KMap {
+    uint8_t bytes[128];
+    bool ok = false;
+  };
+  std::vector<KMap> kmaps;
   cudaEvent_t ev_cons[2] = {}, ev_scored = nullptr;
   bool cons_pending[2] = {};
   bool cons_dirty = false;   // a scoring launch signalled rows no consumer read
@@ -618,6 +624,12 @@ void enqueue_score(kc_cache* c, uint64_t layer, const float* q32, const StepGeom
   sp.stages = c->score_stages;
   sp.k_policy = c->k_policy;
   sp.use_mma = c->score_mma;
+  if (c->score_mma == 3 && kc::score_tc_supported(c->dtype, (int)c->h, (int)c->G)) {
+    if (c->kmaps.size() < c->layers.size()) c->kmaps.resize(c->layers.size());
+    auto& km = c->kmaps[layer];
+    if (!km.ok) km.ok = kc::encode_k_map(km.bytes, c->k_layer(layer), c->dtype, c->rows, c->cfg.max_seq);
+    sp.kmap = km.ok ? km.bytes : nullptr;
+  }
   // ~3 waves of CTAs ahead (one CTA per item, 3 per SM)
   sp.tlb_ahead = c->tlb_ahead >= 0 ? c->tlb_ahead
                                     : std::max(1, (3 * kc::sm_count() + g.n_splits - 1) / std::max(g.n_splits, 1));
@@ -1728,7 +1740,7 @@ int kc_set_tuning(kc_cache* c, const char* key, int64_t value) {
     }
     else if (k == "k_policy") c->k_policy = (int)value;
     else if (k == "tlb_ahead") c->tlb_ahead = (int)value;
-    else if (k == "score_mma") c->score_mma = (int)std::max<int64_t>(0, std::min<int64_t>(2, value));
+    else if (k == "score_mma") c->score_mma = (int)std::max<int64_t>(0, std::min<int64_t>(3, value));
     else if (k == "cand_force_fallback") c->cand_force_fallback = value ? 1 : 0;
     else if (k == "consume") {
       if (value < 0 || value > 2) fail(KC_EARG, "consume: 0 off, 1 MHA, 2 every supported shape");

@@ -207,6 +207,46 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
   return m;
 }
 
+// ---- GQA tensor-core scoring: q in NP parts of the MMA input type ------------
+// (score_mma_kernel, score_tc_kernel). fp16: q * 2^e = hi + lo (2^e puts the
+// head's max |q| at 2^14, both parts normal); bf16: three parts.
+// q split into NP parts of T; returns the scale to undo (2^-e for fp16)
+template <typename T>
+struct QSplit;
+template <>
+struct QSplit<__half> {
+  static constexpr int NP = 2;
+  __device__ static float prescale(float amax) {
+    if (!(amax > 0.0f) || !isfinite(amax)) return 1.0f;
+    return ldexpf(1.0f, 14 - ilogbf(amax));
+  }
+  __device__ static uint32_t pack(float x, float y) {
+    const __half2 h = __floats2half2_rn(x, y);
+    return *reinterpret_cast<const uint32_t*>(&h);
+  }
+  __device__ static float2 unpack(uint32_t w) {
+    return __half22float2(*reinterpret_cast<const __half2*>(&w));
+  }
+};
+template <>
+struct QSplit<__nv_bfloat16> {
+  static constexpr int NP = 3;
+  __device__ static float prescale(float) { return 1.0f; }
+  __device__ static uint32_t pack(float x, float y) {
+    const __nv_bfloat162 h = __floats2bfloat162_rn(x, y);
+    return *reinterpret_cast<const uint32_t*>(&h);
+  }
+  __device__ static float2 unpack(uint32_t w) {
+    return __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w));
+  }
+};
+
+
+// named barrier over `n` threads (bar.sync id, n)
+__device__ __forceinline__ void named_sync_n(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
 // ---- selection keys (kc_select.cu) -------------------------------------------
 // Order-preserving bits of a float; -0.0 and +0.0 compare equal, so they must
 // tie (one key).

@@ -44,6 +44,9 @@ struct ScoreParams {
   // dataflow (consume_launch): every CTA bumps row_done[row] (release) once
   // its split's logits and statistics are written; null: no signalling
   uint32_t* row_done;
+  // score_tc_kernel: the layer's K tensor map (CUtensorMap, host memory; see
+  // encode_k_map), or null
+  const void* kmap;
 };
 // row_done counters: one per kRowDoneStride words (a 128-B line per row)
 constexpr int kRowDoneStride = 32;
@@ -53,6 +56,12 @@ void score_launch(const ScoreParams& p, int dtype, cudaStream_t st);
 int score_pick_chunk(int s, int rows, int override_chunk, int G = 1);
 // SMs of the current device
 int sm_count();
+// GQA scoring on tcgen05 (kc_score_tc.cu): shapes it covers, the K tensor map
+// of one layer ([rows][max_seq][128] 16-bit, 64 x 128 SW128 boxes) written to
+// map_out (128 B, 64-B aligned), and the launch (false: not covered)
+bool score_tc_supported(int dtype, int h, int G);
+bool encode_k_map(void* map_out, const void* k_layer, int dtype, uint64_t rows, uint64_t max_seq);
+bool score_tc_launch(const ScoreParams& p, int dtype, cudaStream_t st);
 // whether the candidate-mode scoring kernel covers this shape
 bool score_cand_supported(int dtype, int h, int G, int chunk, int nc);
 

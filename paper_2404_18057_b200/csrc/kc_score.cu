@@ -387,37 +387,6 @@ __device__ __forceinline__ void mma_16816<__nv_bfloat16>(float (&d)[4], uint32_t
       : "r"(a0), "r"(0u), "r"(a2), "r"(0u), "r"(b0), "r"(b1));
 }
 
-// q split into NP parts of T; returns the scale to undo (2^-e for fp16)
-template <typename T>
-struct QSplit;
-template <>
-struct QSplit<__half> {
-  static constexpr int NP = 2;
-  __device__ static float prescale(float amax) {
-    if (!(amax > 0.0f) || !isfinite(amax)) return 1.0f;
-    return ldexpf(1.0f, 14 - ilogbf(amax));
-  }
-  __device__ static uint32_t pack(float x, float y) {
-    const __half2 h = __floats2half2_rn(x, y);
-    return *reinterpret_cast<const uint32_t*>(&h);
-  }
-  __device__ static float2 unpack(uint32_t w) {
-    return __half22float2(*reinterpret_cast<const __half2*>(&w));
-  }
-};
-template <>
-struct QSplit<__nv_bfloat16> {
-  static constexpr int NP = 3;
-  __device__ static float prescale(float) { return 1.0f; }
-  __device__ static uint32_t pack(float x, float y) {
-    const __nv_bfloat162 h = __floats2bfloat162_rn(x, y);
-    return *reinterpret_cast<const uint32_t*>(&h);
-  }
-  __device__ static float2 unpack(uint32_t w) {
-    return __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w));
-  }
-};
-
 // NCW consumer warps: 8 = two halves alternating stages (one CTA per SM at
 // 140 registers), 4 = every warp on every stage (two CTAs per SM)
 template <typename T, int STAGES, int NCW>
@@ -993,6 +962,8 @@ bool score_cand_supported(int dtype, int h, int G, int chunk, int nc) {
 }
 
 void score_launch(const ScoreParams& p, int dtype, cudaStream_t st) {
+  // GQA on tcgen05 (kc_score_tc.cu) when the caller passed the layer's map
+  if (p.use_mma == 3 && p.G >= 2 && p.cand_nc == 0 && score_tc_launch(p, dtype, st)) return;
   if (dtype == KC_F16 && try_fast<__half>(p, st)) return;
   if (dtype == KC_BF16 && try_fast<__nv_bfloat16>(p, st)) return;
   if (p.cand_nc > 0) {  // the caller checked score_cand_supported: never silently dense

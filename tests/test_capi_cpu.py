@@ -69,6 +69,10 @@ def test_kernels_are_sm100a_with_tma_bulk_copies():
     assert "UBLKCP" in sass            # cp.async.bulk (TMA) K staging
     assert "SYNCS" in sass             # mbarrier pipeline
     assert "score_fast_kernel" in sass and "select_reg_kernel" in sass and "recall_pv_kernel" in sass
+    assert "consume_kernel" in sass    # the dataflow consumer
+    # tcgen05 GQA scoring (kc_score_tc.cu): 2-D TMA loads, tensor-core MMA into
+    # TMEM, TMEM loads
+    assert "UTMALDG" in sass and "UTCHMMA" in sass and "LDTM" in sass
 
 
 def test_status_codes_match_the_python_mapping():
