@@ -13,10 +13,13 @@
 // (batch, kv-head) rows in order; each scoring CTA bumps its row's completion
 // counter (release) after its logits and split statistics are written. A small
 // persistent grid of these CTAs, launched on another stream, waits for a row's
-// counter to reach n_splits (acquire) and then selects + recalls + reduces that
-// row while the scoring streams the later rows' K. Selection and recall leave
-// the scoring stream's critical path (previously: score -> select -> recall in
-// stream order, the selection a full-GPU barrier-bound launch per layer).
+// counter to reach n_splits (acquire) and then selects (and, for single-layer
+// calls, recalls + reduces) that row while the scoring streams the later rows'
+// K. The selection leaves the scoring stream's critical path (previously:
+// score -> select in stream order, a full-GPU barrier-bound launch per layer).
+// Multi-layer calls leave the recall to recall_pv_kernel on a side stream
+// under the next layer's scoring: a consumer that also recalls slows the
+// scoring it runs beside.
 //
 // Selection per row with 256 threads, keys streamed from L2 (no register-
 // resident key array, so a consumer CTA fits beside two scoring CTAs):
@@ -29,9 +32,12 @@
 //      scan) into shared memory -- typically ~1.5 nc of them;
 //   4. exact radix select on the candidates, p-exact tie classification, block
 //      scans for position-ordered output (select_reg's fast path);
-//   anything the fast path cannot prove (nc > 1024, > 2048 candidates, p(tau)
-//   not a normal float, nc >= s) takes the streamed exact path: 3 radix passes
-//   over all keys + two ordered classification passes.
+//   anything the fast path cannot prove (nc > 1024, > 1024 candidates or > 128
+//   in one warp's segment, p(tau) not a normal float, nc >= s) takes the
+//   streamed exact path: 3 radix passes over all keys + two ordered
+//   classification passes.
+// select_rows_cached_kernel runs the same row selection stream-ordered for GQA
+// (one row per CTA, the selection values cached in shared memory).
 #include <cfloat>
 
 #include "kc_device.cuh"
@@ -63,7 +69,7 @@ struct CShared {
       uint32_t ckey[kCandCap];  // compacted, position order
       uint32_t cpos[kCandCap];
     } sel;
-    uint32_t hist[kCBins];      // aliases rkey (dead once compacted)
+    uint32_t hist[kCBins];      // aliases rkey / rpos (dead once compacted)
     uint8_t vbuf[kUnionBytes];  // recall: staged V rows
   } u;
   float wsm[kWsm];              // [G][nc] weights
