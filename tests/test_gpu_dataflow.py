@@ -174,3 +174,37 @@ def test_cached_gqa_selection_bitwise(kc, oracle, case):
     if s <= 1000:
         compare_all(oracle, cached, q, ks[0], vs[0], b, n, n_kv, h, s, N, True)
     cache.close()
+
+
+def test_device_calls_order_before_later_calls(kc):
+    """A device-mode call enqueued on one stream, then -- without a sync -- a
+    device-mode call on another stream and a host-mode call: the later calls
+    order after it (the store's device-work event), so every result equals a
+    synchronised single call."""
+    import torch
+    b, n, h, s, N, L = 2, 8, 128, 20000, 64, 3  # >= 16 k: the dataflow path
+    cache, ks, vs = build_cache(kc, b, n, n, h, s, "f16", n_layers=L)
+    qs = [synth_matrix(40 + l, b, n * h) for l in range(L)]
+    ref = [kc.decode_attention_topn(qs[l], cache, l, N, False) for l in range(L)]
+    nc = min(N, s)
+    sa, sb = torch.cuda.Stream(), torch.cuda.Stream()
+    dq = [torch.from_numpy(q).cuda() for q in qs]
+    torch.cuda.synchronize()
+
+    def outs():
+        return [{"out": torch.full((b, n * h), float("nan"), device="cuda"),
+                 "indices": torch.empty(b * n, nc, dtype=torch.int32, device="cuda"),
+                 "weights": torch.empty(b * n, nc, device="cuda"),
+                 "dropped": torch.empty(b * n, dtype=torch.float64, device="cuda")} for _ in range(L)]
+    oa, ob = outs(), outs()
+    for _ in range(2):
+        cache.decode_topn_layers_device(list(range(L)), dq, N, oa, stream=sa)
+        cache.decode_topn_layers_device(list(range(L)), dq, N, ob, stream=sb)
+        host = kc.decode_attention_topn(qs[1], cache, 1, N, False)  # host mode, main stream
+        np.testing.assert_array_equal(host.out, ref[1].out)
+    torch.cuda.synchronize()
+    for l in range(L):
+        for o in (oa, ob):
+            np.testing.assert_array_equal(o[l]["out"].cpu().numpy(), ref[l].out)
+            np.testing.assert_array_equal(o[l]["indices"].cpu().numpy().view(np.uint32), ref[l].selection.indices)
+    cache.close()
