@@ -588,7 +588,7 @@ def run_ours(args, cfg):
                 "d2h_bytes_per_step": L * (b * d * 4 + slots * nc * 8 + slots * 8), "ms_per_step": e2e_ms,
                 "path": "kc_decode_topn_layers with pinned host q / outputs (TieredKVCache.prepare_topn_layers_host: buffers bound once, one C-ABI call per step)"},
         "kernel_isolated_ms_per_launch": {("consume" if flow and k == "select" else k): iso[k][0] / max(iso[k][1], 1)
-                                          for k in iso if not (flow and k == "recall")},
+                                          for k in iso},
         "serial_step_ms": serial_ms,
         "gpu_launches": launches_per_layer * L * args.steps,
         "clocks": clocks,

@@ -963,7 +963,7 @@ bool score_cand_supported(int dtype, int h, int G, int chunk, int nc) {
 
 void score_launch(const ScoreParams& p, int dtype, cudaStream_t st) {
   // GQA on tcgen05 (kc_score_tc.cu) when the caller passed the layer's map
-  if (p.use_mma == 3 && p.G >= 2 && p.cand_nc == 0 && score_tc_launch(p, dtype, st)) return;
+  if (p.use_mma == 3 && p.cand_nc == 0 && score_tc_launch(p, dtype, st)) return;
   if (dtype == KC_F16 && try_fast<__half>(p, st)) return;
   if (dtype == KC_BF16 && try_fast<__nv_bfloat16>(p, st)) return;
   if (p.cand_nc > 0) {  // the caller checked score_cand_supported: never silently dense

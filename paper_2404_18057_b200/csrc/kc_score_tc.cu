@@ -346,7 +346,7 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }  // namespace
 
 bool score_tc_supported(int dtype, int h, int G) {
-  return (dtype == KC_F16 || dtype == KC_BF16) && h == 128 && G >= 2 && G <= 8;
+  return (dtype == KC_F16 || dtype == KC_BF16) && h == 128 && G >= 1 && G <= 8;
 }
 
 bool encode_k_map(void* map_out, const void* k_layer, int dtype, uint64_t rows, uint64_t max_seq) {
