@@ -51,6 +51,7 @@ CASES = [
     (1, 4, 4, 64, 2000, 40, "f16"),      # h = 64: generic scoring kernel
     (1, 4, 2, 128, 1500, 50, "f32"),     # fp32 storage: generic scoring kernel
     (1, 4, 4, 128, 40000, 128, "f16"),   # s > 32k (stream-ordered path: candidate mode)
+    (1, 8, 1, 128, 3000, 300, "f16"),    # G * N > 2048: weights read back from global memory
 ]
 
 

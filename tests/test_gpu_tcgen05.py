@@ -19,6 +19,7 @@ CASES = [
     (1, 8, 1, 2500, 32, "bf16"),    # G = 8, bf16: 24 q-part rows (N = 32)
     (1, 16, 4, 5000, 128, "bf16"),  # G = 4, bf16 (N = 16)
     (3, 8, 2, 129, 200, "f16"),     # N > s, one position past a stage
+    (2, 4, 4, 3000, 64, "f16"),     # MHA (one q head in two parts, N = 16)
 ]
 
 
