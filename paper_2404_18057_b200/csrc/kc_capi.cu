@@ -786,6 +786,13 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
         }
       }
       if (c->cons_dirty) {  // an earlier call threw between a scoring launch and its consumer
+        // earlier consumers may still be waiting on the counters: reset after them
+        if (side != st) {
+          for (cudaStream_t o : {c->side_st, c->cons_st}) {
+            CK(cudaEventRecord(c->ev_scored, o));
+            CK(cudaStreamWaitEvent(st, c->ev_scored, 0));
+          }
+        }
         for (int k = 0; k < 2; ++k)
           if (c->row_done[k].p) CK(cudaMemsetAsync(c->row_done[k].p, 0, c->row_done[k].bytes, st));
         c->cons_dirty = false;
@@ -1441,6 +1448,10 @@ int kc_step_graph_launch(kc_cache* c, void* stream) {
     if (e == cudaSuccess) e = cudaGraphLaunch(c->step_exec, st);
     cudaGraphDestroy(graph);
     CK(e);
+    // events recorded inside the capture are graph nodes: later calls order
+    // after the launched graph instead (its stream), not after them
+    c->cons_pending[0] = c->cons_pending[1] = false;
+    c->mark_device_work(st);
   });
 }
 

@@ -97,17 +97,20 @@ def test_decode_step_errors(kc):
     cache.close()
 
 
-@pytest.mark.parametrize("n,n_kv,dtype", [(4, 4, "f16"), (8, 2, "bf16")], ids=["mha-f16", "gqa-bf16"])
-def test_step_graph_equals_eager(kc, n, n_kv, dtype):
+@pytest.mark.parametrize("n,n_kv,dtype,consume", [(4, 4, "f16", 1), (8, 2, "bf16", 1), (4, 4, "f16", 2)],
+                         ids=["mha-f16", "gqa-bf16", "mha-f16-dataflow"])
+def test_step_graph_equals_eager(kc, n, n_kv, dtype, consume):
     """One CUDA Graph per decode step (kc_step_graph_begin / _launch): the
     captured-then-launched step writes the same outputs, bit for bit, and the
-    same StepStats, ledger bytes and cache rows as the eager calls."""
+    same StepStats, ledger bytes and cache rows as the eager calls (consume 2:
+    the dataflow consumer, eagerly beside its scoring, in the graph after it)."""
     import torch
     b, h, s0, N, L, steps = 2, 128, 500, 64, 3, 3
     tdt = {"f16": torch.float16, "bf16": torch.bfloat16}[dtype]
     runs = []
     for graph in (False, True):
         cache, ks, vs = build_cache(kc, b, n, n_kv, h, s0, dtype, resident=1, n_layers=L, max_seq=s0 + steps + 1)
+        cache.set_tuning("consume", consume)
         stream = torch.cuda.Stream()
         cache.step_stats(reset=True)
         outs, stats = [], []
