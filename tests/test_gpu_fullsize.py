@@ -154,3 +154,50 @@ def test_score_observer_rows(kc, oracle):
     kc.decode_attention_full(q, cache, 0, observer=lambda bi, hd, w: full_seen.append((bi, hd)))
     assert full_seen == [(bi, hd) for bi in range(b) for hd in range(n)]
     cache.close()
+
+
+@pytest.mark.timeout(900)
+@pytest.mark.parametrize("n_kv", [32, 8], ids=["c2", "c3"])
+def test_full_size_pipelined_layers_equal_single_calls(kc, n_kv):
+    """The bench's multi-layer call at full size -- MHA: the select-only
+    consumer + the recall kernel under the next layer's scoring; GQA: the
+    stream-ordered path with the cached row selection -- equals single-layer
+    calls (MHA: the recalling consumer, checked against the oracle above) bit
+    for bit, over 3 layers (both scoring slots, the selection ring)."""
+    import torch
+    b, n, h, s, N, L = (8, 32, 128, 32768, 128, 3) if n_kv == 32 else (32, 32, 128, 16384, 128, 3)
+    cfg = kc.small_config(L, n * h, n, s, kv_heads=n_kv)
+    cache = kc.TieredKVCache(cfg, b, kc.TierPlacement.kcache(0, L, 2, "f16"))
+    kb = torch.empty(s * b, n_kv * h, dtype=torch.float16, device="cuda")
+    vb = torch.empty_like(kb)
+    for l in range(L):
+        kc.fill_uniform(kb, 2 + 100 * l)
+        kc.fill_uniform(vb, 3 + 100 * l)
+        cache.append_kv_device(l, kb, vb)
+    torch.cuda.synchronize()
+    del kb, vb
+    for l in range(L):
+        cache.offload_prefill_v(l)
+    cache.begin_decode()
+    qs = []
+    for l in range(L):
+        q = torch.empty(b, n * h, dtype=torch.float16, device="cuda")
+        kc.fill_uniform(q, 1 + 100 * l)
+        qs.append(q.float())
+    nc = min(N, s)
+
+    def outs():
+        return [{"out": torch.full((b, n * h), float("nan"), device="cuda"),
+                 "indices": torch.empty(b * n, nc, dtype=torch.int32, device="cuda"),
+                 "weights": torch.empty(b * n, nc, device="cuda"),
+                 "dropped": torch.empty(b * n, dtype=torch.float64, device="cuda")} for _ in range(L)]
+    stream = torch.cuda.Stream()
+    multi, single = outs(), outs()
+    cache.decode_topn_layers_device(list(range(L)), qs, N, multi, stream=stream)
+    for l in range(L):
+        cache.decode_topn_layers_device([l], [qs[l]], N, [single[l]], stream=stream)
+    torch.cuda.synchronize()
+    for l in range(L):
+        for key in ("out", "indices", "weights", "dropped"):
+            assert torch.equal(multi[l][key], single[l][key]), (l, key)
+    cache.close()
