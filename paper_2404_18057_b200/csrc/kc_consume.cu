@@ -212,8 +212,9 @@ __device__ __forceinline__ void c_radix_threshold(CShared& S, Get&& get, int nc,
 // Selection key of position j (select_reg_kernel's keys, bit for bit):
 // MHA the ordered logit bits, GQA the fp32 bits of sum_g p_g with the fast exp.
 // GQ: the group size at compile time (1, 2, 4, 8), 0 = runtime G.
-template <int GQ>
+template <int GQ, int UB = 0>
 struct RowKeys {
+  static constexpr int kGQ = GQ;
   const float* lbase;  // the row's first q head's logits
   int64_t lstride;
   int G;
@@ -222,7 +223,9 @@ struct RowKeys {
   float* kcache = nullptr;  // shared-memory copy of the row's values (pass 1 -> pass 2), or null
   static constexpr int kR = GQ > 0 ? GQ : 1;  // raw float4 per position quad
   // loads in flight per lane in a streaming pass: U position quads
-  static constexpr int U = GQ == 1 ? 8 : (GQ == 2 ? 4 : (GQ == 4 ? 2 : 1));
+  // loads in flight per lane in a streaming pass: U position quads (UB > 0:
+  // set by the caller -- more registers, fewer round trips)
+  static constexpr int U = UB > 0 ? UB : (GQ == 1 ? 8 : (GQ == 2 ? 4 : (GQ == 4 ? 2 : 1)));
 
   __device__ __forceinline__ int g_n() const { return GQ > 0 ? GQ : G; }
 
@@ -339,9 +342,9 @@ struct RowCtx {
 };
 
 // weights of selected position `pos` (key `key`) at output slot o
-template <int GQ>
+template <class RK>
 __device__ __forceinline__ void write_sel(const ConsumeParams& p, CShared& S, const RowCtx& r,
-                                          const RowKeys<GQ>& rk, int o, uint32_t pos, uint32_t key) {
+                                          const RK& rk, int o, uint32_t pos, uint32_t key) {
   p.idx[(size_t)r.row * r.nc + o] = pos;
   for (int g = 0; g < r.G; ++g) {
     const float sg = r.G == 1 ? from_ordered(key) : __ldcg(rk.lbase + (size_t)g * rk.lstride + pos);
@@ -355,8 +358,8 @@ __device__ __forceinline__ void write_sel(const ConsumeParams& p, CShared& S, co
 // four group maxima (keys): >= nc distinct positions hold keys >= tau. MHA:
 // lowered by the p-tie window. Returns tau as a comparable value, or NaN when
 // p(tau) is not a normal float (ties unbounded: exact path). Uniform.
-template <int GQ>
-__device__ float bound_from_groups(const ConsumeParams& p, CShared& S, const RowCtx& r, const RowKeys<GQ>& rk,
+template <class RK>
+__device__ float bound_from_groups(const ConsumeParams& p, CShared& S, const RowCtx& r, const RK& rk,
                                    uint32_t (&gm)[4]) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int kw = (r.nc + kCW - 1) / kCW;
@@ -392,9 +395,10 @@ __device__ float bound_from_groups(const ConsumeParams& p, CShared& S, const Row
 // Candidates by two streaming passes over the row's logits (group maxima,
 // then keys >= tau, compacted per warp in position order). Leaves them in
 // ckey/cpos in position order; returns their count, or -1 (exact path).
-template <int GQ>
-__device__ int cands_passes(const ConsumeParams& p, CShared& S, const RowCtx& r, const RowKeys<GQ>& rk) {
-  constexpr int U = RowKeys<GQ>::U;
+template <class RK>
+__device__ int cands_passes(const ConsumeParams& p, CShared& S, const RowCtx& r, const RK& rk) {
+  constexpr int U = RK::U;
+  constexpr int GQ = RK::kGQ;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int s = r.s, nc = r.nc;
   (void)tid;
@@ -404,7 +408,7 @@ __device__ int cands_passes(const ConsumeParams& p, CShared& S, const RowCtx& r,
   const int n_it = w1 > w0 ? (w1 - w0 + 127) / 128 : 0;
 
   // ---- pass 1: group maxima -> tau ----
-  float gmf[4] = {RowKeys<GQ>::kInvalid, RowKeys<GQ>::kInvalid, RowKeys<GQ>::kInvalid, RowKeys<GQ>::kInvalid};
+  float gmf[4] = {RK::kInvalid, RK::kInvalid, RK::kInvalid, RK::kInvalid};
   for (int it0 = 0; it0 < n_it; it0 += U) {
     float f[U][4];
     rk.batch(w0, w1, it0, n_it, lane, f);
@@ -434,8 +438,8 @@ __device__ int cands_passes(const ConsumeParams& p, CShared& S, const RowCtx& r,
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const float4 x = it0 + u < n_it ? *reinterpret_cast<const float4*>(rk.kcache + w0 + (it0 + u) * 128 + 4 * lane)
-                                        : make_float4(RowKeys<GQ>::kInvalid, RowKeys<GQ>::kInvalid,
-                                                      RowKeys<GQ>::kInvalid, RowKeys<GQ>::kInvalid);
+                                        : make_float4(RK::kInvalid, RK::kInvalid,
+                                                      RK::kInvalid, RK::kInvalid);
         f[u][0] = x.x;
         f[u][1] = x.y;
         f[u][2] = x.z;
@@ -489,8 +493,8 @@ __device__ int cands_passes(const ConsumeParams& p, CShared& S, const RowCtx& r,
 
 // Fast path: bound -> candidates -> exact select. false: take the exact path
 // (nothing written).
-template <int GQ>
-__device__ bool select_fast(const ConsumeParams& p, CShared& S, const RowCtx& r, const RowKeys<GQ>& rk) {
+template <class RK>
+__device__ bool select_fast(const ConsumeParams& p, CShared& S, const RowCtx& r, const RK& rk) {
   const int tid = threadIdx.x;
   const int s = r.s, nc = r.nc;
   if (nc >= s || nc > kFastMaxNc) return false;
@@ -566,8 +570,8 @@ __device__ bool select_fast(const ConsumeParams& p, CShared& S, const RowCtx& r,
 
 // Exact path for any row: streamed radix threshold over every key, then two
 // ordered classification passes (per-warp contiguous segments).
-template <int GQ>
-__device__ void select_exact(const ConsumeParams& p, CShared& S, const RowCtx& r, const RowKeys<GQ>& rk) {
+template <class RK>
+__device__ void select_exact(const ConsumeParams& p, CShared& S, const RowCtx& r, const RK& rk) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int s = r.s, nc = r.nc;
   const bool all = nc >= s;
@@ -816,7 +820,7 @@ __device__ __forceinline__ void wait_row(const ConsumeParams& p, int row) {
 // renormaliser, dead-logit discard): shared by the consumer and the
 // stream-ordered cached row selection. kcache: shared memory for the row's
 // selection values (pass 1 -> pass 2), or null.
-template <int GQ>
+template <int GQ, int UB = 0>
 __device__ __forceinline__ void select_row(const ConsumeParams& p, CShared& S, const RowCtx& r,
                                            float* kcache = nullptr) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -832,7 +836,7 @@ __device__ __forceinline__ void select_row(const ConsumeParams& p, CShared& S, c
   }
   __syncthreads();
   KC_STAMP(1);
-  RowKeys<GQ> rk;
+  RowKeys<GQ, UB> rk;
   rk.lbase = p.logits + ((size_t)r.b * n_q + r.kvh * G) * p.lstride;
   rk.lstride = p.lstride;
   rk.G = G;
@@ -888,13 +892,17 @@ __global__ void __maxnreg__(88) consume_kernel(const ConsumeParams p) {
 // (sum_g p_g, G exp per position) computed once in pass 1 and kept in shared
 // memory for pass 2; two CTAs per SM hold all 256 rows of C3 in one wave
 // (select_reg_kernel: one 1024-thread CTA per SM, 1.73 waves).
+// quads in flight per lane in the cached kernel's pass 1 (up to 128 registers)
+template <int GQ>
+constexpr int kCachedU = GQ <= 2 ? 8 : (GQ == 4 ? 4 : 2);
+
 template <int GQ>
 __global__ void __launch_bounds__(kCT, 2) select_rows_cached_kernel(const ConsumeParams p) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   CShared& S = *reinterpret_cast<CShared*>(smem_raw);
   float* kc = reinterpret_cast<float*>(smem_raw + ((sizeof(CShared) + 15) & ~size_t(15)));
   for (int row = p.row0 + blockIdx.x; row < p.row0 + p.rows; row += gridDim.x)
-    select_row<GQ>(p, S, row_ctx(p, row), kc);
+    select_row<GQ, kCachedU<GQ>>(p, S, row_ctx(p, row), kc);
 }
 
 template <int GQ>
