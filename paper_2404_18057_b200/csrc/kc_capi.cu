@@ -259,6 +259,7 @@ struct kc_cache {
   int score_groups = 0;
   int group_first_pct = 0;  // row groups: % of the rows in the first group (0: equal groups)   // row groups per layer (score -> select -> recall each); 0 = auto
   int tlb_ahead = -1;      // K translation warm-up distance in rows (-1 auto: ~3 CTA waves, 0 off); r01: -2 %
+  int tc_grid = 0;         // score_tc_kernel: CTAs per SM of a persistent grid (0: one CTA per item)
   int score_mma = 1;       // GQA scoring on the tensor cores (TF32 split-q mma.sync)
   int k_policy = 0;        // L2 policy of the K stream (kc_device.cuh l2_policy)
   // MHA candidate selection: 0 auto (rows longer than the register-resident
@@ -629,6 +630,7 @@ void enqueue_score(kc_cache* c, uint64_t layer, const float* q32, const StepGeom
     auto& km = c->kmaps[layer];
     if (!km.ok) km.ok = kc::encode_k_map(km.bytes, c->k_layer(layer), c->dtype, c->rows, c->cfg.max_seq);
     sp.kmap = km.ok ? km.bytes : nullptr;
+    sp.grid = c->tc_grid > 0 ? c->tc_grid * kc::sm_count() : 0;
   }
   // ~3 waves of CTAs ahead (one CTA per item, 3 per SM)
   sp.tlb_ahead = c->tlb_ahead >= 0 ? c->tlb_ahead
@@ -978,6 +980,10 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
           cp.rows = sp.rows;
           cp.keep_logits = sp.keep_logits;
           cp.h = (int)c->h;
+          if (c->consume_dbg) {
+            c->cons_dbg.ensure(c->rows * 8 * sizeof(uint64_t));
+            cp.dbg = c->cons_dbg.as<uint64_t>();
+          }
           if (kc::select_rows_cached_launch(cp, st)) return;
         }
         kc::select_launch(sp, st);
@@ -1751,6 +1757,7 @@ int kc_set_tuning(kc_cache* c, const char* key, int64_t value) {
     }
     else if (k == "k_policy") c->k_policy = (int)value;
     else if (k == "tlb_ahead") c->tlb_ahead = (int)value;
+    else if (k == "tc_grid") c->tc_grid = (int)std::max<int64_t>(0, std::min<int64_t>(4, value));
     else if (k == "score_mma") c->score_mma = (int)std::max<int64_t>(0, std::min<int64_t>(3, value));
     else if (k == "cand_force_fallback") c->cand_force_fallback = value ? 1 : 0;
     else if (k == "consume") {

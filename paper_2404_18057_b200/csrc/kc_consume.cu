@@ -665,6 +665,13 @@ __device__ void finish_rows(const ConsumeParams& p, CShared& S, const RowCtx& r)
     const int ng = min(kRedG, r.G - g0);
     for (int item = warp; item < ng * 32; item += kCW) {
       const int gl = item >> 5, vw = item & 31, g = g0 + gl;
+      if (vw * 32 >= nc) {  // no weights: exact zeros (x + 0 == x keeps the tree's result)
+        if (lane == 0) {
+          S.red_d[gl][vw] = 0.0;
+          S.red_f[gl][vw] = 0.0f;
+        }
+        continue;
+      }
       const size_t slot = (size_t)r.b * r.n_q + r.kvh * r.G + g;
       const float* wg = r.wsm_ok ? S.wsm + g * nc : p.w + slot * nc;
       double md = 0.0;
@@ -901,8 +908,13 @@ __global__ void __launch_bounds__(kCT, 2) select_rows_cached_kernel(const Consum
   extern __shared__ __align__(16) uint8_t smem_raw[];
   CShared& S = *reinterpret_cast<CShared*>(smem_raw);
   float* kc = reinterpret_cast<float*>(smem_raw + ((sizeof(CShared) + 15) & ~size_t(15)));
-  for (int row = p.row0 + blockIdx.x; row < p.row0 + p.rows; row += gridDim.x)
-    select_row<GQ, kCachedU<GQ>>(p, S, row_ctx(p, row), kc);
+  for (int row = p.row0 + blockIdx.x; row < p.row0 + p.rows; row += gridDim.x) {
+    const RowCtx r = row_ctx(p, row);
+    KC_STAMP(7);
+    KC_STAMP(0);
+    select_row<GQ, kCachedU<GQ>>(p, S, r, kc);
+    KC_STAMP(6);
+  }
 }
 
 template <int GQ>

@@ -47,6 +47,9 @@ struct ScoreParams {
   // score_tc_kernel: the layer's K tensor map (CUtensorMap, host memory; see
   // encode_k_map), or null
   const void* kmap;
+  // score_tc_kernel: CTAs in the launch (0: one per item; otherwise a
+  // persistent grid walking items blockIdx.x, +gridDim.x, ...)
+  int grid;
 };
 // row_done counters: one per kRowDoneStride words (a 128-B line per row)
 constexpr int kRowDoneStride = 32;

@@ -28,6 +28,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -327,7 +328,9 @@ void launch_tc(const ScoreParams& p, const CUtensorMap& map, cudaStream_t st) {
     cudaFuncSetAttribute(score_tc_kernel<T, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     configured[dev & 63] = 1;
   }
-  score_tc_kernel<T, NB><<<p.rows * p.n_splits, kTcThreads, smem, st>>>(p, map);
+  const int n_items = p.rows * p.n_splits;
+  const int grid = p.grid > 0 ? std::min(p.grid, n_items) : n_items;
+  score_tc_kernel<T, NB><<<grid, kTcThreads, smem, st>>>(p, map);
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
