@@ -259,6 +259,8 @@ struct kc_cache {
   int score_groups = 0;
   int group_first_pct = 0;  // row groups: % of the rows in the first group (0: equal groups)   // row groups per layer (score -> select -> recall each); 0 = auto
   int tlb_ahead = -1;      // K translation warm-up distance in rows (-1 auto: ~3 CTA waves, 0 off); r01: -2 %
+  int recall_lean = -1;    // pipelined recall at <= 72 registers (-1: multi-layer calls)
+  int recall_dbg = 0;      // development probe: 1 recall without V loads, 2 recall kernel without work
   int tc_grid = 0;         // score_tc_kernel: CTAs per SM of a persistent grid (0: one CTA per item)
   int score_mma = 1;       // GQA scoring on the tensor cores (TF32 split-q mma.sync)
   int k_policy = 0;        // L2 policy of the K stream (kc_device.cuh l2_policy)
@@ -864,6 +866,8 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
         rp.v = c->v_layer(layer);
         rp.grid = c->flow_recall_ctas;
         rp.pipelined = c->recall_pipe < 0 ? (c->G > 1 ? 1 : 0) : c->recall_pipe;
+        rp.dbg = c->recall_dbg;
+        rp.lean = c->recall_lean > 0 ? 1 : 0;
         rp.idx = c->idx[slot].as<uint32_t>();
         rp.w = c->w[slot].as<float>();
         rp.norm = c->norm[slot].as<float>();
@@ -996,6 +1000,11 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
       rp.staged = 0;
       rp.grid = c->recall_ctas;
       rp.pipelined = c->recall_pipe < 0 ? (c->G > 1 ? 1 : 0) : c->recall_pipe;
+      rp.dbg = c->recall_dbg;
+      // the lean kernel shares SMs better with the next layer's scoring but
+      // runs longer alone (C3: pipelined 239 -> 235 us per layer, engine
+      // step 335 -> 343): multi-layer calls only by default
+      rp.lean = c->recall_lean < 0 ? (n > 1 ? 1 : 0) : c->recall_lean;
       rp.idx = c->idx[slot].as<uint32_t>();
       rp.w = c->w[slot].as<float>();
       rp.norm = c->norm[slot].as<float>();
@@ -1757,6 +1766,9 @@ int kc_set_tuning(kc_cache* c, const char* key, int64_t value) {
     }
     else if (k == "k_policy") c->k_policy = (int)value;
     else if (k == "tlb_ahead") c->tlb_ahead = (int)value;
+    else if (k == "recall_lean") c->recall_lean = (int)std::max<int64_t>(-1, std::min<int64_t>(1, value));
+    else if (k == "smem_carveout") kc::g_smem_carveout = (int)std::max<int64_t>(-1, std::min<int64_t>(100, value));
+    else if (k == "recall_dbg") c->recall_dbg = (int)std::max<int64_t>(0, std::min<int64_t>(2, value));
     else if (k == "tc_grid") c->tc_grid = (int)std::max<int64_t>(0, std::min<int64_t>(4, value));
     else if (k == "score_mma") c->score_mma = (int)std::max<int64_t>(0, std::min<int64_t>(3, value));
     else if (k == "cand_force_fallback") c->cand_force_fallback = value ? 1 : 0;

@@ -930,6 +930,7 @@ bool launch_cached(const ConsumeParams& p, size_t smem, cudaStream_t st) {
     }
     configured[dev & 63] = (int)smem;
   }
+  apply_carveout((const void*)select_rows_cached_kernel<GQ>);
   select_rows_cached_kernel<GQ><<<p.rows, kCT, smem, st>>>(p);
   return true;
 }

@@ -51,6 +51,10 @@ struct ScoreParams {
   // persistent grid walking items blockIdx.x, +gridDim.x, ...)
   int grid;
 };
+// Preferred shared-memory carveout (percent) applied to the scoring /
+// recall / selection kernels before their launches; < 0: driver default.
+extern int g_smem_carveout;
+void apply_carveout(const void* func);
 // row_done counters: one per kRowDoneStride words (a 128-B line per row)
 constexpr int kRowDoneStride = 32;
 // dtype: KC_F32 / KC_F16 / KC_BF16 (storage)
@@ -176,6 +180,8 @@ struct RecallParams {
   int staged;             // v is the compacted [rows][nc][h] block (DMA recall)
   int grid;               // CTAs (0: one per row); CTAs loop over rows
   int pipelined;          // use recall_pv_pipe_kernel where the shape allows
+  int dbg;                // development probe (pipelined kernel): 1 skip the V loads, 2 no work
+  int lean;               // pipelined kernel capped at 72 registers
 };
 void recall_launch(const RecallParams& p, int dtype, cudaStream_t st);
 

@@ -133,7 +133,7 @@ __global__ void __launch_bounds__(kRecallThreads) recall_pv_kernel(const RecallP
 constexpr int kPipeMaxNc = 128;
 
 template <typename T>
-__global__ void __launch_bounds__(kRecallThreads) recall_pv_pipe_kernel(const RecallParams p) {
+__device__ __forceinline__ void recall_pipe_body(const RecallParams& p) {
   constexpr int kVpr = 16;  // 16-B chunks per 256-B row
   constexpr int kLoads = kPipeMaxNc * kVpr / kRecallThreads;  // 8
   extern __shared__ __align__(16) uint8_t smem[];
@@ -158,11 +158,12 @@ __global__ void __launch_bounds__(kRecallThreads) recall_pv_pipe_kernel(const Re
       if (v < total) {
         const int r = v >> 4, part = v & 15;
         const size_t pos = p.staged ? (size_t)r : (size_t)idx[r];
-        tmp[u] = ld_stream16(vs + pos * kVpr + part, pol);
+        tmp[u] = p.dbg ? make_uint4((uint32_t)pos, 0u, 0u, 0u) : ld_stream16(vs + pos * kVpr + part, pol);
       }
     }
   };
   int row = p.row_offset + blockIdx.x;
+  if (p.dbg == 2) return;
   if (row < end) issue(row);
   int buf = 0;
   while (row < end) {
@@ -209,6 +210,17 @@ __global__ void __launch_bounds__(kRecallThreads) recall_pv_pipe_kernel(const Re
     row = next;
     buf ^= 1;
   }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kRecallThreads) recall_pv_pipe_kernel(const RecallParams p) {
+  recall_pipe_body<T>(p);
+}
+
+// the same at <= 72 registers: 256 x 72 fits beside two GQA scoring CTAs
+template <typename T>
+__global__ void __maxnreg__(72) recall_pv_pipe_lean_kernel(const RecallParams p) {
+  recall_pipe_body<T>(p);
 }
 
 // decode_attention_full P.V: CTA (split, row) accumulates its positions in
@@ -447,8 +459,19 @@ void launch_pipe(const RecallParams& p, cudaStream_t st) {
     cudaFuncSetAttribute(recall_pv_pipe_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     configured |= 1ull << (dev & 63);
   }
+  static unsigned long long configured_lean = 0;
+  if (p.lean && !(configured_lean >> (dev & 63) & 1ull)) {
+    cudaFuncSetAttribute(recall_pv_pipe_lean_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    configured_lean |= 1ull << (dev & 63);
+  }
   const int grid = (p.grid > 0 && p.grid < p.rows) ? p.grid : p.rows;
-  recall_pv_pipe_kernel<T><<<grid, kRecallThreads, smem, st>>>(p);
+  if (p.lean) {
+    apply_carveout((const void*)recall_pv_pipe_lean_kernel<T>);
+    recall_pv_pipe_lean_kernel<T><<<grid, kRecallThreads, smem, st>>>(p);
+  } else {
+    apply_carveout((const void*)recall_pv_pipe_kernel<T>);
+    recall_pv_pipe_kernel<T><<<grid, kRecallThreads, smem, st>>>(p);
+  }
 }
 
 void recall_launch(const RecallParams& p, int dtype, cudaStream_t st) {

@@ -889,6 +889,7 @@ void launch_mma_s(const ScoreParams& p, cudaStream_t st) {
     configured |= 1ull << (dev & 63);
   }
   const int n_items = p.rows * p.n_splits;
+  apply_carveout((const void*)score_mma_kernel<T, STAGES, NCW>);
   score_mma_kernel<T, STAGES, NCW><<<n_items, (NCW + 1) * 32, smem, st>>>(p);
 }
 
@@ -946,6 +947,12 @@ int score_pick_chunk(int s, int rows, int override_chunk, int G) {
 }
 
 int sm_count() { return num_sms(); }
+
+int g_smem_carveout = -1;
+
+void apply_carveout(const void* func) {
+  if (g_smem_carveout >= 0) cudaFuncSetAttribute(func, cudaFuncAttributePreferredSharedMemoryCarveout, g_smem_carveout);
+}
 
 bool full_fast_launch(const FullParams& p, int dtype, cudaStream_t st) {
   if (dtype == KC_F16) return try_full<__half>(p, st);
