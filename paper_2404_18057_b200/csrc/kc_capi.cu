@@ -259,6 +259,7 @@ struct kc_cache {
   int score_groups = 0;
   int group_first_pct = 0;  // row groups: % of the rows in the first group (0: equal groups)   // row groups per layer (score -> select -> recall each); 0 = auto
   int tlb_ahead = -1;      // K translation warm-up distance in rows (-1 auto: ~3 CTA waves, 0 off); r01: -2 %
+  int recall_tma = 0;      // recall_tma_kernel: V rows by TMA bulk copies
   int recall_lean = -1;    // pipelined recall at <= 72 registers (-1: multi-layer calls)
   int recall_dbg = 0;      // development probe: 1 recall without V loads, 2 recall kernel without work
   int tc_grid = 0;         // score_tc_kernel: CTAs per SM of a persistent grid (0: one CTA per item)
@@ -868,6 +869,7 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
         rp.pipelined = c->recall_pipe < 0 ? (c->G > 1 ? 1 : 0) : c->recall_pipe;
         rp.dbg = c->recall_dbg;
         rp.lean = c->recall_lean > 0 ? 1 : 0;
+        rp.tma = c->recall_tma;
         rp.idx = c->idx[slot].as<uint32_t>();
         rp.w = c->w[slot].as<float>();
         rp.norm = c->norm[slot].as<float>();
@@ -1005,6 +1007,7 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
       // runs longer alone (C3: pipelined 239 -> 235 us per layer, engine
       // step 335 -> 343): multi-layer calls only by default
       rp.lean = c->recall_lean < 0 ? (n > 1 ? 1 : 0) : c->recall_lean;
+      rp.tma = c->recall_tma;
       rp.idx = c->idx[slot].as<uint32_t>();
       rp.w = c->w[slot].as<float>();
       rp.norm = c->norm[slot].as<float>();
@@ -1766,6 +1769,7 @@ int kc_set_tuning(kc_cache* c, const char* key, int64_t value) {
     }
     else if (k == "k_policy") c->k_policy = (int)value;
     else if (k == "tlb_ahead") c->tlb_ahead = (int)value;
+    else if (k == "recall_tma") c->recall_tma = value ? 1 : 0;
     else if (k == "recall_lean") c->recall_lean = (int)std::max<int64_t>(-1, std::min<int64_t>(1, value));
     else if (k == "smem_carveout") kc::g_smem_carveout = (int)std::max<int64_t>(-1, std::min<int64_t>(100, value));
     else if (k == "recall_dbg") c->recall_dbg = (int)std::max<int64_t>(0, std::min<int64_t>(2, value));

@@ -182,6 +182,7 @@ struct RecallParams {
   int pipelined;          // use recall_pv_pipe_kernel where the shape allows
   int dbg;                // development probe (pipelined kernel): 1 skip the V loads, 2 no work
   int lean;               // pipelined kernel capped at 72 registers
+  int tma;                // recall_tma_kernel (TMA bulk copies of the V rows) where the shape allows
 };
 void recall_launch(const RecallParams& p, int dtype, cudaStream_t st);
 

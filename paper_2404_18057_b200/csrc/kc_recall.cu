@@ -223,6 +223,79 @@ __global__ void __maxnreg__(72) recall_pv_pipe_lean_kernel(const RecallParams p)
   recall_pipe_body<T>(p);
 }
 
+// The same operation with the V rows moved by the TMA unit: warp 0 issues one
+// 256-B cp.async.bulk per selected row (global or host-resident arena ->
+// shared memory, completion as transaction bytes on the buffer's mbarrier)
+// for the CTA's next row while all threads reduce the current one. No
+// registers or LSU slots hold the in-flight PCIe reads. Same operation order
+// as recall_pv_kernel. h = 128 16-bit rows, nc <= 128, G <= 8.
+template <typename T>
+__global__ void __launch_bounds__(kRecallThreads) recall_tma_kernel(const RecallParams p) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  T* vb = reinterpret_cast<T*>(smem);                                 // [2][kPipeMaxNc][kH]
+  float* wb = reinterpret_cast<float*>(smem + 2 * kPipeMaxNc * 256);  // [2][kMaxGroup][kPipeMaxNc]
+  __shared__ __align__(8) uint64_t full[2];
+  const int G = p.G, n_q = p.n_kv * G, nc = p.nc;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int end = p.row_offset + p.rows;
+  if (tid == 0) {
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const uint64_t pol = l2_evict_first_policy();
+  auto issue = [&](int row, int buf) {  // warp 0
+    const T* vs = static_cast<const T*>(p.v) + (size_t)row * (p.staged ? (size_t)nc : (size_t)p.max_seq) * kH;
+    const uint32_t* idx = p.idx + (size_t)row * nc;
+    if (lane == 0) mbar_arrive_expect_tx(&full[buf], (uint32_t)nc * (uint32_t)(kH * sizeof(T)));
+    __syncwarp();
+    T* dst = vb + (size_t)buf * kPipeMaxNc * kH;
+    for (int r = lane; r < nc; r += 32) {
+      const size_t pos = p.staged ? (size_t)r : (size_t)__ldcg(idx + r);
+      tma_bulk_g2s(dst + r * kH, vs + pos * kH, (uint32_t)(kH * sizeof(T)), &full[buf], pol);
+    }
+  };
+  int row = p.row_offset + blockIdx.x;
+  if (row < end && warp == 0) issue(row, 0);
+  for (int it = 0; row < end; ++it) {
+    const int buf = it & 1;
+    const int b = row / p.n_kv;
+    const int kvh = row - b * p.n_kv;
+    float* wd = wb + buf * kMaxGroup * kPipeMaxNc;
+    for (int e = tid; e < G * nc; e += kRecallThreads) {
+      const int g = e / nc, r = e - g * nc;
+      const size_t slot = (size_t)b * n_q + kvh * G + g;
+      float w = p.w[slot * nc + r];
+      if (p.renormalize) w = __fmul_rn(w, p.norm[slot]);
+      wd[g * kPipeMaxNc + r] = w;
+    }
+    mbar_wait(&full[buf], (uint32_t)(it >> 1) & 1u);
+    // weights visible; every thread is past the previous row's reduction, so
+    // the other buffer is free for the next row's copies
+    __syncthreads();
+    const int next = row + gridDim.x;
+    if (next < end && warp == 0) issue(next, buf ^ 1);
+    const T* vt = vb + (size_t)buf * kPipeMaxNc * kH;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {  // G*h <= 1024 outputs
+      const int o = tid + i * kRecallThreads;
+      if (o < G * kH) {
+        const int g = o / kH, c = o - g * kH;
+        const float* wg = wd + g * kPipeMaxNc;
+        float a = 0.0f;
+        if (!p.reverse) {
+          for (int r = 0; r < nc; ++r) a = __fadd_rn(a, __fmul_rn(wg[r], to_f32<T>(vt[r * kH + c])));
+        } else {
+          for (int r = nc - 1; r >= 0; --r) a = __fadd_rn(a, __fmul_rn(wg[r], to_f32<T>(vt[r * kH + c])));
+        }
+        p.out[((size_t)b * n_q + kvh * G + g) * kH + c] = a;
+      }
+    }
+    row = next;
+  }
+}
+
 // decode_attention_full P.V: CTA (split, row) accumulates its positions in
 // order with the global softmax weights; pv_reduce sums splits in order.
 template <typename T>
@@ -474,7 +547,26 @@ void launch_pipe(const RecallParams& p, cudaStream_t st) {
   }
 }
 
+template <typename T>
+void launch_tma(const RecallParams& p, cudaStream_t st) {
+  const size_t smem = 2 * kPipeMaxNc * 256 + 2 * kMaxGroup * kPipeMaxNc * sizeof(float);
+  static unsigned long long configured = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!(configured >> (dev & 63) & 1ull)) {
+    cudaFuncSetAttribute(recall_tma_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    configured |= 1ull << (dev & 63);
+  }
+  const int grid = (p.grid > 0 && p.grid < p.rows) ? p.grid : p.rows;
+  recall_tma_kernel<T><<<grid, kRecallThreads, smem, st>>>(p);
+}
+
 void recall_launch(const RecallParams& p, int dtype, cudaStream_t st) {
+  if (p.tma && p.h == kH && p.nc <= kPipeMaxNc && p.G <= kMaxGroup && dtype != KC_F32) {
+    if (dtype == KC_F16) launch_tma<__half>(p, st);
+    else launch_tma<__nv_bfloat16>(p, st);
+    return;
+  }
   if (p.pipelined && p.h == kH && p.nc <= kPipeMaxNc && p.G <= kMaxGroup && dtype != KC_F32) {
     if (dtype == KC_F16) launch_pipe<__half>(p, st);
     else launch_pipe<__nv_bfloat16>(p, st);
