@@ -259,6 +259,7 @@ struct kc_cache {
   int score_groups = 0;
   int group_first_pct = 0;  // row groups: % of the rows in the first group (0: equal groups)   // row groups per layer (score -> select -> recall each); 0 = auto
   int tlb_ahead = -1;      // K translation warm-up distance in rows (-1 auto: ~3 CTA waves, 0 off); r01: -2 %
+  int consume_lean = 0;    // consume_lean_kernel (<= 72 registers)
   int recall_tma = 0;      // recall_tma_kernel: V rows by TMA bulk copies
   int recall_lean = -1;    // pipelined recall at <= 72 registers (-1: multi-layer calls)
   int recall_dbg = 0;      // development probe: 1 recall without V loads, 2 recall kernel without work
@@ -772,8 +773,14 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
     // rows and larger N measured faster stream-ordered (r02 C5 sweep: 4 k x
     // N=128 237 vs 224 us per layer, 32 k x N=512 1097 vs 885: > 1024
     // candidates take the consumer's exact path), and inside a step-graph
-    // capture the consumer could only follow its scoring
-    const bool flow_auto = c->G == 1 && g.nc <= 256 && g.s >= 16384 && !c->capture_st;
+    // capture the consumer could only follow its scoring. GQA: single-layer
+    // calls (the engine's layer-by-layer step) of >= 8 k positions -- the
+    // stream-ordered path exposes its last row group's recall there (r02,
+    // 8-layer engine sweeps, 5 shapes: 8 k-64 k positions, 64-512 rows, 9-14 %
+    // faster); multi-layer calls hide the recall under the next layer and
+    // stay stream-ordered (C3 237 vs 267 us per layer)
+    const bool flow_auto = g.nc <= 256 && !c->capture_st &&
+                           ((c->G == 1 && g.s >= 16384) || (c->G > 1 && n == 1 && g.s >= 8192));
     const bool flow = (c->consume == 2 || (c->consume == 1 && flow_auto)) &&
                       kc::consume_supported((int)c->G, (int)c->h) && !c->select_global && c->select_cand != 1;
     if (flow) {
@@ -854,7 +861,14 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
         c->cons_dbg.ensure(c->rows * 8 * sizeof(uint64_t));
         cp.dbg = c->cons_dbg.as<uint64_t>();
       }
-      const int ctas = c->consume_ctas > 0 ? c->consume_ctas : (own_recall ? 40 : 32);
+      cp.lean = c->consume_lean > 0 ? 1 : 0;
+      // auto grid: MHA 40 recalling / 32 selecting only; GQA: a row's
+      // selection work grows with s like its scoring, its recall does not, so
+      // the CTAs that keep pace fall with s: 32 + 2^20 / s (r02 sweeps: best
+      // 128 / 96 / 64 / 48 at 8 k / 16 k / 32 k / 64 k positions)
+      const int ctas = c->consume_ctas > 0 ? c->consume_ctas
+                       : c->G > 1 ? std::min(2 * kc::sm_count(), 32 + (int)((1ll << 20) / std::max(g.s, 1)))
+                                  : (own_recall ? 40 : 32);
       c->timed(1, cs, [&] { kc::consume_launch(cp, c->dtype, ctas, cs); });
       c->cons_dirty = false;
       ++c->cons_seq;
@@ -1769,6 +1783,7 @@ int kc_set_tuning(kc_cache* c, const char* key, int64_t value) {
     }
     else if (k == "k_policy") c->k_policy = (int)value;
     else if (k == "tlb_ahead") c->tlb_ahead = (int)value;
+    else if (k == "consume_lean") c->consume_lean = (int)std::max<int64_t>(-1, std::min<int64_t>(1, value));
     else if (k == "recall_tma") c->recall_tma = value ? 1 : 0;
     else if (k == "recall_lean") c->recall_lean = (int)std::max<int64_t>(-1, std::min<int64_t>(1, value));
     else if (k == "smem_carveout") kc::g_smem_carveout = (int)std::max<int64_t>(-1, std::min<int64_t>(100, value));
@@ -1866,7 +1881,7 @@ int kc_debug_read(kc_cache* c, const char* what, void* out, uint64_t bytes) {
   return guarded([&] {
     const std::string w = what ? what : "";
     const DevBuf* src = w == "consume" ? &c->cons_dbg : w == "logits0" ? &c->logits : w == "logits1" ? &c->logits_b
-                                                                                      : nullptr;
+                         : w == "partials0" ? &c->partials : nullptr;
     if (!src || !out) fail(KC_EARG, "kc_debug_read: unknown probe");
     set_dev(c);
     CK(cudaDeviceSynchronize());

@@ -881,18 +881,32 @@ __device__ __forceinline__ RowCtx row_ctx(const ConsumeParams& p, int row) {
   return r;
 }
 
-template <typename T, int GQ>
-__global__ void __maxnreg__(88) consume_kernel(const ConsumeParams p) {
-  __shared__ CShared S;
+template <typename T, int GQ, int UB>
+__device__ __forceinline__ void consume_rows(const ConsumeParams& p, CShared& S) {
   for (int row = p.row0 + blockIdx.x; row < p.row0 + p.rows; row += gridDim.x) {
     RowCtx r = row_ctx(p, row);
     KC_STAMP(7);
     wait_row(p, row);
     KC_STAMP(0);
-    select_row<GQ>(p, S, r);
+    select_row<GQ, UB>(p, S, r);
     if (p.v) recall_row<T>(p, S, r);  // null: selection only
     KC_STAMP(6);
   }
+}
+
+template <typename T, int GQ>
+__global__ void __maxnreg__(88) consume_kernel(const ConsumeParams p) {
+  __shared__ CShared S;
+  consume_rows<T, GQ, 0>(p, S);
+}
+
+// <= 72 registers, one position quad in flight per lane: 256 x 72 fits
+// beside two GQA scoring CTAs (2 x 5 warps x 144), so the consumer takes no
+// scoring slot (ConsumeParams::lean)
+template <typename T, int GQ>
+__global__ void __maxnreg__(72) consume_lean_kernel(const ConsumeParams p) {
+  __shared__ CShared S;
+  consume_rows<T, GQ, 1>(p, S);
 }
 
 // Stream-ordered GQA selection: one row per CTA, the row's selection values
@@ -937,6 +951,16 @@ bool launch_cached(const ConsumeParams& p, size_t smem, cudaStream_t st) {
 
 template <typename T>
 void launch_g(const ConsumeParams& p, int grid, cudaStream_t st) {
+  if (p.lean) {
+    switch (p.G) {
+      case 1: consume_lean_kernel<T, 1><<<grid, kCT, 0, st>>>(p); break;
+      case 2: consume_lean_kernel<T, 2><<<grid, kCT, 0, st>>>(p); break;
+      case 4: consume_lean_kernel<T, 4><<<grid, kCT, 0, st>>>(p); break;
+      case 8: consume_lean_kernel<T, 8><<<grid, kCT, 0, st>>>(p); break;
+      default: consume_lean_kernel<T, 0><<<grid, kCT, 0, st>>>(p); break;
+    }
+    return;
+  }
   switch (p.G) {
     case 1: consume_kernel<T, 1><<<grid, kCT, 0, st>>>(p); break;
     case 2: consume_kernel<T, 2><<<grid, kCT, 0, st>>>(p); break;

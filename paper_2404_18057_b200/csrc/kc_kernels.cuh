@@ -145,6 +145,7 @@ struct ConsumeParams {
   uint32_t* row_done;      // [rows][kRowDoneStride] split completion counters; null: rows are complete
   uint32_t* err;           // set before trapping on a row that never completes
   uint64_t* dbg;           // development probe: [rows][8] phase timestamps (ns), or null
+  int lean;                // consume_lean_kernel (<= 72 registers)
 };
 bool consume_supported(int G, int h);
 // stream-ordered GQA row selection with the selection values cached in shared

@@ -484,8 +484,6 @@ __global__ void __launch_bounds__((NCW + 1) * 32) score_mma_kernel(const ScorePa
 #pragma unroll
         for (int i = 0; i < 4; ++i)
           kc[t][i] = *reinterpret_cast<const uint4*>(sb + (16 * wq + 8 * t + gid) * ROWB + 16 * (tig + 4 * i));
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[st]);
       float dd[2][NP][4];
 #pragma unroll
       for (int t = 0; t < 2; ++t)
@@ -504,6 +502,19 @@ __global__ void __launch_bounds__((NCW + 1) * 32) score_mma_kernel(const ScorePa
           for (int k = 0; k < NP; ++k) mma_16816<T>(dd[t][k], af[k][j][0], af[k][j][1], b0, b1);
         }
       }
+      // free the stage only once every lane's shared-memory loads have
+      // returned: ptxas schedules the arrive right behind the first MMAs
+      // (it does not depend on the loaded registers) and an arrive does not
+      // wait for loads still in flight, so the producer's next TMA fill of
+      // the stage could land under them (observed: an 8-position n-tile of
+      // wrong logits every few C3 layers while a recall ran beside the
+      // scoring). The CTA-scope fence waits for this lane's loads.
+      // (A data dependency instead -- the loaded words XOR-reduced over the
+      // warp into the arrive's address -- measured 4-7 us per C3 layer
+      // slower.)
+      __threadfence_block();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
       // dd[t][.][0..1] = head gid at the stage's positions 16wq + 8t + 2tig, +1
       if (hv) {
         float sc[4];

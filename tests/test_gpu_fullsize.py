@@ -162,8 +162,12 @@ def test_full_size_pipelined_layers_equal_single_calls(kc, n_kv):
     """The bench's multi-layer call at full size -- MHA: the select-only
     consumer + the recall kernel under the next layer's scoring; GQA: the
     stream-ordered path with the cached row selection -- equals single-layer
-    calls (MHA: the recalling consumer, checked against the oracle above) bit
-    for bit, over 3 layers (both scoring slots, the selection ring)."""
+    calls (the recalling consumer; MHA checked against the oracle above) and
+    stream-ordered single-layer calls bit for bit, over 3 layers (both scoring
+    slots, the selection ring). Repeated multi-layer calls stay bit-identical:
+    the scoring beside a running recall once read an overwritten ring stage
+    (score_mma_kernel released stages before its shared-memory loads
+    returned: an 8-position tile of wrong logits every few C3 layers)."""
     import torch
     b, n, h, s, N, L = (8, 32, 128, 32768, 128, 3) if n_kv == 32 else (32, 32, 128, 16384, 128, 3)
     cfg = kc.small_config(L, n * h, n, s, kv_heads=n_kv)
@@ -196,8 +200,21 @@ def test_full_size_pipelined_layers_equal_single_calls(kc, n_kv):
     cache.decode_topn_layers_device(list(range(L)), qs, N, multi, stream=stream)
     for l in range(L):
         cache.decode_topn_layers_device([l], [qs[l]], N, [single[l]], stream=stream)
+    cache.set_tuning("consume", 0)
+    ordered = outs()
+    for l in range(L):
+        cache.decode_topn_layers_device([l], [qs[l]], N, [ordered[l]], stream=stream)
+    cache.set_tuning("consume", 1)
     torch.cuda.synchronize()
     for l in range(L):
         for key in ("out", "indices", "weights", "dropped"):
             assert torch.equal(multi[l][key], single[l][key]), (l, key)
+            assert torch.equal(multi[l][key], ordered[l][key]), (l, key)
+    for rep in range(6):
+        again = outs()
+        cache.decode_topn_layers_device(list(range(L)), qs, N, again, stream=stream)
+        torch.cuda.synchronize()
+        for l in range(L):
+            for key in ("out", "indices", "weights", "dropped"):
+                assert torch.equal(multi[l][key], again[l][key]), (rep, l, key)
     cache.close()
