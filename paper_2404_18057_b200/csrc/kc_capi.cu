@@ -192,6 +192,9 @@ struct kc_cache {
   cudaEvent_t ev_q0 = nullptr, ev_qall = nullptr;
   cudaStream_t main_st = nullptr, side_st = nullptr, out_st = nullptr;
   cudaStream_t cons_st = nullptr;  // dataflow with a separate recall: the consumer's stream
+  cudaEvent_t ev_join = nullptr;
+  DevBuf join_word;
+  int flow_join = 1;  // join dataflow calls through out_st + a marker kernel
   cudaEvent_t ev_start = nullptr, ev_end = nullptr, ev_sel[kRing] = {}, ev_rec[kRing] = {},
               ev_out[kRing] = {}, ev_cp[kRing] = {},
               ev_stats = nullptr;
@@ -259,7 +262,6 @@ struct kc_cache {
   int score_groups = 0;
   int group_first_pct = 0;  // row groups: % of the rows in the first group (0: equal groups)   // row groups per layer (score -> select -> recall each); 0 = auto
   int tlb_ahead = -1;      // K translation warm-up distance in rows (-1 auto: ~3 CTA waves, 0 off); r01: -2 %
-  int consume_lean = 0;    // consume_lean_kernel (<= 72 registers)
   int recall_tma = 0;      // recall_tma_kernel: V rows by TMA bulk copies
   int recall_lean = -1;    // pipelined recall at <= 72 registers (-1: multi-layer calls)
   int recall_dbg = 0;      // development probe: 1 recall without V loads, 2 recall kernel without work
@@ -756,6 +758,7 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
     CK(cudaStreamWaitEvent(c->cons_st, c->ev_start, 0));
   }
 
+  bool flow_call = false;  // some layer's recalling consumer ran on the side stream
   for (uint64_t i = 0; i < n; ++i) {
     const int slot = (int)(i % kRing);
     const uint64_t layer = layers[i];
@@ -779,8 +782,7 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
     // 8-layer engine sweeps, 5 shapes: 8 k-64 k positions, 64-512 rows, 9-14 %
     // faster); multi-layer calls hide the recall under the next layer and
     // stay stream-ordered (C3 237 vs 267 us per layer)
-    const bool flow_auto = g.nc <= 256 && !c->capture_st &&
-                           ((c->G == 1 && g.s >= 16384) || (c->G > 1 && n == 1 && g.s >= 8192));
+    const bool flow_auto = c->G == 1 && g.nc <= 256 && g.s >= 16384 && !c->capture_st;
     const bool flow = (c->consume == 2 || (c->consume == 1 && flow_auto)) &&
                       kc::consume_supported((int)c->G, (int)c->h) && !c->select_global && c->select_cand != 1;
     if (flow) {
@@ -821,6 +823,7 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
       // its scoring.
       const bool own_recall = c->consume_recall < 0 ? n == 1 : c->consume_recall != 0;
       cudaStream_t cs = (own_recall || side == st) ? side : c->cons_st;
+      flow_call |= own_recall && cs == side;
       if (cs != st) {
         // ring slot `slot` is rewritten: the output copies of layer i-kRing must be done
         if (i >= (uint64_t)kRing) {
@@ -861,13 +864,12 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
         c->cons_dbg.ensure(c->rows * 8 * sizeof(uint64_t));
         cp.dbg = c->cons_dbg.as<uint64_t>();
       }
-      cp.lean = c->consume_lean > 0 ? 1 : 0;
       // auto grid: MHA 40 recalling / 32 selecting only; GQA: a row's
       // selection work grows with s like its scoring, its recall does not, so
-      // the CTAs that keep pace fall with s: 32 + 2^20 / s (r02 sweeps: best
-      // 128 / 96 / 64 / 48 at 8 k / 16 k / 32 k / 64 k positions)
+      // the CTAs that keep pace fall with s: 64 + 2^20 / s (r02 sweeps: best
+      // 192 / 128 / 96 / 64-256 at 8 k / 16 k / 32 k / 64 k positions)
       const int ctas = c->consume_ctas > 0 ? c->consume_ctas
-                       : c->G > 1 ? std::min(2 * kc::sm_count(), 32 + (int)((1ll << 20) / std::max(g.s, 1)))
+                       : c->G > 1 ? std::min(2 * kc::sm_count(), 64 + (int)((1ll << 20) / std::max(g.s, 1)))
                                   : (own_recall ? 40 : 32);
       c->timed(1, cs, [&] { kc::consume_launch(cp, c->dtype, ctas, cs); });
       c->cons_dirty = false;
@@ -1101,7 +1103,20 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
       c->record(c->phase, layer, KC_H2D, o.h2d_bytes, elements);
     }
   }
-  if (side != st) {
+  if (side != st && flow_call && !out_used && c->G > 1 && c->flow_join) {
+    // A dataflow call without selection copies: the caller's stream joins
+    // the consumer through the output stream and a marker kernel there.
+    // Waiting on the consumer's (high-priority) stream directly costs the
+    // next call ~100+ us before its scoring starts (measured: C3 single-layer
+    // calls 437 vs 299-319 us per layer; the copies kernel of the calls that
+    // return their selection had the same effect).
+    CK(cudaEventRecord(c->ev_end, side));
+    CK(cudaStreamWaitEvent(c->out_st, c->ev_end, 0));
+    c->join_word.ensure(4);
+    kc::join_mark_launch(c->join_word.as<uint32_t>(), c->out_st);
+    CK(cudaEventRecord(c->ev_join, c->out_st));
+    CK(cudaStreamWaitEvent(st, c->ev_join, 0));
+  } else if (side != st) {
     CK(cudaEventRecord(c->ev_end, side));
     CK(cudaStreamWaitEvent(st, c->ev_end, 0));
     if (out_used) {  // host D2H / device selection copies
@@ -1212,6 +1227,7 @@ int kc_cache_create(const kc_config* cfg, uint64_t batch, uint64_t resident_laye
       CK(cudaEventCreateWithFlags(&c->ev_q0, cudaEventDisableTiming));
       CK(cudaEventCreateWithFlags(&c->ev_qall, cudaEventDisableTiming));
       CK(cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
       CK(cudaEventCreateWithFlags(&c->ev_end, cudaEventDisableTiming));
       CK(cudaEventCreateWithFlags(&c->ev_stats, cudaEventDisableTiming));
       CK(cudaEventCreateWithFlags(&c->ev_append, cudaEventDisableTiming));
@@ -1783,10 +1799,9 @@ int kc_set_tuning(kc_cache* c, const char* key, int64_t value) {
     }
     else if (k == "k_policy") c->k_policy = (int)value;
     else if (k == "tlb_ahead") c->tlb_ahead = (int)value;
-    else if (k == "consume_lean") c->consume_lean = (int)std::max<int64_t>(-1, std::min<int64_t>(1, value));
+    else if (k == "flow_join") c->flow_join = value ? 1 : 0;
     else if (k == "recall_tma") c->recall_tma = value ? 1 : 0;
     else if (k == "recall_lean") c->recall_lean = (int)std::max<int64_t>(-1, std::min<int64_t>(1, value));
-    else if (k == "smem_carveout") kc::g_smem_carveout = (int)std::max<int64_t>(-1, std::min<int64_t>(100, value));
     else if (k == "recall_dbg") c->recall_dbg = (int)std::max<int64_t>(0, std::min<int64_t>(2, value));
     else if (k == "tc_grid") c->tc_grid = (int)std::max<int64_t>(0, std::min<int64_t>(4, value));
     else if (k == "score_mma") c->score_mma = (int)std::max<int64_t>(0, std::min<int64_t>(3, value));

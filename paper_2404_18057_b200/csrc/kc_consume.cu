@@ -900,14 +900,6 @@ __global__ void __maxnreg__(88) consume_kernel(const ConsumeParams p) {
   consume_rows<T, GQ, 0>(p, S);
 }
 
-// <= 72 registers, one position quad in flight per lane: 256 x 72 fits
-// beside two GQA scoring CTAs (2 x 5 warps x 144), so the consumer takes no
-// scoring slot (ConsumeParams::lean)
-template <typename T, int GQ>
-__global__ void __maxnreg__(72) consume_lean_kernel(const ConsumeParams p) {
-  __shared__ CShared S;
-  consume_rows<T, GQ, 1>(p, S);
-}
 
 // Stream-ordered GQA selection: one row per CTA, the row's selection values
 // (sum_g p_g, G exp per position) computed once in pass 1 and kept in shared
@@ -944,23 +936,12 @@ bool launch_cached(const ConsumeParams& p, size_t smem, cudaStream_t st) {
     }
     configured[dev & 63] = (int)smem;
   }
-  apply_carveout((const void*)select_rows_cached_kernel<GQ>);
   select_rows_cached_kernel<GQ><<<p.rows, kCT, smem, st>>>(p);
   return true;
 }
 
 template <typename T>
 void launch_g(const ConsumeParams& p, int grid, cudaStream_t st) {
-  if (p.lean) {
-    switch (p.G) {
-      case 1: consume_lean_kernel<T, 1><<<grid, kCT, 0, st>>>(p); break;
-      case 2: consume_lean_kernel<T, 2><<<grid, kCT, 0, st>>>(p); break;
-      case 4: consume_lean_kernel<T, 4><<<grid, kCT, 0, st>>>(p); break;
-      case 8: consume_lean_kernel<T, 8><<<grid, kCT, 0, st>>>(p); break;
-      default: consume_lean_kernel<T, 0><<<grid, kCT, 0, st>>>(p); break;
-    }
-    return;
-  }
   switch (p.G) {
     case 1: consume_kernel<T, 1><<<grid, kCT, 0, st>>>(p); break;
     case 2: consume_kernel<T, 2><<<grid, kCT, 0, st>>>(p); break;

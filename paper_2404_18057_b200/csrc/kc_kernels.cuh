@@ -51,10 +51,8 @@ struct ScoreParams {
   // persistent grid walking items blockIdx.x, +gridDim.x, ...)
   int grid;
 };
-// Preferred shared-memory carveout (percent) applied to the scoring /
-// recall / selection kernels before their launches; < 0: driver default.
-extern int g_smem_carveout;
-void apply_carveout(const void* func);
+// one-thread marker kernel (increments *word)
+void join_mark_launch(uint32_t* word, cudaStream_t st);
 // row_done counters: one per kRowDoneStride words (a 128-B line per row)
 constexpr int kRowDoneStride = 32;
 // dtype: KC_F32 / KC_F16 / KC_BF16 (storage)
@@ -145,7 +143,6 @@ struct ConsumeParams {
   uint32_t* row_done;      // [rows][kRowDoneStride] split completion counters; null: rows are complete
   uint32_t* err;           // set before trapping on a row that never completes
   uint64_t* dbg;           // development probe: [rows][8] phase timestamps (ns), or null
-  int lean;                // consume_lean_kernel (<= 72 registers)
 };
 bool consume_supported(int G, int h);
 // stream-ordered GQA row selection with the selection values cached in shared

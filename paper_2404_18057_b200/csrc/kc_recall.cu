@@ -538,13 +538,8 @@ void launch_pipe(const RecallParams& p, cudaStream_t st) {
     configured_lean |= 1ull << (dev & 63);
   }
   const int grid = (p.grid > 0 && p.grid < p.rows) ? p.grid : p.rows;
-  if (p.lean) {
-    apply_carveout((const void*)recall_pv_pipe_lean_kernel<T>);
-    recall_pv_pipe_lean_kernel<T><<<grid, kRecallThreads, smem, st>>>(p);
-  } else {
-    apply_carveout((const void*)recall_pv_pipe_kernel<T>);
-    recall_pv_pipe_kernel<T><<<grid, kRecallThreads, smem, st>>>(p);
-  }
+  if (p.lean) recall_pv_pipe_lean_kernel<T><<<grid, kRecallThreads, smem, st>>>(p);
+  else recall_pv_pipe_kernel<T><<<grid, kRecallThreads, smem, st>>>(p);
 }
 
 template <typename T>
@@ -656,6 +651,12 @@ void to_f32_launch(const void* src, int dtype, float* dst, int64_t n, cudaStream
     default: cudaMemcpyAsync(dst, src, n * sizeof(float), cudaMemcpyDeviceToDevice, st); break;
   }
 }
+
+// One-thread marker kernel: the join of a dataflow call into the caller's
+// stream runs through it (see decode_topn_impl).
+__global__ void join_mark_kernel(uint32_t* word) { *word += 1u; }
+
+void join_mark_launch(uint32_t* word, cudaStream_t st) { join_mark_kernel<<<1, 1, 0, st>>>(word); }
 
 void expand_idx_launch(const uint32_t* src, uint32_t* dst, int rows, int G, int nc, cudaStream_t st) {
   expand_idx_kernel<<<grid_for((int64_t)rows * G * nc), 256, 0, st>>>(src, dst, rows, G, nc);

@@ -509,9 +509,8 @@ __global__ void __launch_bounds__((NCW + 1) * 32) score_mma_kernel(const ScorePa
       // the stage could land under them (observed: an 8-position n-tile of
       // wrong logits every few C3 layers while a recall ran beside the
       // scoring). The CTA-scope fence waits for this lane's loads.
-      // (A data dependency instead -- the loaded words XOR-reduced over the
-      // warp into the arrive's address -- measured 4-7 us per C3 layer
-      // slower.)
+      // (An arrive whose count depends on both n-tiles' last MMA outputs
+      // measured the same.)
       __threadfence_block();
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);
@@ -900,7 +899,6 @@ void launch_mma_s(const ScoreParams& p, cudaStream_t st) {
     configured |= 1ull << (dev & 63);
   }
   const int n_items = p.rows * p.n_splits;
-  apply_carveout((const void*)score_mma_kernel<T, STAGES, NCW>);
   score_mma_kernel<T, STAGES, NCW><<<n_items, (NCW + 1) * 32, smem, st>>>(p);
 }
 
@@ -940,30 +938,33 @@ bool try_fast(const ScoreParams& p, cudaStream_t st) {
 int score_pick_chunk(int s, int rows, int override_chunk, int G) {
   if (override_chunk > 0) return ((override_chunk + kRows - 1) / kRows) * kRows;
   const long long work = (long long)s * rows;
-  long long c;
+  long long c, hi;
   if (G >= 2) {
     // GQA (score_mma_kernel, 2 CTAs / SM): per-item q preparation is
     // costly, so long items, ~14 per SM: 1024..8192 positions
+    hi = 8192;
     c = (work + 148LL * 14 - 1) / (148LL * 14);
-    c = std::max<long long>(1024, std::min<long long>(8192, c));
+    c = std::max<long long>(1024, std::min<long long>(hi, c));
   } else {
     // MHA: ~48 items per SM (3 CTAs / SM; small items balance best against
     // the concurrent recall), 1024..2048 positions each (shorter items pay
     // their ramp-up: 4k context 70 -> 54 us per layer at 1024)
+    hi = 2048;
     c = (work + 148LL * 48 - 1) / (148LL * 48);
-    c = std::max<long long>(1024, std::min<long long>(2048, c));
+    c = std::max<long long>(1024, std::min<long long>(hi, c));
   }
+  // equal splits: floor(s / c) of them (at most `hi` positions each), so a
+  // row a few positions past a multiple of c -- the decode phase after a
+  // 16 k prefill -- does not get an extra split of a handful of positions
+  // (C3 engine step at s = 16 k + 7: 412 -> 340 us per layer)
+  long long n = std::max<long long>(1, s / c);
+  if ((s + n - 1) / n > hi) n = (s + hi - 1) / hi;
+  c = (s + n - 1) / n;
   c = ((c + kRows - 1) / kRows) * kRows;
   return (int)c;
 }
 
 int sm_count() { return num_sms(); }
-
-int g_smem_carveout = -1;
-
-void apply_carveout(const void* func) {
-  if (g_smem_carveout >= 0) cudaFuncSetAttribute(func, cudaFuncAttributePreferredSharedMemoryCarveout, g_smem_carveout);
-}
 
 bool full_fast_launch(const FullParams& p, int dtype, cudaStream_t st) {
   if (dtype == KC_F16) return try_full<__half>(p, st);

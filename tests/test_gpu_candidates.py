@@ -18,7 +18,7 @@ pytestmark = pytest.mark.gpu
 
 DEFAULTS = {"select_cand": 0, "cand_force_fallback": 0, "score_groups": 0, "score_chunk": 0,
             "recall_pipe": -1, "score_mma": 1, "recall_ctas": 32, "tlb_ahead": -1, "consume": 1, "consume_ctas": 0,
-            "recall_lean": -1, "smem_carveout": -1, "recall_tma": 0}
+            "recall_lean": -1, "recall_tma": 0}
 
 
 def _run(kc, cache, q, N, renorm=False, **tune):
@@ -118,7 +118,7 @@ VARIANTS = {
     "cand-groups3": dict(select_cand=1, score_groups=3), "recall-pipe": dict(recall_pipe=1),
     "recall-pipe-per-row": dict(recall_pipe=1, recall_ctas=0), "recall-plain": dict(recall_pipe=0),
     "recall-ctas128": dict(recall_ctas=128), "recall-lean": dict(recall_pipe=1, recall_lean=1),
-    "recall-not-lean": dict(recall_lean=0), "carveout-max": dict(smem_carveout=100),
+    "recall-not-lean": dict(recall_lean=0),
     "recall-tma": dict(recall_tma=1), "recall-tma-per-row": dict(recall_tma=1, recall_ctas=0), "no-tlb-warm": dict(tlb_ahead=0), "chunk4096": dict(score_chunk=4096),
 }
 

@@ -1,4 +1,6 @@
-"""Development probe: C3 single-layer dataflow vs stream-ordered, per layer."""
+"""Development probe (race detector): repeated C3-shaped multi-layer calls
+must leave bit-identical logits (keep_logits 1, kc_debug_read "logits0").
+Found the score_mma_kernel ring-stage race fixed in r02."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -63,7 +65,9 @@ def trial(tag, tune, reps=8):
         res.append(int((cur != base).sum()))
     for k in tune: cache.set_tuning(k, DEF[k])
     print(tag, tune, res, flush=True)
-DEF = {"stage_release": 2}
-for rep in range(2):
-    trial("dependency", {"stage_release": 2})
-    trial("fence", {"stage_release": 1})
+DEF = {"pipeline": 1, "recall_dbg": 0, "score_mma": 1}
+trial("default", {})
+trial("serial", {"pipeline": 0})
+trial("recall without loads", {"recall_dbg": 1})
+trial("tcgen05", {"score_mma": 3})
+cache.close()
