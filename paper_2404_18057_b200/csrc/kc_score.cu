@@ -940,10 +940,12 @@ int score_pick_chunk(int s, int rows, int override_chunk, int G) {
   const long long work = (long long)s * rows;
   long long c, hi;
   if (G >= 2) {
-    // GQA (score_mma_kernel, 2 CTAs / SM): per-item q preparation is
-    // costly, so long items, ~14 per SM: 1024..8192 positions
+    // GQA (score_mma_kernel, 3 CTAs / SM): ~28 items per SM, 1024..8192
+    // positions (r02, C3: 1024 vs 2048 positions 233 vs 238 us per layer
+    // pipelined, 332 vs 346 in the engine step; 64 k x 64 rows and
+    // 8 k x 512 rows also best at 1024)
     hi = 8192;
-    c = (work + 148LL * 14 - 1) / (148LL * 14);
+    c = (work + 148LL * 28 - 1) / (148LL * 28);
     c = std::max<long long>(1024, std::min<long long>(hi, c));
   } else {
     // MHA: ~48 items per SM (3 CTAs / SM; small items balance best against
