@@ -153,7 +153,8 @@ struct kc_cache {
   // GPU pages, so the recall's scattered 256-B reads do not pay a page walk
   // per 4 KB. KCACHE_V_ARENA=pinned selects the mmap +
   // cudaHostRegister arena (4 KB GPU pages).
-  std::vector<void*> v_managed;  // [layer - L], same pointer on host and device
+  std::vector<void*> v_managed;  // [layer - L - n_pin], same pointer on host and device
+  uint64_t n_pin = 0;             // offloaded layers in the pinned arena (the first ones)
   void* v_host = nullptr;       // pinned arena: mmap'd, registered
   void* v_host_dev = nullptr;   // device alias of v_host
   size_t v_host_bytes = 0;
@@ -330,17 +331,22 @@ struct kc_cache {
     if (layer >= L && layers[layer].stage >= 0) return v_stage[layers[layer].stage].p;
     return v_arena_layer(layer);
   }
+  // Offloaded layers beyond the driver's managed-memory grant live in the
+  // pinned arena -- the FIRST n_pin offloaded layers, so that their slower
+  // recall (GPU page walks, section 5 of DESIGN.md) runs under a later
+  // layer's scoring rather than as a step's exposed last recall.
+  bool layer_managed(uint64_t layer) const { return layer >= L && layer - L >= n_pin; }
   void* v_arena_layer(uint64_t layer) const {
     if (layer < L) return (void*)((char*)v_dev + layer * v_layer_bytes);
     const uint64_t j = layer - L;
-    if (j < v_managed.size()) return v_managed[j];
-    return (void*)((char*)v_host_dev + (j - v_managed.size()) * v_layer_bytes);
+    if (j >= n_pin) return v_managed[j - n_pin];
+    return (void*)((char*)v_host_dev + j * v_layer_bytes);
   }
   // host view of an offloaded layer's V (host gather path)
   const char* v_host_layer(uint64_t layer) const {
     const uint64_t j = layer - L;
-    if (j < v_managed.size()) return static_cast<const char*>(v_managed[j]);
-    return static_cast<const char*>(v_host) + (j - v_managed.size()) * v_layer_bytes;
+    if (j >= n_pin) return static_cast<const char*>(v_managed[j - n_pin]);
+    return static_cast<const char*>(v_host) + j * v_layer_bytes;
   }
   bool v_in_slow(uint64_t layer) const { return layer >= L && layers[layer].offloaded; }
   void check_layer(uint64_t layer) const {
@@ -1198,6 +1204,7 @@ int kc_cache_create(const kc_config* cfg, uint64_t batch, uint64_t resident_laye
         const uint64_t n_off = cfg->n_layers - c->L;
         const char* kind = getenv("KCACHE_V_ARENA");
         const uint64_t m = (kind && !strcmp(kind, "pinned")) ? 0 : alloc_managed_layers(c, n_off, numa_node);
+        c->n_pin = n_off - m;
         if (m < n_off) {
           c->v_host_bytes = checked_mul({c->v_layer_bytes, n_off - m});
           c->v_host = alloc_pinned_arena(c->v_host_bytes, numa_node, &c->v_host_dev);
@@ -1299,7 +1306,7 @@ int kc_offload_prefill_v(kc_cache* c, uint64_t layer) {
       const size_t pitch = (size_t)c->cfg.max_seq * c->h * c->esz;
       CK(cudaStreamWaitEvent(c->off_st, c->ev_staged[slot], 0));
       if (st.len > 0) {
-        if (layer - c->L < c->v_managed.size())
+        if (c->layer_managed(layer))
           kc::copy_rows_launch(c->v_stage[slot].p, c->v_arena_layer(layer), (int64_t)pitch,
                                (int64_t)(st.len * c->h * c->esz), (int)c->rows, c->stage_copy_ctas, c->off_st);
         else
