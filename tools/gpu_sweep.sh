@@ -1,13 +1,9 @@
 mkdir -p gpurun_out
-O=gpurun_out/pinfirst.txt
+O=gpurun_out/c2recall.txt
 : > $O
-for i in 1 2; do
-python bench.py --no-cpu-baseline --no-full-kv > gpurun_out/pf_c2_$i.json 2>gpurun_out/pf_c2_$i.err
-grep '^{' gpurun_out/pf_c2_$i.json | python -c "
-import sys,json
-d=json.loads(sys.stdin.read()); print('c2', round(d['value'],1), round(d['ms_per_step'],3), round(d['e2e']['value'],1), round(d['engine_ms_per_step'],3), d['clocks']['sm_mhz'], d['clocks']['reasons'])" >> $O
-cat gpurun_out/pf_c2_$i.err >> $O
-done
-timeout 2400 python -m pytest tests -m gpu -x -q -p no:cacheprovider > gpurun_out/gpu_all4.log 2>&1
-tail -2 gpurun_out/gpu_all4.log >> $O
+C2="--layers 16 --steps 10"
+timeout 900 python tools/tune_sweep.py $C2 --grid recall_pipe=-1,1 --grid recall_lean=0,1 --grid flow_recall_ctas=16,24 >> $O 2>&1
+timeout 900 python tools/tune_sweep.py $C2 --grid recall_pipe=1 --grid recall_dbg=0,1,2 >> $O 2>&1
+timeout 900 python tools/tune_sweep.py $C2 --grid recall_tma=1 --grid flow_recall_ctas=16,24 >> $O 2>&1
+timeout 900 python tools/tune_sweep.py $C2 --grid pipeline=0 --profile >> $O 2>&1
 cat $O
