@@ -498,6 +498,7 @@ void destroy(kc_cache* c) {
   c->host_out.release();
   for (cudaEvent_t e : c->prof_pool) cudaEventDestroy(e);
   if (c->ev_start) cudaEventDestroy(c->ev_start);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
   if (c->ev_end) cudaEventDestroy(c->ev_end);
   if (c->ev_stats) cudaEventDestroy(c->ev_stats);
   if (c->ev_append) cudaEventDestroy(c->ev_append);
