@@ -217,4 +217,17 @@ def test_full_size_pipelined_layers_equal_single_calls(kc, n_kv):
         for l in range(L):
             for key in ("out", "indices", "weights", "dropped"):
                 assert torch.equal(multi[l][key], again[l][key]), (rep, l, key)
+    # the dataflow consumer forced on every shape (GQA included), multi- and
+    # single-layer calls
+    cache.set_tuning("consume", 2)
+    forced_multi, forced_single = outs(), outs()
+    cache.decode_topn_layers_device(list(range(L)), qs, N, forced_multi, stream=stream)
+    for l in range(L):
+        cache.decode_topn_layers_device([l], [qs[l]], N, [forced_single[l]], stream=stream)
+    cache.set_tuning("consume", 1)
+    torch.cuda.synchronize()
+    for l in range(L):
+        for key in ("out", "indices", "weights", "dropped"):
+            assert torch.equal(multi[l][key], forced_multi[l][key]), ("forced multi", l, key)
+            assert torch.equal(multi[l][key], forced_single[l][key]), ("forced single", l, key)
     cache.close()
