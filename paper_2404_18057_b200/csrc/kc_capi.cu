@@ -783,12 +783,11 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
     // rows and larger N measured faster stream-ordered (r02 C5 sweep: 4 k x
     // N=128 237 vs 224 us per layer, 32 k x N=512 1097 vs 885: > 1024
     // candidates take the consumer's exact path), and inside a step-graph
-    // capture the consumer could only follow its scoring. GQA: single-layer
-    // calls (the engine's layer-by-layer step) of >= 8 k positions -- the
-    // stream-ordered path exposes its last row group's recall there (r02,
-    // 8-layer engine sweeps, 5 shapes: 8 k-64 k positions, 64-512 rows, 9-14 %
-    // faster); multi-layer calls hide the recall under the next layer and
-    // stay stream-ordered (C3 237 vs 267 us per layer)
+    // capture the consumer could only follow its scoring. GQA stays
+    // stream-ordered: multi-layer calls hide the recall under the next layer
+    // (C3 237 vs 267 us per layer), and the single-layer gain (5-11 % in
+    // back-to-back decode calls) turns into a loss whenever the consumer's
+    // CTAs reach the SMs before the scoring's, as in kc_decode_step
     const bool flow_auto = c->G == 1 && g.nc <= 256 && g.s >= 16384 && !c->capture_st;
     const bool flow = (c->consume == 2 || (c->consume == 1 && flow_auto)) &&
                       kc::consume_supported((int)c->G, (int)c->h) && !c->select_global && c->select_cand != 1;
