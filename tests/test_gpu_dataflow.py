@@ -209,3 +209,33 @@ def test_device_calls_order_before_later_calls(kc):
             np.testing.assert_array_equal(o[l]["out"].cpu().numpy(), ref[l].out)
             np.testing.assert_array_equal(o[l]["indices"].cpu().numpy().view(np.uint32), ref[l].selection.indices)
     cache.close()
+
+
+@pytest.mark.parametrize("flow_join", [1, 0])
+def test_device_call_without_selection_outputs(kc, flow_join):
+    """Device-mode GQA dataflow calls that return only the attention output
+    (the caller's stream joins the consumer through the output stream and a
+    marker kernel, flow_join 1, or directly): back-to-back single-layer calls
+    equal the stream-ordered results bit for bit."""
+    import torch
+    b, n, n_kv, h, s, N, L = 2, 8, 2, 128, 3000, 64, 3
+    cache, ks, vs = build_cache(kc, b, n, n_kv, h, s, "f16", n_layers=L)
+    qs = [torch.from_numpy(synth_matrix(60 + l, b, n * h)).cuda() for l in range(L)]
+    stream = torch.cuda.Stream()
+
+    def run(consume):
+        cache.set_tuning("consume", consume)
+        outs = [torch.full((b, n * h), float("nan"), device="cuda") for _ in range(L)]
+        for l in range(L):
+            cache.decode_topn_layers_device([l], [qs[l]], N, [{"out": outs[l]}], stream=stream, want_selection=False)
+        torch.cuda.synchronize()
+        cache.set_tuning("consume", 1)
+        return outs
+
+    cache.set_tuning("flow_join", flow_join)
+    ref = run(0)
+    got = run(2)
+    cache.set_tuning("flow_join", 1)
+    for l in range(L):
+        assert torch.equal(got[l], ref[l]), l
+    cache.close()

@@ -60,3 +60,25 @@ def test_tcgen05_pipelined_layers(kc):
         np.testing.assert_array_equal(outs[l]["out"], singles[l].out)
         np.testing.assert_array_equal(outs[l]["indices"], singles[l].selection.indices)
     cache.close()
+
+
+@pytest.mark.parametrize("tc_grid", [1, 2])
+def test_tcgen05_persistent_grid_bitwise(kc, tc_grid):
+    """The persistent-grid launch of the tcgen05 scoring (tc_grid CTAs per SM
+    walking the items) computes every item with the same instructions: the
+    outputs equal the one-CTA-per-item launch bit for bit."""
+    b, n, n_kv, h, s, N = 4, 16, 4, 128, 9000, 64
+    cache, ks, vs = build_cache(kc, b, n, n_kv, h, s, "f16")
+    q = synth_matrix(5, b, n * h)
+    cache.set_tuning("score_mma", 3)
+    cache.set_tuning("score_chunk", 1024)
+    ref = kc.decode_attention_topn(q, cache, 0, N, False)
+    cache.set_tuning("tc_grid", tc_grid)
+    got = kc.decode_attention_topn(q, cache, 0, N, False)
+    cache.set_tuning("tc_grid", 0)
+    cache.set_tuning("score_mma", 1)
+    cache.set_tuning("score_chunk", 0)
+    np.testing.assert_array_equal(got.out, ref.out)
+    np.testing.assert_array_equal(got.selection.indices, ref.selection.indices)
+    np.testing.assert_array_equal(got.selection.weights, ref.selection.weights)
+    cache.close()
