@@ -194,7 +194,10 @@ struct kc_cache {
   cudaStream_t main_st = nullptr, side_st = nullptr, out_st = nullptr;
   cudaStream_t cons_st = nullptr;  // dataflow with a separate recall: the consumer's stream
   cudaEvent_t ev_join = nullptr;
+  cudaEvent_t ev_ctr = nullptr;  // the dataflow counters' last reset (on the stream that enqueued it)
+  bool ctr_pending = false;      // the next consumer must wait for ev_ctr
   DevBuf join_word;
+  int dbg_ctr_race = 0;  // test hook: stale new dataflow counters and a delayed reset
   int flow_join = 1;  // join dataflow calls through out_st + a marker kernel
   cudaEvent_t ev_start = nullptr, ev_end = nullptr, ev_sel[kRing] = {}, ev_rec[kRing] = {},
               ev_out[kRing] = {}, ev_cp[kRing] = {},
@@ -499,6 +502,7 @@ void destroy(kc_cache* c) {
   for (cudaEvent_t e : c->prof_pool) cudaEventDestroy(e);
   if (c->ev_start) cudaEventDestroy(c->ev_start);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
+  if (c->ev_ctr) cudaEventDestroy(c->ev_ctr);
   if (c->ev_end) cudaEventDestroy(c->ev_end);
   if (c->ev_stats) cudaEventDestroy(c->ev_stats);
   if (c->ev_append) cudaEventDestroy(c->ev_append);
@@ -798,13 +802,28 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
         c->logits_b.ensure(c->logits.bytes);
         c->partials_b.ensure(c->partials.bytes);
       }
+      // counters zeroed on this call (first use, or after an interrupted
+      // call): the consumer, on another stream, must not poll them before
+      // the reset -- it orders after ev_ctr below (a fresh cudaMalloc can hold
+      // any stale value, e.g. one >= n_splits: a consumer that polled it would
+      // take the row as complete and read partials the scoring has not written)
+      bool ctr_reset = false;
+      DevBuf* fresh[2] = {nullptr, nullptr};
+      int n_fresh = 0;
       for (DevBuf* b : {&c->row_done[ls], &c->cons_err}) {
         const size_t want = b == &c->cons_err ? 4 : c->rows * 4 * kc::kRowDoneStride;
         if (b->bytes < want) {
           b->ensure(want);
-          CK(cudaMemsetAsync(b->p, 0, b->bytes, st));
+          if (c->dbg_ctr_race) CK(cudaMemset(b->p, 0xff, b->bytes));  // test hook: stale contents
+          fresh[n_fresh++] = b;
         }
       }
+      if (n_fresh && c->dbg_ctr_race) {  // test hook: ... and a late reset
+        CK(cudaDeviceSynchronize());
+        kc::spin_launch(20000000, st);
+      }
+      for (int k = 0; k < n_fresh; ++k) CK(cudaMemsetAsync(fresh[k]->p, 0, fresh[k]->bytes, st));
+      ctr_reset = n_fresh > 0;
       if (c->cons_dirty) {  // an earlier call threw between a scoring launch and its consumer
         // earlier consumers may still be waiting on the counters: reset after them
         if (side != st) {
@@ -816,6 +835,11 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
         for (int k = 0; k < 2; ++k)
           if (c->row_done[k].p) CK(cudaMemsetAsync(c->row_done[k].p, 0, c->row_done[k].bytes, st));
         c->cons_dirty = false;
+        ctr_reset = true;
+      }
+      if (ctr_reset && !c->capture_st) {
+        CK(cudaEventRecord(c->ev_ctr, st));
+        c->ctr_pending = true;
       }
       if (c->cons_pending[ls]) CK(cudaStreamWaitEvent(st, c->ev_cons[ls], 0));
       c->cons_dirty = true;
@@ -831,6 +855,12 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
       cudaStream_t cs = (own_recall || side == st) ? side : c->cons_st;
       flow_call |= own_recall && cs == side;
       if (cs != st) {
+        // (inside a capture the consumer node follows its scoring node, and
+        // the reset was enqueued before the capture began)
+        if (c->ctr_pending && !c->capture_st) {
+          CK(cudaStreamWaitEvent(cs, c->ev_ctr, 0));
+          c->ctr_pending = false;
+        }
         // ring slot `slot` is rewritten: the output copies of layer i-kRing must be done
         if (i >= (uint64_t)kRing) {
           CK(cudaStreamWaitEvent(cs, c->ev_rec[slot], 0));
@@ -1235,6 +1265,7 @@ int kc_cache_create(const kc_config* cfg, uint64_t batch, uint64_t resident_laye
       CK(cudaEventCreateWithFlags(&c->ev_qall, cudaEventDisableTiming));
       CK(cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming));
       CK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&c->ev_ctr, cudaEventDisableTiming));
       CK(cudaEventCreateWithFlags(&c->ev_end, cudaEventDisableTiming));
       CK(cudaEventCreateWithFlags(&c->ev_stats, cudaEventDisableTiming));
       CK(cudaEventCreateWithFlags(&c->ev_append, cudaEventDisableTiming));
@@ -1444,12 +1475,18 @@ void prepare_step_buffers(kc_cache* c, uint64_t top_n, cudaStream_t st) {
   // dataflow path: both scoring slots, the row counters and the error word
   c->logits_b.ensure(c->logits.bytes);
   c->partials_b.ensure(c->partials.bytes);
+  bool reset = false;
   for (DevBuf* b : {&c->row_done[0], &c->row_done[1], &c->cons_err}) {
     const size_t want = b == &c->cons_err ? 4 : c->rows * 4 * kc::kRowDoneStride;
     if (b->bytes < want) {
       b->ensure(want);
       CK(cudaMemsetAsync(b->p, 0, b->bytes, st));
+      reset = true;
     }
+  }
+  if (reset) {  // a later dataflow consumer orders after this reset (ctr_pending)
+    CK(cudaEventRecord(c->ev_ctr, st));
+    c->ctr_pending = true;
   }
   if (c->L > 0) {  // full attention on the V-resident layers
     c->part_out.ensure(checked_mul({slots, (uint64_t)c->max_splits, c->h, 4}));
@@ -1806,6 +1843,7 @@ int kc_set_tuning(kc_cache* c, const char* key, int64_t value) {
     }
     else if (k == "k_policy") c->k_policy = (int)value;
     else if (k == "tlb_ahead") c->tlb_ahead = (int)value;
+    else if (k == "dbg_ctr_race") c->dbg_ctr_race = value ? 1 : 0;
     else if (k == "flow_join") c->flow_join = value ? 1 : 0;
     else if (k == "recall_tma") c->recall_tma = value ? 1 : 0;
     else if (k == "recall_lean") c->recall_lean = (int)std::max<int64_t>(-1, std::min<int64_t>(1, value));

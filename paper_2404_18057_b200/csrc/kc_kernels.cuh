@@ -53,6 +53,8 @@ struct ScoreParams {
 };
 // one-thread marker kernel (increments *word)
 void join_mark_launch(uint32_t* word, cudaStream_t st);
+// test hook: one thread sleeping ~ns nanoseconds on the stream
+void spin_launch(uint64_t ns, cudaStream_t st);
 // row_done counters: one per kRowDoneStride words (a 128-B line per row)
 constexpr int kRowDoneStride = 32;
 // dtype: KC_F32 / KC_F16 / KC_BF16 (storage)

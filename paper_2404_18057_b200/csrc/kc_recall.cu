@@ -658,6 +658,19 @@ __global__ void join_mark_kernel(uint32_t* word) { *word += 1u; }
 
 void join_mark_launch(uint32_t* word, cudaStream_t st) { join_mark_kernel<<<1, 1, 0, st>>>(word); }
 
+// Test hook: one thread sleeping for ~ns nanoseconds (delays a stream).
+__global__ void spin_kernel(uint64_t ns) {
+  uint64_t t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  do {
+    __nanosleep(1000);
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  } while (t - t0 < ns);
+}
+
+void spin_launch(uint64_t ns, cudaStream_t st) { spin_kernel<<<1, 1, 0, st>>>(ns); }
+
+
 void expand_idx_launch(const uint32_t* src, uint32_t* dst, int rows, int G, int nc, cudaStream_t st) {
   expand_idx_kernel<<<grid_for((int64_t)rows * G * nc), 256, 0, st>>>(src, dst, rows, G, nc);
 }

@@ -239,3 +239,27 @@ def test_device_call_without_selection_outputs(kc, flow_join):
     for l in range(L):
         assert torch.equal(got[l], ref[l]), l
     cache.close()
+
+
+
+def test_consumer_waits_for_counter_reset(kc):
+    """The dataflow counters of a first call are zeroed on the caller's
+    stream; the consumer (another stream) must order after that reset. Test
+    hook dbg_ctr_race: the new counters start as 0xffffffff (a stale
+    allocation) and the reset is delayed by 20 ms -- a consumer that polled
+    them early would take every row as complete and read unwritten partials
+    (seen as rare full-suite failures before the fix: weights off by 1e3
+    with correct indices)."""
+    b, n, h, s, N = 2, 8, 128, 20000, 64  # >= 16 k: the dataflow path
+    cache, ks, vs = build_cache(kc, b, n, n, h, s, "f16")
+    q = synth_matrix(9, b, n * h)
+    ref = _decode(kc, cache, q, N, consume=0)
+    # the consumer kernel loaded already (a first launch can synchronise the
+    # context while the module loads, which would hide the race)
+    _same(_decode(kc, cache, q, N, consume=2), ref)
+    cache.close()
+    cache, ks, vs = build_cache(kc, b, n, n, h, s, "f16")
+    cache.set_tuning("dbg_ctr_race", 1)
+    got = _decode(kc, cache, q, N, consume=2)
+    _same(got, ref)
+    cache.close()
