@@ -56,9 +56,15 @@ def single():
 
 
 ref = None
-for mode, tune, fn in (("multi", {}, multi), ("single", {}, single), ("multi ordered", {"consume": 0}, multi),
-                       ("single ordered", {"consume": 0}, single), ("multi dataflow", {"consume": 2}, multi),
-                       ("single dataflow", {"consume": 2}, single)):
+MODES = (("multi", {}, multi), ("single", {}, single), ("multi ordered", {"consume": 0}, multi),
+         ("single ordered", {"consume": 0}, single), ("multi dataflow", {"consume": 2}, multi),
+         ("single dataflow", {"consume": 2}, single), ("multi tma recall", {"recall_tma": 1}, multi),
+         ("single tma recall ordered", {"recall_tma": 1, "consume": 0}, single))
+if os.environ.get("TC"):  # tcgen05 scoring rounds differently: its own reference
+    MODES = (("multi tcgen05", {"score_mma": 3}, multi), ("single tcgen05", {"score_mma": 3}, single),
+             ("multi tcgen05 persistent", {"score_mma": 3, "tc_grid": 2}, multi))
+DEFAULT = {"consume": 1, "recall_tma": 0, "score_mma": 1, "tc_grid": 0}
+for mode, tune, fn in MODES:
     for k, v in tune.items():
         cache.set_tuning(k, v)
     bad = []
@@ -69,6 +75,6 @@ for mode, tune, fn in (("multi", {}, multi), ("single", {}, single), ("multi ord
         bad.append(sum(int((o[l][key] != ref[l][key]).reshape(o[l][key].shape[0], -1).any(1).sum())
                        for l in range(L) for key in ("out", "indices", "weights", "dropped")))
     for k in tune:
-        cache.set_tuning(k, 1)
+        cache.set_tuning(k, DEFAULT[k])
     print(shape, mode, bad, flush=True)
 cache.close()
