@@ -296,7 +296,9 @@ struct kc_cache {
   // dataflow recall: -1 auto (inside the consumer for single-layer calls, the
   // recall kernel on the side stream for multi-layer calls), 1 / 0 force
   int consume_recall = -1;
-  int flow_recall_ctas = 24;  // recall grid beside the select-only consumer (C2: 24 326 us, 32 334 us per layer)  // stream-ordered GQA: one-row CTAs with cached selection values
+  // recall grid beside the select-only consumer (C2, unthrottled: 24 326 us,
+  // 32 334 us per layer; under sw_power_cap 20 334 us vs 24 339, 16 345)
+  int flow_recall_ctas = 20;
   int consume_dbg = 0;    // development probe: consumer phase timestamps (kc_debug_read "consume")
   DevBuf cons_dbg;
   // per-kernel CUDA-event timing (kc_profile): [kind] -> (start, stop) pairs
