@@ -111,3 +111,27 @@ def test_host_side_validation_matches_reference_errors():
     assert fp["fast_bytes"] + fp["slow_bytes"] == 137438953472
     assert kc.attention_score_scale(128) == float(np.float32(1) / np.sqrt(np.float32(128)))
     assert kc.ModelConfig.default_ffn_hidden(4096) == 10928  # ceil(8d/3) to a multiple of 16
+
+
+def test_split_plan_is_balanced():
+    """kc_score_chunk_plan (host-side, no GPU): splits are 64-position
+    multiples of bounded length that cover the row, and a row a few positions
+    past a multiple of the target (the decode phase after a 16 k prefill)
+    keeps the same number of splits instead of gaining an extra one of a
+    handful of positions (C3 at 16 k + 7: 17 splits before r02's plan)."""
+    from paper_2404_18057_b200 import kcache as kc
+    for rows, g, hi in ((256, 1, 2048), (256, 4, 8192), (64, 4, 8192), (8, 1, 2048), (512, 4, 8192)):
+        for s in (100, 1000, 4096, 4100, 16384, 16391, 16448, 32768, 32775, 65536, 131072, 131100):
+            c = kc.score_chunk_plan(s, rows, g)
+            n = (s + c - 1) // c
+            assert c % 64 == 0 and 64 <= c <= max(hi, 64 * ((s + 63) // 64)), (s, rows, g, c)
+            assert (n - 1) * c < s <= n * c
+        for base in (4096, 16384, 32768, 131072):
+            c0 = kc.score_chunk_plan(base, rows, g)
+            if c0 >= hi:  # splits at the length cap: one more position needs one more split
+                continue
+            for extra in (1, 7, 40):
+                c1 = kc.score_chunk_plan(base + extra, rows, g)
+                assert (base + extra + c1 - 1) // c1 == (base + c0 - 1) // c0, (base, extra, rows, g, c0, c1)
+    assert kc.score_chunk_plan(16384, 256, 4) == 1024  # C3: ~28 GQA items per SM
+    assert kc.score_chunk_plan(32768, 256, 1) == 1216  # C2
