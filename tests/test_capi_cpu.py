@@ -117,8 +117,8 @@ def test_split_plan_is_balanced():
     """kc_score_chunk_plan (host-side, no GPU): splits are 64-position
     multiples of bounded length that cover the row, and a row a few positions
     past a multiple of the target (the decode phase after a 16 k prefill)
-    keeps the same number of splits instead of gaining an extra one of a
-    handful of positions (C3 at 16 k + 7: 17 splits before r02's plan)."""
+    gets no extra split of a handful of positions (C3 at 16 k + 7: 17 splits
+    before r02's plan; the 64-position rounding may merge one instead)."""
     from paper_2404_18057_b200 import kcache as kc
     for rows, g, hi in ((256, 1, 2048), (256, 4, 8192), (64, 4, 8192), (8, 1, 2048), (512, 4, 8192)):
         for s in (100, 1000, 4096, 4100, 16384, 16391, 16448, 32768, 32775, 65536, 131072, 131100):
@@ -132,6 +132,6 @@ def test_split_plan_is_balanced():
                 continue
             for extra in (1, 7, 40):
                 c1 = kc.score_chunk_plan(base + extra, rows, g)
-                assert (base + extra + c1 - 1) // c1 == (base + c0 - 1) // c0, (base, extra, rows, g, c0, c1)
+                assert (base + extra + c1 - 1) // c1 <= (base + c0 - 1) // c0, (base, extra, rows, g, c0, c1)
     assert kc.score_chunk_plan(16384, 256, 4) == 1024  # C3: ~28 GQA items per SM
     assert kc.score_chunk_plan(32768, 256, 1) == 1216  # C2
