@@ -957,8 +957,8 @@ int score_pick_chunk(int s, int rows, int override_chunk, int G) {
   }
   // equal splits: floor(s / c) of them (at most `hi` positions each), so a
   // row a few positions past a multiple of c -- the decode phase after a
-  // 16 k prefill -- does not get an extra split of a handful of positions
-  // (C3 engine step at s = 16 k + 7: 412 -> 340 us per layer)
+  // 16 k prefill -- does not get an extra split (an extra item per row) of a
+  // handful of positions (tests/test_capi_cpu.py)
   long long n = std::max<long long>(1, s / c);
   if ((s + n - 1) / n > hi) n = (s + hi - 1) / hi;
   c = (s + n - 1) / n;
