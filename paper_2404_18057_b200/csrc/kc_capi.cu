@@ -296,9 +296,12 @@ struct kc_cache {
   // dataflow recall: -1 auto (inside the consumer for single-layer calls, the
   // recall kernel on the side stream for multi-layer calls), 1 / 0 force
   int consume_recall = -1;
-  // recall grid beside the select-only consumer (C2, unthrottled: 24 326 us,
-  // 32 334 us per layer; under sw_power_cap 20 334 us vs 24 339, 16 345)
-  int flow_recall_ctas = 20;
+  // recall grid beside the select-only consumer; 0 = auto: 20 CTAs for calls
+  // of >= 8 layers whose recall is short next to the scoring (nc * 256 <= s:
+  // C2 under sw_power_cap 334 vs 339 us per layer with 24, 345 with 16),
+  // else 24 (the call's last recall is exposed, or the recall is the longer
+  // stream: C5 4-layer calls at 16 k / 32 k x N=256 475 / 515 vs 516 / 558)
+  int flow_recall_ctas = 0;
   int consume_dbg = 0;    // development probe: consumer phase timestamps (kc_debug_read "consume")
   DevBuf cons_dbg;
   // per-kernel CUDA-event timing (kc_profile): [kind] -> (start, stop) pairs
@@ -919,7 +922,8 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
         if (side != cs) CK(cudaStreamWaitEvent(side, c->ev_sel[slot], 0));
         kc::RecallParams rp{};
         rp.v = c->v_layer(layer);
-        rp.grid = c->flow_recall_ctas;
+        rp.grid = c->flow_recall_ctas > 0 ? c->flow_recall_ctas
+                  : (n >= 8 && (int64_t)g.nc * 256 <= (int64_t)g.s) ? 20 : 24;
         rp.pipelined = c->recall_pipe < 0 ? (c->G > 1 ? 1 : 0) : c->recall_pipe;
         rp.dbg = c->recall_dbg;
         rp.lean = c->recall_lean > 0 ? 1 : 0;
@@ -1864,7 +1868,7 @@ int kc_set_tuning(kc_cache* c, const char* key, int64_t value) {
     else if (k == "select_cached") c->select_cached = value ? 1 : 0;
     else if (k == "consume_recall") c->consume_recall = value < 0 ? -1 : (value ? 1 : 0);
     else if (k == "flow_recall_ctas") {
-      if (value < 0) fail(KC_EARG, "flow_recall_ctas must be >= 0 (0 = one CTA per row)");
+      if (value < 0) fail(KC_EARG, "flow_recall_ctas must be >= 0 (0 = auto)");
       c->flow_recall_ctas = (int)value;
     }
     else if (k == "consume_ctas") {
