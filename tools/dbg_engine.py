@@ -7,7 +7,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2404_18057_b200 import kcache as kc
 
-b, n, h, s, N, L, n_kv = 32, 32, 128, 16384, 128, 8, 8
+b, n, h, s, N, L, n_kv = int(os.environ.get('B', 32)), 32, 128, int(os.environ.get('S', 16384)), 128, 8, 8
 cfg = kc.small_config(L, n * h, n, s + int(os.environ.get('EXTRA', '64')), kv_heads=n_kv)
 cache = kc.TieredKVCache(cfg, b, kc.TierPlacement.kcache(0, L, 2, "f16"))
 kb = torch.empty(s * b, n_kv * h, dtype=torch.float16, device="cuda")
@@ -87,8 +87,9 @@ def app_topn16():
 def step32():
     for l in range(L):
         cache.decode_step_device(l, q32[l], kv16[l][0].float(), kv16[l][1].float(), out, N, stream=stream)
-for cons in (0, 2, 0, 2):
-    cache.set_tuning("consume", cons)
+cache.set_tuning("consume", 2)
+for ctas in [int(x) for x in os.environ.get('CTAS', '48,56,64,72,80').split(',')]:
+    cache.set_tuning("consume_ctas", ctas)
     r = [round(t(f, reps=2), 1) for f in (app_topn, app_topn16, step)]
-    print("consume", cons, "append+topn(q32) / append+topn(q16) / decode_step, us per layer", r, flush=True)
+    print("consume 2 ctas", ctas, "append+topn(q32) / append+topn(q16) / decode_step, us per layer", r, flush=True)
 cache.close()
