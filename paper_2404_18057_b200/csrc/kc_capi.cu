@@ -909,13 +909,14 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
         c->cons_dbg.ensure(c->rows * 8 * sizeof(uint64_t));
         cp.dbg = c->cons_dbg.as<uint64_t>();
       }
-      // auto grid: MHA 40 recalling / 32 selecting only; GQA 64 up to 32 k
+      // auto grid: MHA 44 recalling (r02 final, kc_decode_step at C2: 401-404
+      // us per layer vs 410-412 at 40, 404 at 48) / 32 selecting only; GQA 64 up to 32 k
       // positions, 48 beyond (r02 kc_decode_step sweeps, us per layer: 32 x
       // 16 k 368 at 64 CTAs vs 387-477 at 72-96 and ~440 stream-ordered; 16 x
       // 32 k 328-349 at 48-64; 8 x 64 k 339-343 at 32-48)
       const int ctas = c->consume_ctas > 0 ? c->consume_ctas
                        : c->G > 1 ? (g.s <= 32768 ? 64 : 48)
-                                  : (own_recall ? 40 : 32);
+                                  : (own_recall ? 44 : 32);
       c->timed(1, cs, [&] { kc::consume_launch(cp, c->dtype, ctas, cs); });
       c->cons_dirty = false;
       ++c->cons_seq;

@@ -7,7 +7,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2404_18057_b200 import kcache as kc
 
-b, n, h, s, N, L, n_kv = int(os.environ.get('B', 32)), 32, 128, int(os.environ.get('S', 16384)), 128, 8, 8
+b, n, h, s, N, L, n_kv = int(os.environ.get('B', 32)), 32, 128, int(os.environ.get('S', 16384)), 128, 8, int(os.environ.get('KV', 8))
 cfg = kc.small_config(L, n * h, n, s + int(os.environ.get('EXTRA', '64')), kv_heads=n_kv)
 cache = kc.TieredKVCache(cfg, b, kc.TierPlacement.kcache(0, L, 2, "f16"))
 kb = torch.empty(s * b, n_kv * h, dtype=torch.float16, device="cuda")
