@@ -155,3 +155,49 @@ def test_step_graph_rejects_host_io(kc):
     cache.step_graph_launch(stream)  # ends the (empty) capture
     stream.synchronize()
     cache.close()
+
+
+def test_gqa_engine_step_dataflow_equals_stream_ordered(kc):
+    """kc_decode_step on a GQA cache in the dataflow consumer's range (16 k
+    positions, 64 rows: the auto policy's single-layer dataflow with its
+    small grid) equals the stream-ordered step bit for bit, layer after layer
+    with the append and fp16 q of an engine step."""
+    import torch
+    b, n, n_kv, h, s, N, L, steps = 8, 32, 8, 128, 16384, 128, 2, 3
+    cfg = kc.small_config(L, n * h, n, s + 16, kv_heads=n_kv)
+    outs = {}
+    for consume in (0, 1):
+        cache = kc.TieredKVCache(cfg, b, kc.TierPlacement.kcache(0, L, 2, "f16"))
+        kb = torch.empty(s * b, n_kv * h, dtype=torch.float16, device="cuda")
+        vb = torch.empty_like(kb)
+        for l in range(L):
+            kc.fill_uniform(kb, 2 + 100 * l)
+            kc.fill_uniform(vb, 3 + 100 * l)
+            cache.append_kv_device(l, kb, vb)
+        torch.cuda.synchronize()
+        del kb, vb
+        for l in range(L):
+            cache.offload_prefill_v(l)
+        cache.begin_decode()
+        cache.set_tuning("consume", consume)
+        stream = torch.cuda.Stream()
+        # every step's inputs stay alive until the stream is done with them
+        # (the calls are asynchronous on `stream`)
+        ins = []
+        for t in range(steps):
+            for l in range(L):
+                q = torch.empty(b, n * h, dtype=torch.float16, device="cuda")
+                kv = torch.empty(2, b, n_kv * h, dtype=torch.float16, device="cuda")
+                kc.fill_uniform(q, 500 + 10 * t + l)
+                kc.fill_uniform(kv, 700 + 10 * t + l)
+                ins.append((l, q, kv, torch.empty(b, n * h, device="cuda")))
+        torch.cuda.synchronize()
+        res = []
+        for l, q, kv, out in ins:
+            cache.decode_step_device(l, q, kv[0], kv[1], out, N, stream=stream)
+            res.append(out)
+        torch.cuda.synchronize()
+        outs[consume] = [r.cpu() for r in res]
+        cache.close()
+    diffs = [float((a - c).abs().max()) for a, c in zip(outs[0], outs[1])]
+    assert all(d == 0.0 for d in diffs), diffs
