@@ -1,5 +1,8 @@
+"""Development probe: what the end-to-end leg (host q in, host outputs back)
+adds per output on a C3-shaped cache, 8-layer calls.
+    python tools/e2e_probe.py"""
 import os, sys, time, json
-sys.path.insert(0, '/root/repo')
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch, numpy as np
 from paper_2404_18057_b200 import kcache as kc
 b, n, h, s, N, L, n_kv = 32, 32, 128, 16384, 128, 8, 8
