@@ -792,16 +792,13 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
     // rows and larger N measured faster stream-ordered (r02 C5 sweep: 4 k x
     // N=128 237 vs 224 us per layer, 32 k x N=512 1097 vs 885: > 1024
     // candidates take the consumer's exact path), and inside a step-graph
-    // capture the consumer could only follow its scoring. GQA: single-layer
-    // calls (the engine's layer-by-layer step) of 16 k-64 k positions and
-    // >= 64 rows, with a consumer grid small enough that its CTAs never wait
-    // for SM room (a larger grid slows the scoring ~3.5x when its
-    // CTAs reach the SMs first, as behind kc_decode_step's append and q
-    // conversion); multi-layer GQA calls hide the recall under the next layer
-    // and stay stream-ordered (C3 237 vs 267 us per layer)
-    const bool flow_auto = g.nc <= 256 && !c->capture_st &&
-                           ((c->G == 1 && g.s >= 16384) ||
-                            (c->G > 1 && n == 1 && g.s >= 16384 && g.s <= 65536 && c->rows >= 64));
+    // capture the consumer could only follow its scoring. GQA stays
+    // stream-ordered: multi-layer calls hide the recall under the next layer
+    // (C3 237 vs 267 us per layer); single-layer calls gain with a small
+    // consumer grid on some boxes and lose on others (C3 engine step 11.78 vs
+    // 13.43 ms, and 14.10 vs 13.58 ms: the consumer's CTAs reaching the SMs
+    // before the scoring's) -- consume 2 opts in
+    const bool flow_auto = c->G == 1 && g.nc <= 256 && g.s >= 16384 && !c->capture_st;
     const bool flow = (c->consume == 2 || (c->consume == 1 && flow_auto)) &&
                       kc::consume_supported((int)c->G, (int)c->h) && !c->select_global && c->select_cand != 1;
     if (flow) {
@@ -910,12 +907,14 @@ void decode_topn_impl(kc_cache* c, uint64_t n, const uint64_t* layers, const voi
         cp.dbg = c->cons_dbg.as<uint64_t>();
       }
       // auto grid: MHA 44 recalling (r02 final, kc_decode_step at C2: 401-404
-      // us per layer vs 410-412 at 40, 404 at 48) / 32 selecting only; GQA 64 up to 32 k
-      // positions, 48 beyond (r02 kc_decode_step sweeps, us per layer: 32 x
-      // 16 k 368 at 64 CTAs vs 387-477 at 72-96 and ~440 stream-ordered; 16 x
-      // 32 k 328-349 at 48-64; 8 x 64 k 339-343 at 32-48)
+      // us per layer vs 410-412 at 40, 404 at 48) / 32 selecting only; GQA 64
+      // at <= 16 k positions, 48 beyond, at most one per row (r02
+      // kc_decode_step sweeps, us per layer: 32 x 16 k 368 at 64 CTAs vs
+      // 387-477 at 72-96 and ~440 stream-ordered; 16 x 32 k 328 at 48, 349 at
+      // 64; 8 x 64 k 339-343 at 32-48; 4 x 128 k 367 at 32 vs 464
+      // stream-ordered)
       const int ctas = c->consume_ctas > 0 ? c->consume_ctas
-                       : c->G > 1 ? (g.s <= 32768 ? 64 : 48)
+                       : c->G > 1 ? std::min(rows_i, g.s <= 16384 ? 64 : 48)
                                   : (own_recall ? 44 : 32);
       c->timed(1, cs, [&] { kc::consume_launch(cp, c->dtype, ctas, cs); });
       c->cons_dirty = false;

@@ -158,15 +158,15 @@ def test_step_graph_rejects_host_io(kc):
 
 
 def test_gqa_engine_step_dataflow_equals_stream_ordered(kc):
-    """kc_decode_step on a GQA cache in the dataflow consumer's range (16 k
-    positions, 64 rows: the auto policy's single-layer dataflow with its
-    small grid) equals the stream-ordered step bit for bit, layer after layer
-    with the append and fp16 q of an engine step."""
+    """kc_decode_step on a GQA cache through the dataflow consumer (consume 2,
+    16 k positions, 64 rows, its small auto grid) equals the stream-ordered
+    step bit for bit, layer after layer with the append and fp16 q of an
+    engine step."""
     import torch
     b, n, n_kv, h, s, N, L, steps = 8, 32, 8, 128, 16384, 128, 2, 3
     cfg = kc.small_config(L, n * h, n, s + 16, kv_heads=n_kv)
     outs = {}
-    for consume in (0, 1):
+    for consume in (0, 2):
         cache = kc.TieredKVCache(cfg, b, kc.TierPlacement.kcache(0, L, 2, "f16"))
         kb = torch.empty(s * b, n_kv * h, dtype=torch.float16, device="cuda")
         vb = torch.empty_like(kb)
@@ -199,5 +199,5 @@ def test_gqa_engine_step_dataflow_equals_stream_ordered(kc):
         torch.cuda.synchronize()
         outs[consume] = [r.cpu() for r in res]
         cache.close()
-    diffs = [float((a - c).abs().max()) for a, c in zip(outs[0], outs[1])]
+    diffs = [float((a - c).abs().max()) for a, c in zip(outs[0], outs[2])]
     assert all(d == 0.0 for d in diffs), diffs

@@ -87,8 +87,11 @@ def app_topn16():
 def step32():
     for l in range(L):
         cache.decode_step_device(l, q32[l], kv16[l][0].float(), kv16[l][1].float(), out, N, stream=stream)
+cache.set_tuning("consume", 0)
+r = [round(t(f, reps=2), 1) for f in (app_topn, app_topn16, step)]
+print("stream-ordered", r, flush=True)
 cache.set_tuning("consume", 2)
-for ctas in [int(x) for x in os.environ.get('CTAS', '48,56,64,72,80').split(',')]:
+for ctas in [int(x) for x in os.environ.get('CTAS', '0').split(',')]:
     cache.set_tuning("consume_ctas", ctas)
     r = [round(t(f, reps=2), 1) for f in (app_topn, app_topn16, step)]
     print("consume 2 ctas", ctas, "append+topn(q32) / append+topn(q16) / decode_step, us per layer", r, flush=True)
